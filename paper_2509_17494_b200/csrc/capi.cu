@@ -1,0 +1,461 @@
+// capi.cu -- the extern "C" boundary (include/helmtg_b200.h) and the handle.
+//
+// The handle is the GPU-resident counterpart of helmtg::TwoGridOperators
+// (proj/core/include/helmtg/twogrid.hpp:92-105): everything two_grid_step
+// consumes is built once on the host and uploaded to HBM; every call after
+// that is a sequence of stream-ordered kernel launches with no allocation.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "coarse.hpp"
+#include "common.hpp"
+#include "helmtg_b200.h"
+#include "kernels.hpp"
+#include "setup.hpp"
+
+namespace htg {
+long long launch_count();
+void reset_launch_count();
+DDDevice upload_dd_impl(const DDSetup& dd, const HostProblem& hp, std::vector<void*>& allocs, size_t& bytes,
+                        cudaStream_t st, double2*& ystage);
+}  // namespace htg
+
+using namespace htg;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return HTG_OK;
+    } catch (const InvalidArgument& e) {
+        g_err = e.what();
+        return HTG_ERR_INVALID;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return HTG_ERR_INVALID;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return HTG_ERR_RUNTIME;
+    }
+}
+
+struct DevArena {
+    std::vector<void*> ptrs;
+    size_t bytes = 0;
+    template <class T>
+    T* alloc(size_t n) {
+        void* p = nullptr;
+        if (n == 0) n = 1;
+        HTG_CUDA(cudaMalloc(&p, n * sizeof(T)));
+        ptrs.push_back(p);
+        bytes += n * sizeof(T);
+        return static_cast<T*>(p);
+    }
+    template <class T>
+    T* upload(const std::vector<T>& v, cudaStream_t st) {
+        T* p = alloc<T>(v.size());
+        if (!v.empty()) HTG_CUDA(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+        return p;
+    }
+    ~DevArena() {
+        for (void* p : ptrs) cudaFree(p);
+    }
+};
+
+std::once_flag g_tables_once;
+void upload_tables_once() {
+    std::call_once(g_tables_once, [] {
+        for (int p = 2; p <= kMaxP; p += 2) {
+            Basis1D b = make_basis(p);
+            upload_basis_tables(&b.M[0][0], &b.S[0][0], &b.E[0][0], p / 2 - 1);
+        }
+    });
+}
+
+}  // namespace
+
+struct htg_handle {
+    HostProblem hp;
+    Basis1D basis;
+    htg_config cfg{};
+    cudaStream_t st = nullptr;
+    bool own_stream = false;
+    DevArena mem;
+    FineGeom g{};
+    double4* qtab = nullptr;
+    long long ndof = 0, cndof = 0;
+    // scratch
+    double2 *r = nullptr, *v = nullptr, *rc = nullptr, *uc = nullptr, *ystage = nullptr, *tmp = nullptr;
+    double2 *fio = nullptr, *uio = nullptr;  // host-API staging
+    double* partial = nullptr;
+    double* dscal = nullptr;  // device scalars
+    int npart = 0;
+    // subdomain solver
+    DDDevice dd{};
+    int nclasses = 0;
+    // coarse solver
+    std::unique_ptr<CoarseSolver> coarse;
+    // pinned host scalars
+    double* hscal = nullptr;
+    ~htg_handle() {
+        coarse.reset();
+        if (hscal) cudaFreeHost(hscal);
+        if (own_stream && st) cudaStreamDestroy(st);
+    }
+};
+
+namespace {
+
+void build_handle(htg_handle* H, const htg_problem& prob, const htg_config& cfg) {
+    upload_tables_once();
+    H->hp = make_problem(prob);
+    validate_config(cfg, H->hp);
+    H->cfg = cfg;
+    H->basis = make_basis(H->hp.p);
+    const HostProblem& hp = H->hp;
+    cudaStream_t st = H->st;
+    DevArena& M = H->mem;
+    H->ndof = hp.ndof();
+    const int m = hp.p / 2;
+    H->cndof = (long long)(hp.nx * m + 1) * (hp.ny * m + 1);
+
+    // coefficient tables
+    const int ncls = int(hp.cls_k.size());
+    std::vector<double2> m0(ncls), ms(ncls);
+    std::vector<double4> q(ncls);
+    const double h2 = hp.h * hp.h, hc = 2.0 * hp.h / hp.p;
+    for (int c = 0; c < ncls; ++c) {
+        const double k = hp.cls_k[c], e = hp.cls_eps[c];
+        m0[c] = make_double2(k * k * h2, e * h2);
+        ms[c] = make_double2(k * k * h2, (k * k * cfg.alpha_s + e) * h2);
+        if (cfg.coarsening == HTG_COARSE_OPTIMIZED_FD) {
+            const QsfemWeights w = qsfem_weights(hc * k);
+            q[c] = make_double4(w.q0, w.q1, w.q2, e * hc * hc);
+        }
+    }
+    FineGeom& g = H->g;
+    g.nx = hp.nx;
+    g.ny = hp.ny;
+    g.p = hp.p;
+    g.ndof = H->ndof;
+    g.cls = hp.uniform ? nullptr : M.upload(hp.cls, st);
+    g.mtab0 = M.upload(m0, st);
+    g.mtabS = M.upload(ms, st);
+    g.kh_b = M.upload(hp.khb, st);
+    g.kh_t = M.upload(hp.kht, st);
+    g.kh_l = M.upload(hp.khl, st);
+    g.kh_r = M.upload(hp.khr, st);
+    g.tg_b = M.upload(hp.tb, st);
+    g.tg_t = M.upload(hp.tt, st);
+    g.tg_l = M.upload(hp.tl, st);
+    g.tg_r = M.upload(hp.tr, st);
+    g.has_dirichlet = hp.has_dirichlet ? 1 : 0;
+    H->qtab = M.upload(q, st);
+
+    // scratch
+    H->r = M.alloc<double2>(H->ndof);
+    H->v = M.alloc<double2>(H->ndof);
+    H->tmp = M.alloc<double2>(H->ndof);
+    H->fio = M.alloc<double2>(H->ndof);
+    H->uio = M.alloc<double2>(H->ndof);
+    H->rc = M.alloc<double2>(H->cndof);
+    H->uc = M.alloc<double2>(H->cndof);
+    H->npart = std::max(k1_partials(g, 0), 148 * 8 * 2);
+    H->partial = M.alloc<double>(H->npart);
+    H->dscal = M.alloc<double>(64);
+    HTG_CUDA(cudaMallocHost(&H->hscal, 64 * sizeof(double)));
+
+    if (cfg.smoother == HTG_SMOOTHER_CSDD) {
+        DDSetup dd = build_dd(hp, H->basis, cfg.alpha_s, cfg.l_dd);
+        H->nclasses = int(dd.classes.size());
+        H->dd = upload_dd_impl(dd, hp, M.ptrs, M.bytes, st, H->ystage);
+    }
+    if (cfg.coarsening == HTG_COARSE_OPTIMIZED_FD) H->coarse = make_coarse_solver(hp, st);
+    HTG_CUDA(cudaStreamSynchronize(st));
+}
+
+K1Args k1args(htg_handle* H, const double2* f, const double2* u, int shifted) {
+    K1Args a{};
+    a.g = H->g;
+    a.u = u;
+    a.f = f;
+    a.rows = 0;
+    a.shifted = shifted;
+    a.partial = H->partial;
+    return a;
+}
+
+void residual(htg_handle* H, const double2* f, const double2* u, double2* r, int shifted) {
+    K1Args a = k1args(H, f, u, shifted);
+    a.r = r;
+    k1_launch(kK1Write, a, H->st);
+}
+
+// ||f - A u||^2 into H->dscal[slot] (device)
+void residual_norm2(htg_handle* H, const double2* f, const double2* u, int slot) {
+    K1Args a = k1args(H, f, u, 0);
+    const int n = k1_launch(kK1Norm, a, H->st);
+    reduce_partials(H->partial, n, H->dscal + slot, H->st);
+}
+
+void residual_restrict(htg_handle* H, const double2* f, const double2* u, double2* rc) {
+    K1Args a = k1args(H, f, u, 0);
+    a.rc = rc;
+    k1_launch(kK1Restrict, a, H->st);
+}
+
+// out = dd_step(u, f): g = f - A_s u (skipped when u is null, i.e. zero)
+void dd_step(htg_handle* H, const double2* u, const double2* f, double2* out) {
+    const double2* gvec = f;
+    if (u) {
+        residual(H, f, u, H->tmp, 1);
+        gvec = H->tmp;
+    }
+    dd_gemm_launch(H->g, H->dd, gvec, H->ystage, H->st);
+    dd_combine_launch(H->g, H->dd, H->ystage, u, out, H->st);
+}
+
+// csdd_smoother (twogrid.cpp:114-120): r = f - A u; v = 0; n_dd x v = dd_step(v, r); u += v
+void csdd(htg_handle* H, double2* u, const double2* f) {
+    residual(H, f, u, H->r, 0);
+    if (H->cfg.n_dd == 1) {
+        // v = dd_step(0, r) and u += v fused into the combine
+        dd_gemm_launch(H->g, H->dd, H->r, H->ystage, H->st);
+        dd_combine_launch(H->g, H->dd, H->ystage, u, u, H->st);
+        return;
+    }
+    dd_step(H, nullptr, H->r, H->v);
+    for (int i = 1; i < H->cfg.n_dd; ++i) dd_step(H, H->v, H->r, H->v);
+    vec_axpy(u, H->v, 1.0, H->ndof, H->st);
+}
+
+void two_grid_step(htg_handle* H, double2* u, const double2* f) {
+    for (int i = 0; i < H->cfg.n_s; ++i) csdd(H, u, f);
+    if (H->cfg.coarsening != HTG_COARSE_NONE) {
+        residual_restrict(H, f, u, H->rc);
+        H->coarse->solve(H->rc, H->uc, H->st);
+        prolong_add_launch(H->g, u, H->uc, H->cfg.omega_c, H->st);
+    }
+    for (int i = 0; i < H->cfg.n_s; ++i) csdd(H, u, f);
+}
+
+double host_norm2(htg_handle* H, int slot) {
+    HTG_CUDA(cudaMemcpyAsync(H->hscal, H->dscal + slot, sizeof(double), cudaMemcpyDeviceToHost, H->st));
+    HTG_CUDA(cudaStreamSynchronize(H->st));
+    return H->hscal[0];
+}
+
+int gmres_solve(htg_handle* H, const double2* f, double2* u, double nf, double* hist, int cap, int* iters, int* conv);
+
+int solve(htg_handle* H, const double2* f, double2* u, double* hist, int cap, int* iters, int* conv) {
+    vec_zero(u, H->ndof, H->st);
+    // ||f||
+    vec_dot(f, f, H->ndof, H->partial, reinterpret_cast<double2*>(H->dscal + 8), H->st);
+    const double nf = std::sqrt(host_norm2(H, 8));
+    *iters = 0;
+    *conv = 1;
+    if (nf == 0.0) return HTG_OK;
+    if (H->cfg.outer == HTG_OUTER_RICHARDSON) {
+        for (int it = 1; it <= H->cfg.max_iters; ++it) {
+            two_grid_step(H, u, f);
+            residual_norm2(H, f, u, 0);
+            const double rr = std::sqrt(host_norm2(H, 0)) / nf;
+            if (it - 1 < cap) hist[it - 1] = rr;
+            *iters = it;
+            if (rr <= H->cfg.stop_rel_residual) return HTG_OK;
+        }
+        *conv = 0;
+        return HTG_NOT_CONVERGED;
+    }
+    return gmres_solve(H, f, u, nf, hist, cap, iters, conv);
+}
+
+int gmres_solve(htg_handle* H, const double2* f, double2* u, double nf, double* hist, int cap, int* iters,
+                int* conv) {
+    (void)H, (void)f, (void)u, (void)nf, (void)hist, (void)cap, (void)iters, (void)conv;
+    throw InvalidArgument("outer = krylov: GMRES not implemented on the GPU yet");
+}
+
+}  // namespace
+
+// ====================================================================== C-ABI
+extern "C" {
+
+void htg_config_default(htg_config* c) {
+    c->alpha_s = 0.2;
+    c->alpha_c = 0.0;
+    c->n_s = 1;
+    c->n_dd = 1;
+    c->omega_c = 1.0;
+    c->l_dd = 4;
+    c->coarsening = HTG_COARSE_OPTIMIZED_FD;
+    c->smoother = HTG_SMOOTHER_CSDD;
+    c->outer = HTG_OUTER_RICHARDSON;
+    c->stop_rel_residual = 1e-6;
+    c->max_iters = 200;
+}
+
+const char* htg_last_error(void) { return g_err.c_str(); }
+
+int htg_create(const htg_problem* prob, const htg_config* cfg, void* stream, htg_handle** out) {
+    return guard([&] {
+        if (!prob || !out) throw InvalidArgument("null argument");
+        htg_config c;
+        if (cfg)
+            c = *cfg;
+        else
+            htg_config_default(&c);
+        auto H = std::make_unique<htg_handle>();
+        H->st = static_cast<cudaStream_t>(stream);  // NULL: the legacy default stream
+        build_handle(H.get(), *prob, c);
+        *out = H.release();
+    });
+}
+
+int htg_destroy(htg_handle* h) {
+    return guard([&] {
+        if (h) {
+            cudaStreamSynchronize(h->st);
+            delete h;
+        }
+    });
+}
+
+int htg_info(const htg_handle* h, long long* out) {
+    return guard([&] {
+        out[0] = h->ndof;
+        out[1] = h->cndof;
+        out[2] = h->dd.nsub;
+        out[3] = h->nclasses;
+        out[4] = (long long)h->mem.bytes + (h->coarse ? h->coarse->device_bytes() : 0);
+        out[5] = h->coarse ? h->coarse->device_bytes() : 0;
+        out[6] = h->hp.nx;
+        out[7] = h->hp.ny;
+        out[8] = h->hp.p;
+    });
+}
+
+int htg_set_stream(htg_handle* h, void* stream) {
+    return guard([&] {
+        if (h->own_stream) cudaStreamDestroy(h->st);
+        h->own_stream = false;
+        h->st = static_cast<cudaStream_t>(stream);
+    });
+}
+
+#define D2(p) reinterpret_cast<double2*>(p)
+#define CD2(p) reinterpret_cast<const double2*>(p)
+
+int htg_residual(htg_handle* h, const double* f, const double* u, double* r, int shifted) {
+    return guard([&] { residual(h, CD2(f), CD2(u), D2(r), shifted ? 1 : 0); });
+}
+
+int htg_residual_norm(htg_handle* h, const double* f, const double* u, double* out) {
+    return guard([&] {
+        residual_norm2(h, CD2(f), CD2(u), 0);
+        *out = std::sqrt(host_norm2(h, 0));
+    });
+}
+
+int htg_dd_step(htg_handle* h, const double* u, const double* f, double* out) {
+    return guard([&] {
+        if (!h->dd.nsub) throw InvalidArgument("handle has no CSDD smoother");
+        dd_step(h, CD2(u), CD2(f), D2(out));
+    });
+}
+
+int htg_csdd_smoother(htg_handle* h, double* u, const double* f) {
+    return guard([&] {
+        if (!h->dd.nsub) throw InvalidArgument("handle has no CSDD smoother");
+        csdd(h, D2(u), CD2(f));
+    });
+}
+
+int htg_restrict(htg_handle* h, const double* r, double* rc) {
+    return guard([&] {
+        // IP^H r = restriction of the residual f - A u with u = 0, f = r
+        vec_zero(h->tmp, h->ndof, h->st);
+        residual_restrict(h, CD2(r), h->tmp, D2(rc));
+    });
+}
+
+int htg_residual_restrict(htg_handle* h, const double* f, const double* u, double* rc) {
+    return guard([&] { residual_restrict(h, CD2(f), CD2(u), D2(rc)); });
+}
+
+int htg_prolong_add(htg_handle* h, double* u, const double* uc, double omega) {
+    return guard([&] { prolong_add_launch(h->g, D2(u), CD2(uc), omega, h->st); });
+}
+
+int htg_coarse_apply(htg_handle* h, const double* x, double* y) {
+    return guard([&] { coarse_apply_launch(h->g, h->qtab, 0.0, CD2(x), D2(y), h->st); });
+}
+
+int htg_coarse_solve(htg_handle* h, const double* rc, double* uc) {
+    return guard([&] {
+        if (!h->coarse) throw InvalidArgument("handle has no coarse level");
+        h->coarse->solve(CD2(rc), D2(uc), h->st);
+    });
+}
+
+int htg_two_grid_step(htg_handle* h, double* u, const double* f) {
+    return guard([&] { two_grid_step(h, D2(u), CD2(f)); });
+}
+
+int htg_solve(htg_handle* h, const double* f, double* u, double* history, int hist_cap, int* iterations,
+              int* converged) {
+    int rc = HTG_OK;
+    const int g = guard([&] { rc = solve(h, CD2(f), D2(u), history, hist_cap, iterations, converged); });
+    return g != HTG_OK ? g : rc;
+}
+
+int htg_solve_host(htg_handle* h, const double* f_host, double* u_host, double* history, int hist_cap,
+                   int* iterations, int* converged) {
+    int rc = HTG_OK;
+    const int g = guard([&] {
+        const size_t nb = size_t(h->ndof) * sizeof(double2);
+        HTG_CUDA(cudaMemcpyAsync(h->fio, f_host, nb, cudaMemcpyHostToDevice, h->st));
+        rc = solve(h, h->fio, h->uio, history, hist_cap, iterations, converged);
+        HTG_CUDA(cudaMemcpyAsync(u_host, h->uio, nb, cudaMemcpyDeviceToHost, h->st));
+        HTG_CUDA(cudaStreamSynchronize(h->st));
+    });
+    return g != HTG_OK ? g : rc;
+}
+
+int htg_two_grid_step_host(htg_handle* h, double* u_host, const double* f_host) {
+    return guard([&] {
+        const size_t nb = size_t(h->ndof) * sizeof(double2);
+        HTG_CUDA(cudaMemcpyAsync(h->fio, f_host, nb, cudaMemcpyHostToDevice, h->st));
+        HTG_CUDA(cudaMemcpyAsync(h->uio, u_host, nb, cudaMemcpyHostToDevice, h->st));
+        two_grid_step(h, h->uio, h->fio);
+        HTG_CUDA(cudaMemcpyAsync(u_host, h->uio, nb, cudaMemcpyDeviceToHost, h->st));
+        HTG_CUDA(cudaStreamSynchronize(h->st));
+    });
+}
+
+int htg_csdd_smoother_host(htg_handle* h, double* u_host, const double* f_host) {
+    return guard([&] {
+        if (!h->dd.nsub) throw InvalidArgument("handle has no CSDD smoother");
+        const size_t nb = size_t(h->ndof) * sizeof(double2);
+        HTG_CUDA(cudaMemcpyAsync(h->fio, f_host, nb, cudaMemcpyHostToDevice, h->st));
+        HTG_CUDA(cudaMemcpyAsync(h->uio, u_host, nb, cudaMemcpyHostToDevice, h->st));
+        csdd(h, h->uio, h->fio);
+        HTG_CUDA(cudaMemcpyAsync(u_host, h->uio, nb, cudaMemcpyDeviceToHost, h->st));
+        HTG_CUDA(cudaStreamSynchronize(h->st));
+    });
+}
+
+long long htg_launch_count(void) { return launch_count(); }
+void htg_reset_launch_count(void) { reset_launch_count(); }
+
+}  // extern "C"

@@ -1,0 +1,399 @@
+// k_dd.cu -- K2: the CSDD smoother's subdomain solves as one batched
+// complex-fp64 GEMM on the FP64 tensor cores, plus the partition-of-unity combine.
+//
+// Reference: dd_step (proj/core/src/twogrid.cpp:92-112) gathers g on every
+// Omega_i, runs one SparseLU solve per subdomain and averages the U-parts
+// with 1/L_j. Subdomains with identical local operators share one factor; the
+// host precomputes per class B_c = (A_s^(i))^-1[Dofs(U_i), :], so a sweep is
+//   Y_c (|U| x N_c) = B_c (|U| x |Omega|) * G_c (|Omega| x N_c)
+// where column s of G_c is the gathered residual of subdomain s. Each CTA
+// computes a 64 x 64 tile of Y with mma.sync.m8n8k4.f64 (DMMA), the complex
+// product as 4 real products; the gather is fused into the cp.async producer.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "common.hpp"
+#include "kernels.hpp"
+#include "setup.hpp"
+
+namespace htg {
+
+namespace {
+
+constexpr int kTM = 64, kTN = 64, kKC = 8, kLD = kKC + 4, kStages = 4, kThreads = 128;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    const int sz = pred ? 16 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+struct GemmSmem {
+    double2 A[kStages][kTM][kLD];
+    double2 B[kStages][kTN][kLD];
+};
+
+template <int P>
+__global__ void __launch_bounds__(kThreads) k_dd_gemm(FineGeom g, DDDevice d, const double2* __restrict__ r,
+                                                      double2* __restrict__ ystage) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    GemmSmem& sm = *reinterpret_cast<GemmSmem*>(smem_raw);
+    const int4 tile = d.tiles[blockIdx.x];
+    const int c = tile.x, m0 = tile.y, n0 = tile.z;
+    const int* ci = d.cls_info + 8 * c;
+    const int nu = ci[3], kpad = ci[4], boff = ci[5], loff = ci[6], ncol = ci[7];
+    const int sub0 = tile.w;  // offset of this class's subdomain list
+    const double2* Bc = d.Bmat + (size_t)boff;
+    const int* locg = d.loc_g + loff;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp >> 1, wn = warp & 1;
+
+    // producer assignment: A: rows tid/2, 4 k each; B: col tid/2, 4 k each
+    const int prow = tid >> 1, pk = (tid & 1) * 4;
+    const double2* arow = Bc + (size_t)(m0 + prow) * kpad;
+    const int col = n0 + prow;
+    const bool colok = col < ncol;
+    int ox = 0, oy = 0;
+    if (colok) {
+        const int so = d.sub_o[d.class_subs[sub0 + col]];
+        ox = (so & 0xffff) * P;
+        oy = (so >> 16) * P;
+    }
+    const int nkc = kpad / kKC;
+
+    auto load_stage = [&](int stage, int kc) {
+        const int k0 = kc * kKC + pk;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) cp_async16(&sm.A[stage][prow][pk + i], arow + k0 + i, true);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int lg = locg[k0 + i];
+            const bool ok = colok && lg >= 0;
+            const double2* src = r;
+            if (ok) src = r + dof_index(g.nx, g.ny, P, ox + (lg & 0xffff), oy + (lg >> 16));
+            cp_async16(&sm.B[stage][prow][pk + i], src, ok);
+        }
+    };
+
+    double cr[4][4][2], cim[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            cr[a][b][0] = cr[a][b][1] = 0.0;
+            cim[a][b][0] = cim[a][b][1] = 0.0;
+        }
+
+#pragma unroll
+    for (int s = 0; s < kStages - 1; ++s) {
+        if (s < nkc) load_stage(s, s);
+        cp_commit();
+    }
+    for (int kc = 0; kc < nkc; ++kc) {
+        cp_wait<kStages - 2>();
+        __syncthreads();
+        const int stage = kc % kStages;
+#pragma unroll
+        for (int ks = 0; ks < kKC / 4; ++ks) {
+            const int kk = ks * 4 + (lane & 3);
+            double2 af[4], bf[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                af[t] = sm.A[stage][wm * 32 + t * 8 + (lane >> 2)][kk];
+                bf[t] = sm.B[stage][wn * 32 + t * 8 + (lane >> 2)][kk];
+            }
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) {
+                const double ar = af[mt].x, ai = af[mt].y, nai = -af[mt].y;
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) {
+                    dmma(cr[mt][nt][0], cr[mt][nt][1], ar, bf[nt].x);
+                    dmma(cr[mt][nt][0], cr[mt][nt][1], nai, bf[nt].y);
+                    dmma(cim[mt][nt][0], cim[mt][nt][1], ar, bf[nt].y);
+                    dmma(cim[mt][nt][0], cim[mt][nt][1], ai, bf[nt].x);
+                }
+            }
+        }
+        const int nxt = kc + kStages - 1;
+        if (nxt < nkc) load_stage(nxt % kStages, nxt);
+        cp_commit();
+    }
+    cp_wait<0>();
+    // epilogue: C[row][col], row = lane/4, col = 2 (lane%4) + i
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+        const int row = m0 + wm * 32 + mt * 8 + (lane >> 2);
+        if (row >= nu) continue;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int cc = n0 + wn * 32 + nt * 8 + 2 * (lane & 3) + i;
+                if (cc >= ncol) continue;
+                const int s = d.class_subs[sub0 + cc];
+                ystage[(size_t)s * d.nu_max + row] = make_double2(cr[mt][nt][i], cim[mt][nt][i]);
+            }
+    }
+}
+
+// out = u + (sum over U-memberships of Y) / L, summed in subdomain order
+template <int P>
+__global__ void k_dd_combine(FineGeom g, DDDevice d, const double2* __restrict__ ystage, const double2* u,
+                             double2* out) {
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const int pp = P * P;
+    const long long cellid = t / pp;
+    const int pos = int(t - cellid * pp);
+    const int x = int(cellid % (g.nx + 1)), y = int(cellid / (g.nx + 1));
+    if (y > g.ny) return;
+    int jx, jy;
+    const bool rx = x == g.nx, ty = y == g.ny;
+    if (rx && ty) {
+        if (pos) return;
+        jx = jy = 0;
+    } else if (rx) {  // vertex + v-edge
+        if (pos >= P) return;
+        jx = 0;
+        jy = pos;
+    } else if (ty) {  // vertex + h-edge
+        if (pos >= P) return;
+        jx = pos;
+        jy = 0;
+    } else if (pos == 0) {
+        jx = jy = 0;
+    } else if (pos < P) {
+        jx = pos;
+        jy = 0;
+    } else if (pos < 2 * P - 1) {
+        jx = 0;
+        jy = pos - P + 1;
+    } else {
+        const int q = pos - (2 * P - 1);
+        jx = q / (P - 1) + 1;
+        jy = q % (P - 1) + 1;
+    }
+    const int gx = x * P + jx, gy = y * P + jy;
+    const int l = d.l_dd;
+    int bxs[2], bys[2], nbxs = 0, nbys = 0;
+    {
+        const int c0 = jx ? x : x - 1, c1 = min(x, g.nx - 1);
+        for (int cc = max(c0, 0); cc <= c1; ++cc) {
+            const int b = cc / l;
+            if (nbxs == 0 || bxs[nbxs - 1] != b) bxs[nbxs++] = b;
+        }
+    }
+    {
+        const int c0 = jy ? y : y - 1, c1 = min(y, g.ny - 1);
+        for (int cc = max(c0, 0); cc <= c1; ++cc) {
+            const int b = cc / l;
+            if (nbys == 0 || bys[nbys - 1] != b) bys[nbys++] = b;
+        }
+    }
+    double2 acc = make_double2(0.0, 0.0);
+    for (int iy = 0; iy < nbys; ++iy)
+        for (int ix = 0; ix < nbxs; ++ix) {
+            const int s = bys[iy] * d.nbx + bxs[ix];
+            const int c = d.sub_class[s];
+            const int* ci = d.cls_info + 8 * c;
+            const int so = d.sub_o[s];
+            const int lgx = gx - (so & 0xffff) * P, lgy = gy - (so >> 16) * P;
+            const int li = int(dof_index(ci[0], ci[1], P, lgx, lgy));
+            const int row = d.rowmap[ci[6] + li];
+            const double2 yv = ystage[(size_t)s * d.nu_max + row];
+            acc.x += yv.x;
+            acc.y += yv.y;
+        }
+    const double inv = 1.0 / double(nbxs * nbys);
+    const long long di = dof_index(g.nx, g.ny, P, gx, gy);
+    double2 base = u ? u[di] : make_double2(0.0, 0.0);
+    out[di] = make_double2(base.x + acc.x * inv, base.y + acc.y * inv);
+}
+
+}  // namespace
+
+void dd_gemm_launch(const FineGeom& g, const DDDevice& d, const double2* r, double2* ystage, cudaStream_t st) {
+    const size_t smem = sizeof(GemmSmem);
+    static bool attr[9] = {};
+    auto go = [&](auto kern, int p) {
+        if (!attr[p]) {
+            HTG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            attr[p] = true;
+        }
+        kern<<<d.ntiles, kThreads, smem, st>>>(g, d, r, ystage);
+    };
+    switch (g.p) {
+        case 2: go(k_dd_gemm<2>, 2); break;
+        case 4: go(k_dd_gemm<4>, 4); break;
+        case 6: go(k_dd_gemm<6>, 6); break;
+        default: go(k_dd_gemm<8>, 8); break;
+    }
+    HTG_CUDA(cudaGetLastError());
+    count_launch();
+}
+
+void dd_combine_launch(const FineGeom& g, const DDDevice& d, const double2* ystage, const double2* u, double2* out,
+                       cudaStream_t st) {
+    const long long n = (long long)(g.nx + 1) * (g.ny + 1) * g.p * g.p;
+    const unsigned nb = unsigned((n + 255) / 256);
+    switch (g.p) {
+        case 2: k_dd_combine<2><<<nb, 256, 0, st>>>(g, d, ystage, u, out); break;
+        case 4: k_dd_combine<4><<<nb, 256, 0, st>>>(g, d, ystage, u, out); break;
+        case 6: k_dd_combine<6><<<nb, 256, 0, st>>>(g, d, ystage, u, out); break;
+        default: k_dd_combine<8><<<nb, 256, 0, st>>>(g, d, ystage, u, out); break;
+    }
+    HTG_CUDA(cudaGetLastError());
+    count_launch();
+}
+
+// Host: lay the classes out for the kernels (padded B_c, local gather tables,
+// U-row maps, tile list) and upload.
+DDDevice upload_dd_impl(const DDSetup& dd, const HostProblem& hp, std::vector<void*>& allocs, size_t& bytes,
+                        cudaStream_t st, double2*& ystage) {
+    DDDevice d;
+    const int nc = int(dd.classes.size());
+    d.nclass = nc;
+    d.nbx = dd.nbx;
+    d.nby = dd.nby;
+    d.nsub = dd.nbx * dd.nby;
+    d.l_dd = dd.l_dd;
+    const int p = hp.p;
+    std::vector<int> info(8 * nc), locg, rowmap, class_subs;
+    std::vector<double2> Bm;
+    std::vector<int4> tiles;
+    std::vector<std::vector<int>> subs(nc);
+    for (int s = 0; s < d.nsub; ++s) subs[dd.sub_class[s]].push_back(s);
+    int nu_max = 0;
+    for (int ci = 0; ci < nc; ++ci) {
+        const DDClass& c = dd.classes[ci];
+        const int kpad = (c.nloc + kKC - 1) / kKC * kKC;
+        const int rpad = (c.nu + kTM - 1) / kTM * kTM;
+        nu_max = std::max(nu_max, c.nu);
+        int* in = &info[8 * ci];
+        in[0] = c.onx;
+        in[1] = c.ony;
+        in[2] = c.nloc;
+        in[3] = c.nu;
+        in[4] = kpad;
+        in[5] = int(Bm.size());
+        in[6] = int(locg.size());
+        in[7] = int(subs[ci].size());
+        const size_t b0 = Bm.size();
+        Bm.resize(b0 + size_t(rpad) * kpad, make_double2(0.0, 0.0));
+        for (int rI = 0; rI < c.nu; ++rI)
+            for (int l = 0; l < c.nloc; ++l) {
+                const cplx v = c.B[size_t(rI) * c.nloc + l];
+                Bm[b0 + size_t(rI) * kpad + l] = make_double2(v.real(), v.imag());
+            }
+        // local dof -> (lgx, lgy), and local dof -> U row
+        std::vector<int> lg(kpad, -1), rm(kpad, -1);
+        for (int gy = 0; gy <= c.ony * p; ++gy)
+            for (int gx = 0; gx <= c.onx * p; ++gx) lg[dof_index(c.onx, c.ony, p, gx, gy)] = gx | (gy << 16);
+        for (int rI = 0; rI < c.nu; ++rI) rm[c.umem[rI]] = rI;
+        locg.insert(locg.end(), lg.begin(), lg.end());
+        rowmap.insert(rowmap.end(), rm.begin(), rm.end());
+        const int off = int(class_subs.size());
+        class_subs.insert(class_subs.end(), subs[ci].begin(), subs[ci].end());
+        for (int m0 = 0; m0 < c.nu; m0 += kTM)
+            for (int n0 = 0; n0 < int(subs[ci].size()); n0 += kTN) tiles.push_back(make_int4(ci, m0, n0, off));
+    }
+    // big classes first
+    std::stable_sort(tiles.begin(), tiles.end(), [&](const int4& a, const int4& b) {
+        return info[8 * a.x + 4] * 1.0 > info[8 * b.x + 4] * 1.0;
+    });
+    std::vector<int> sub_o(d.nsub);
+    for (int s = 0; s < d.nsub; ++s) sub_o[s] = dd.sub_ox[s] | (dd.sub_oy[s] << 16);
+    auto up = [&](const auto& v) {
+        using T = typename std::decay_t<decltype(v)>::value_type;
+        void* ptr = nullptr;
+        HTG_CUDA(cudaMalloc(&ptr, std::max<size_t>(1, v.size()) * sizeof(T)));
+        allocs.push_back(ptr);
+        bytes += v.size() * sizeof(T);
+        if (!v.empty()) HTG_CUDA(cudaMemcpyAsync(ptr, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+        return static_cast<const T*>(ptr);
+    };
+    d.cls_info = up(info);
+    d.Bmat = up(Bm);
+    d.loc_g = up(locg);
+    d.rowmap = up(rowmap);
+    d.sub_class = up(dd.sub_class);
+    d.sub_o = up(sub_o);
+    d.tiles = up(tiles);
+    d.class_subs = up(class_subs);
+    d.ntiles = int(tiles.size());
+    d.nu_max = nu_max;
+    void* ys = nullptr;
+    const size_t ysz = size_t(d.nsub) * nu_max * sizeof(double2);
+    HTG_CUDA(cudaMalloc(&ys, std::max<size_t>(ysz, 16)));
+    allocs.push_back(ys);
+    bytes += ysz;
+    ystage = static_cast<double2*>(ys);
+    return d;
+}
+
+}  // namespace htg
+
+// ------------------------------------------------------------------ FP64 tensor peak
+namespace htg {
+namespace {
+__global__ void k_dmma_peak(double* out, int iters) {
+    double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+    double c[8][2];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) c[t][0] = c[t][1] = 0.0;
+    for (int i = 0; i < iters; ++i)
+#pragma unroll
+        for (int t = 0; t < 8; ++t) dmma(c[t][0], c[t][1], a, b);
+    double s = 0.0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) s += c[t][0] + c[t][1];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+}  // namespace
+}  // namespace htg
+
+extern "C" int htg_measure_fp64_tensor_peak(double* tflops) {
+    using namespace htg;
+    try {
+        int sms = 0;
+        HTG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+        const int blocks = sms * 2, threads = 512, iters = 4096;
+        double* out = nullptr;
+        HTG_CUDA(cudaMalloc(&out, sizeof(double) * blocks * threads));
+        cudaEvent_t e0, e1;
+        HTG_CUDA(cudaEventCreate(&e0));
+        HTG_CUDA(cudaEventCreate(&e1));
+        k_dmma_peak<<<blocks, threads>>>(out, 64);
+        float best = 1e30f;
+        for (int rep = 0; rep < 3; ++rep) {
+            HTG_CUDA(cudaEventRecord(e0));
+            k_dmma_peak<<<blocks, threads>>>(out, iters);
+            HTG_CUDA(cudaEventRecord(e1));
+            HTG_CUDA(cudaEventSynchronize(e1));
+            float ms = 0.f;
+            HTG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+            best = std::min(best, ms);
+        }
+        count_launch(4);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaFree(out);
+        const double flops = double(blocks) * (threads / 32) * iters * 8 * 512.0;
+        *tflops = flops / (best * 1e-3) / 1e12;
+        return 0;
+    } catch (const std::exception& e) {
+        return 1;
+    }
+}

@@ -1,0 +1,666 @@
+// k_fine.cu -- K1 (matrix-free residual, + fused restriction / norm), K3b
+// (prolongation), K4 (QSFEM coarse stencil) and small vector kernels.
+//
+// K1 restates r = f - A u of proj/core/src/twogrid.cpp:116,272,287 where A is
+// the assembled FE Helmholtz matrix of proj/core/src/fespace.cpp:181-210. The
+// square-element matrices are tensor products of the 1-D factors M, S
+// (K_e = S(x)M + M(x)S, M_e = M(x)M), so per cell row the apply is sum-factorised:
+//   T = Z M, V = Z S            (contract the y index of the cell-row slab Z)
+//   O[a] = sum_c S[a][c] T[c] + M[a][c] (V[c] - m_cell T[c])   (contract x)
+// A CTA owns a strip of cells in x and marches upward over cell rows; the
+// top-edge (b = 1) contributions of a cell row are carried in registers into
+// the next lattice row, so every u and f value is read once from HBM.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+
+#include "common.hpp"
+#include "kernels.hpp"
+
+namespace htg {
+
+__constant__ double c_M[4][kMaxP + 1][kMaxP + 1];
+__constant__ double c_S[4][kMaxP + 1][kMaxP + 1];
+__constant__ double c_E[4][kMaxP + 1][kMaxP / 2 + 1];
+
+void upload_basis_tables(const double* M, const double* S, const double* E, int slot) {
+    HTG_CUDA(cudaMemcpyToSymbol(c_M, M, sizeof(double) * (kMaxP + 1) * (kMaxP + 1),
+                                sizeof(double) * (kMaxP + 1) * (kMaxP + 1) * slot));
+    HTG_CUDA(cudaMemcpyToSymbol(c_S, S, sizeof(double) * (kMaxP + 1) * (kMaxP + 1),
+                                sizeof(double) * (kMaxP + 1) * (kMaxP + 1) * slot));
+    HTG_CUDA(cudaMemcpyToSymbol(c_E, E, sizeof(double) * (kMaxP + 1) * (kMaxP / 2 + 1),
+                                sizeof(double) * (kMaxP + 1) * (kMaxP / 2 + 1) * slot));
+}
+
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 rmul(double s, double2 a) { return make_double2(s * a.x, s * a.y); }
+__device__ __forceinline__ double2 rfma(double s, double2 a, double2 c) {
+    return make_double2(fma(s, a.x, c.x), fma(s, a.y, c.y));
+}
+// (-i kh) z
+__device__ __forceinline__ double2 mik(double kh, double2 z) { return make_double2(kh * z.y, -kh * z.x); }
+
+template <int P>
+__device__ __forceinline__ long long dofp(int nx, int ny, int gx, int gy) {
+    return dof_index(nx, ny, P, gx, gy);
+}
+
+// A fine dof (gx, gy) is constrained iff it lies in the closure of a Dirichlet
+// boundary edge (proj/core/src/fespace.cpp:146-153).
+template <int P>
+__device__ bool fine_dir(const FineGeom& g, int gx, int gy) {
+    const int NGx = g.nx * P, NGy = g.ny * P;
+    const bool L = gx == 0, R = gx == NGx, Bm = gy == 0, T = gy == NGy;
+    if (!(L || R || Bm || T)) return false;
+    if (L || R) {
+        const int8_t* tg = L ? g.tg_l : g.tg_r;
+        const int y = gy / P, jy = gy - y * P;
+        if (jy) {
+            if (tg[y] == kDirichlet) return true;
+        } else if ((y > 0 && tg[y - 1] == kDirichlet) || (y < g.ny && tg[y] == kDirichlet)) {
+            return true;
+        }
+    }
+    if (Bm || T) {
+        const int8_t* tg = Bm ? g.tg_b : g.tg_t;
+        const int x = gx / P, jx = gx - x * P;
+        if (jx) {
+            if (tg[x] == kDirichlet) return true;
+        } else if ((x > 0 && tg[x - 1] == kDirichlet) || (x < g.nx && tg[x] == kDirichlet)) {
+            return true;
+        }
+    }
+    return false;
+}
+
+// Coarse vertex (X, Y), m = p/2: coarse boundary edges inherit the tag of the
+// fine edge they subdivide (proj/core/src/twogrid.cpp:140-148).
+__device__ bool coarse_dir(const FineGeom& g, int m, int X, int Y) {
+    const int CX = g.nx * m, CY = g.ny * m;
+    const bool L = X == 0, R = X == CX, Bm = Y == 0, T = Y == CY;
+    if (!(L || R || Bm || T)) return false;
+    if (L || R) {
+        const int8_t* tg = L ? g.tg_l : g.tg_r;
+        if ((Y > 0 && tg[(Y - 1) / m] == kDirichlet) || (Y < CY && tg[Y / m] == kDirichlet)) return true;
+    }
+    if (Bm || T) {
+        const int8_t* tg = Bm ? g.tg_b : g.tg_t;
+        if ((X > 0 && tg[(X - 1) / m] == kDirichlet) || (X < CX && tg[X / m] == kDirichlet)) return true;
+    }
+    return false;
+}
+
+template <int P>
+__device__ __forceinline__ int lidx(int xc, int a) {
+    return a == 0 ? xc * P : (a == 1 ? (xc + 1) * P : xc * P + a - 1);
+}
+
+// ---------------------------------------------------------------- K1
+constexpr int kK1Threads = 128;
+
+template <int P>
+struct K1Smem {
+    static constexpr int B = P + 1, MM = P / 2;
+    double2 T[kK1Threads][B];
+    double2 Va[kK1Threads][B];  // V - m(cell right of / containing gx) T
+    double2 Vb[kK1Threads][B];  // V - m(cell left of vertex gx) T
+    double2 Z[kK1Threads][2];
+    double2 Rt[kK1Threads][MM];
+    double M[B][B], S[B][B], E[B][MM + 1];
+    double red[kK1Threads / 32];
+};
+
+template <int P, int MODE>
+__global__ void __launch_bounds__(kK1Threads) k1_residual(K1Args a) {
+    constexpr int B = P + 1, MM = P / 2, W = (kK1Threads - 1 - P) / P;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    K1Smem<P>& sm = *reinterpret_cast<K1Smem<P>*>(smem_raw);
+    const FineGeom& g = a.g;
+    const int tid = threadIdx.x;
+    for (int i = tid; i < B * B; i += kK1Threads) {
+        sm.M[i / B][i % B] = c_M[P / 2 - 1][i / B][i % B];
+        sm.S[i / B][i % B] = c_S[P / 2 - 1][i / B][i % B];
+    }
+    for (int i = tid; i < B * (MM + 1); i += kK1Threads) sm.E[i / (MM + 1)][i % (MM + 1)] = c_E[P / 2 - 1][i / (MM + 1)][i % (MM + 1)];
+    __syncthreads();
+
+    const int nx = g.nx, ny = g.ny, NG = nx * P + 1;
+    const int x0 = blockIdx.x * W;
+    const int G0 = max(x0 * P - P, 0);
+    const int gx = G0 + tid;
+    const int gend = min((x0 + W) * P + 1, NG);
+    const bool valid = gx < gend;
+    const int own_lo = x0 * P, own_hi = (x0 + W >= nx) ? NG : (x0 + W) * P;
+    const bool owned = valid && gx >= own_lo && gx < own_hi;
+    const int x = gx / P, j = gx - x * P;
+    const bool halo_bubble = valid && !owned && j > 0 && x == x0 - 1;
+    const bool emit = owned || (MODE == kK1Restrict && halo_bubble);
+    const int ys = blockIdx.y * a.rows, ye = min(ys + a.rows, ny);
+    const int nhalo = MODE == kK1Restrict ? 2 : 1;
+    const int ystart = max(ys - nhalo, 0);
+    const double2* mt = a.shifted ? g.mtabS : g.mtab0;
+    auto coef = [&](int xc, int y) -> double2 { return mt[g.cls ? g.cls[(size_t)y * nx + xc] : 0]; };
+    const double2 zero = make_double2(0.0, 0.0);
+
+    // coarse x-contraction bookkeeping (restriction)
+    const int cX0 = x0 * MM;
+    const int cXend = (x0 + W >= nx) ? nx * MM + 1 : (x0 + W) * MM;
+
+    double2 zraw0 = valid ? a.u[dofp<P>(nx, ny, gx, ystart * P)] : zero;
+    double2 carryO = zero, sprev = zero;
+    double acc = 0.0;
+
+    auto add_cell = [&](int xc, int al, int y, double2* O) {
+        // contributions of cell (xc, y), gx acting as local x-index al
+        for (int cl = 0; cl <= P; ++cl) {
+            const double s = sm.S[al][cl], mm = sm.M[al][cl];
+            if (s == 0.0 && mm == 0.0) continue;
+            const int li = lidx<P>(xc, cl) - G0;
+            const double2* T = sm.T[li];
+            const double2* V = (cl == 1) ? sm.Vb[li] : sm.Va[li];
+#pragma unroll
+            for (int bp = 0; bp < B; ++bp) O[bp] = rfma(mm, V[bp], rfma(s, T[bp], O[bp]));
+        }
+        (void)y;
+    };
+    auto horiz_robin = [&](int xc, int al, double kh, int zb, double2& out) {
+        double2 s = zero;
+        for (int cl = 0; cl <= P; ++cl) {
+            const double mm = sm.M[al][cl];
+            if (mm != 0.0) s = rfma(mm, sm.Z[lidx<P>(xc, cl) - G0][zb], s);
+        }
+        out = cadd(out, mik(kh, s));
+    };
+
+    // emit one lattice row of residual values r[jy], jy < nj
+    auto finish_row = [&](int y, int nj, const double2* Au_in, const double2* uraw, double2* rr) {
+        for (int jy = 0; jy < nj; ++jy) {
+            const int gy = y * P + jy;
+            double2 Au = Au_in[jy];
+            if (g.has_dirichlet && fine_dir<P>(g, gx, gy)) Au = uraw[jy];
+            const double2 fv = a.f[dofp<P>(nx, ny, gx, gy)];
+            rr[jy] = csub(fv, Au);
+        }
+    };
+
+    // restriction of one lattice row: rows Y = y*MM + i, i < nrow (1 at the top)
+    auto restrict_row = [&](int y, int nj, const double2* rr, bool write) {
+        // y-contraction for this gx
+        double2 t[MM];
+        double2 snext = zero;
+#pragma unroll
+        for (int i = 0; i < MM; ++i) t[i] = zero;
+        if (emit) {
+            for (int jy = 0; jy < nj; ++jy) {
+                const int gy = y * P + jy;
+                double2 rv = rr[jy];
+                if (g.has_dirichlet && fine_dir<P>(g, gx, gy)) rv = zero;  // zero IP rows
+                if (jy == 0) {
+                    t[0] = cadd(t[0], rv);
+                } else if (jy + 1 <= MM) {
+#pragma unroll
+                    for (int i = 0; i < MM; ++i) t[i] = rfma(sm.E[jy + 1][i], rv, t[i]);
+                    snext = rfma(sm.E[jy + 1][MM], rv, snext);
+                }
+            }
+            t[0] = cadd(t[0], sprev);
+        }
+        sprev = snext;
+        if (!write) return;
+#pragma unroll
+        for (int i = 0; i < MM; ++i) sm.Rt[tid][i] = t[i];
+        __syncthreads();
+        const int ncx = cXend - cX0;
+        const int nrow = (nj == 1 && y == ny) ? 1 : MM;
+        for (int w = tid; w < ncx * nrow; w += kK1Threads) {
+            const int X = cX0 + (w % ncx), i = w / ncx, Y = y * MM + i;
+            const int xc = X / MM, ip = X - xc * MM;
+            double2 s = zero;
+            if (ip == 0) {
+                if (xc * P - G0 >= 0) s = sm.Rt[xc * P - G0][i];  // vertex xc
+                if (xc < nx)
+                    for (int d = 2; d <= MM; ++d) s = rfma(sm.E[d][0], sm.Rt[xc * P + d - 1 - G0][i], s);
+                if (xc > 0)
+                    for (int d = 2; d <= MM; ++d) s = rfma(sm.E[d][MM], sm.Rt[(xc - 1) * P + d - 1 - G0][i], s);
+            } else {
+                for (int d = 2; d <= MM; ++d) s = rfma(sm.E[d][ip], sm.Rt[xc * P + d - 1 - G0][i], s);
+            }
+            if (g.has_dirichlet && coarse_dir(g, MM, X, Y)) s = zero;  // zero IP columns
+            a.rc[(size_t)Y * (nx * MM + 1) + X] = s;
+        }
+    };
+
+    for (int y = ystart; y < ye; ++y) {
+        double2 zr[B], z[B];
+        zr[0] = zraw0;
+        zr[1] = valid ? a.u[dofp<P>(nx, ny, gx, (y + 1) * P)] : zero;
+#pragma unroll
+        for (int jy = 1; jy < P; ++jy) zr[jy + 1] = valid ? a.u[dofp<P>(nx, ny, gx, y * P + jy)] : zero;
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+            z[b] = zr[b];
+            if (g.has_dirichlet) {
+                const int gy = b == 0 ? y * P : (b == 1 ? (y + 1) * P : y * P + b - 1);
+                if (valid && fine_dir<P>(g, gx, gy)) z[b] = zero;
+            }
+        }
+        // y contraction: T = Z M, V = Z S (M, S symmetric)
+        double2 T[B], V[B];
+#pragma unroll
+        for (int bp = 0; bp < B; ++bp) {
+            T[bp] = zero;
+            V[bp] = zero;
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                T[bp] = rfma(sm.M[bp][b], z[b], T[bp]);
+                V[bp] = rfma(sm.S[bp][b], z[b], V[bp]);
+            }
+        }
+        if (valid) {
+            const double2 mr = (x < nx) ? coef(x, y) : zero;
+            const double2 ml = (j == 0 && x >= 1) ? coef(x - 1, y) : zero;
+#pragma unroll
+            for (int bp = 0; bp < B; ++bp) {
+                sm.T[tid][bp] = T[bp];
+                sm.Va[tid][bp] = csub(V[bp], cmul(mr, T[bp]));
+                sm.Vb[tid][bp] = csub(V[bp], cmul(ml, T[bp]));
+            }
+            sm.Z[tid][0] = z[0];
+            sm.Z[tid][1] = z[1];
+        }
+        __syncthreads();
+        double2 O[B];
+#pragma unroll
+        for (int bp = 0; bp < B; ++bp) O[bp] = zero;
+        if (emit) {
+            if (x < nx) add_cell(x, j == 0 ? 0 : j + 1, y, O);
+            if (j == 0 && x >= 1) add_cell(x - 1, 1, y, O);
+            if (gx == 0) {
+                const double kh = g.kh_l[y];
+#pragma unroll
+                for (int bp = 0; bp < B; ++bp) O[bp] = cadd(O[bp], mik(kh, T[bp]));
+            }
+            if (gx == NG - 1) {
+                const double kh = g.kh_r[y];
+#pragma unroll
+                for (int bp = 0; bp < B; ++bp) O[bp] = cadd(O[bp], mik(kh, T[bp]));
+            }
+            if (y == 0) {
+                if (x < nx) horiz_robin(x, j == 0 ? 0 : j + 1, g.kh_b[x], 0, O[0]);
+                if (j == 0 && x >= 1) horiz_robin(x - 1, 1, g.kh_b[x - 1], 0, O[0]);
+            }
+            if (y == ny - 1) {
+                if (x < nx) horiz_robin(x, j == 0 ? 0 : j + 1, g.kh_t[x], 1, O[1]);
+                if (j == 0 && x >= 1) horiz_robin(x - 1, 1, g.kh_t[x - 1], 1, O[1]);
+            }
+        }
+        const bool out_row = MODE == kK1Restrict ? (y >= ys - 1) : (y >= ys);
+        double2 rr[P];
+#pragma unroll
+        for (int jy = 0; jy < P; ++jy) rr[jy] = zero;
+        if (out_row && emit) {
+            double2 Au[P], ur[P];
+            Au[0] = cadd(O[0], carryO);
+            ur[0] = zr[0];
+#pragma unroll
+            for (int jy = 1; jy < P; ++jy) {
+                Au[jy] = O[jy + 1];
+                ur[jy] = zr[jy + 1];
+            }
+            finish_row(y, P, Au, ur, rr);
+            if (MODE == kK1Write && y >= ys) {
+#pragma unroll
+                for (int jy = 0; jy < P; ++jy) a.r[dofp<P>(nx, ny, gx, y * P + jy)] = rr[jy];
+            } else if (MODE == kK1Norm && y >= ys && owned) {
+#pragma unroll
+                for (int jy = 0; jy < P; ++jy) acc += rr[jy].x * rr[jy].x + rr[jy].y * rr[jy].y;
+            }
+        }
+        if (MODE == kK1Restrict && out_row) restrict_row(y, P, rr, y >= ys);
+        carryO = O[1];
+        zraw0 = zr[1];
+        __syncthreads();
+    }
+    // top lattice row (only vertex / h-edge dofs): carried b = 1 contributions
+    if (ye == ny) {
+        double2 rr[1] = {zero};
+        if (emit) {
+            double2 Au[1] = {carryO}, ur[1] = {zraw0};
+            finish_row(ny, 1, Au, ur, rr);
+            if (MODE == kK1Write) a.r[dofp<P>(nx, ny, gx, ny * P)] = rr[0];
+            if (MODE == kK1Norm && owned) acc += rr[0].x * rr[0].x + rr[0].y * rr[0].y;
+        }
+        if (MODE == kK1Restrict) restrict_row(ny, 1, rr, true);
+    }
+    if (MODE == kK1Norm) {
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+        if ((tid & 31) == 0) sm.red[tid >> 5] = acc;
+        __syncthreads();
+        if (tid == 0) {
+            double s = 0.0;
+            for (int w = 0; w < kK1Threads / 32; ++w) s += sm.red[w];
+            a.partial[blockIdx.y * gridDim.x + blockIdx.x] = s;
+        }
+    }
+}
+
+}  // namespace htg
+
+namespace htg {
+
+static std::atomic<long long> g_launches{0};
+void count_launch(int n) { g_launches += n; }
+long long launch_count() { return g_launches.load(); }
+void reset_launch_count() { g_launches = 0; }
+
+template <int P>
+static int k1_grid_x(int nx) {
+    constexpr int W = (kK1Threads - 1 - P) / P;
+    return (nx + W - 1) / W;
+}
+
+static int k1_gx(const FineGeom& g) {
+    switch (g.p) {
+        case 2: return k1_grid_x<2>(g.nx);
+        case 4: return k1_grid_x<4>(g.nx);
+        case 6: return k1_grid_x<6>(g.nx);
+        default: return k1_grid_x<8>(g.nx);
+    }
+}
+
+static int k1_rows(const FineGeom& g, int rows) {
+    if (rows > 0) return rows;
+    const long long strips = k1_gx(g);
+    long long r = (g.ny * strips + 443) / 444;
+    return int(std::max<long long>(4, std::min<long long>(r, g.ny)));
+}
+
+int k1_partials(const FineGeom& g, int rows) {
+    const int r = k1_rows(g, rows);
+    return k1_gx(g) * ((g.ny + r - 1) / r);
+}
+
+template <int P, int MODE>
+static void k1_launch_t(K1Args a, cudaStream_t st) {
+    a.rows = k1_rows(a.g, a.rows);
+    dim3 grid(k1_grid_x<P>(a.g.nx), (a.g.ny + a.rows - 1) / a.rows);
+    const size_t smem = sizeof(K1Smem<P>);
+    static bool attr = false;
+    if (!attr) {
+        HTG_CUDA(cudaFuncSetAttribute(k1_residual<P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        attr = true;
+    }
+    k1_residual<P, MODE><<<grid, kK1Threads, smem, st>>>(a);
+    HTG_CUDA(cudaGetLastError());
+    count_launch();
+}
+
+template <int P>
+static void k1_mode(int mode, const K1Args& a, cudaStream_t st) {
+    if (mode == kK1Write) k1_launch_t<P, kK1Write>(a, st);
+    else if (mode == kK1Norm) k1_launch_t<P, kK1Norm>(a, st);
+    else k1_launch_t<P, kK1Restrict>(a, st);
+}
+
+int k1_launch(int mode, const K1Args& a, cudaStream_t st) {
+    switch (a.g.p) {
+        case 2: k1_mode<2>(mode, a, st); break;
+        case 4: k1_mode<4>(mode, a, st); break;
+        case 6: k1_mode<6>(mode, a, st); break;
+        default: k1_mode<8>(mode, a, st); break;
+    }
+    return k1_partials(a.g, a.rows);
+}
+
+// deterministic: fixed per-thread strided sums, fixed tree
+__global__ void k_reduce(const double* __restrict__ part, int n, double* out) {
+    __shared__ double s[256];
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < n; i += 256) acc += part[i];
+    s[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[0] = s[0];
+}
+
+void reduce_partials(const double* partial, int n, double* out, cudaStream_t st) {
+    k_reduce<<<1, 256, 0, st>>>(partial, n, out);
+    HTG_CUDA(cudaGetLastError());
+    count_launch();
+}
+
+// ---------------------------------------------------------------- K3b
+// u += omega IP uc, IP = (P1 (x) P1) restricted to the nonzero rows: per unit
+// cell the dofs with jx, jy < m (vertex and degree <= m bubbles); rows of fine
+// Dirichlet dofs and columns of coarse Dirichlet dofs are zero
+// (proj/core/src/twogrid.cpp:150-187).
+template <int P>
+__global__ void k_prolong(FineGeom g, double2* __restrict__ u, const double2* __restrict__ uc, double omega) {
+    constexpr int MM = P / 2;
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const int q = int(t % (MM * MM));
+    const long long cell = t / (MM * MM);
+    const int x = int(cell % (g.nx + 1)), y = int(cell / (g.nx + 1));
+    if (y > g.ny) return;
+    const int jx = q % MM, jy = q / MM;
+    if ((x == g.nx && jx) || (y == g.ny && jy)) return;
+    const int gx = x * P + jx, gy = y * P + jy;
+    if (g.has_dirichlet && fine_dir<P>(g, gx, gy)) return;
+    const int cnx1 = g.nx * MM + 1;
+    double wx[MM + 1], wy[MM + 1];
+    int nwx, nwy;
+    if (jx == 0) {
+        wx[0] = 1.0;
+        nwx = 1;
+    } else {
+        for (int i = 0; i <= MM; ++i) wx[i] = c_E[P / 2 - 1][jx + 1][i];
+        nwx = MM + 1;
+    }
+    if (jy == 0) {
+        wy[0] = 1.0;
+        nwy = 1;
+    } else {
+        for (int i = 0; i <= MM; ++i) wy[i] = c_E[P / 2 - 1][jy + 1][i];
+        nwy = MM + 1;
+    }
+    double2 s = make_double2(0.0, 0.0);
+    for (int iy = 0; iy < nwy; ++iy) {
+        const int Y = y * MM + iy;
+        for (int ix = 0; ix < nwx; ++ix) {
+            const int X = x * MM + ix;
+            if (g.has_dirichlet && coarse_dir(g, MM, X, Y)) continue;
+            s = rfma(wx[ix] * wy[iy], uc[(size_t)Y * cnx1 + X], s);
+        }
+    }
+    const long long d = dofp<P>(g.nx, g.ny, gx, gy);
+    u[d] = rfma(omega, s, u[d]);
+}
+
+void prolong_add_launch(const FineGeom& g, double2* u, const double2* uc, double omega, cudaStream_t st) {
+    const int MM = g.p / 2;
+    const long long n = (long long)(g.nx + 1) * (g.ny + 1) * MM * MM;
+    const int bs = 256;
+    const unsigned nb = unsigned((n + bs - 1) / bs);
+    switch (g.p) {
+        case 2: k_prolong<2><<<nb, bs, 0, st>>>(g, u, uc, omega); break;
+        case 4: k_prolong<4><<<nb, bs, 0, st>>>(g, u, uc, omega); break;
+        case 6: k_prolong<6><<<nb, bs, 0, st>>>(g, u, uc, omega); break;
+        default: k_prolong<8><<<nb, bs, 0, st>>>(g, u, uc, omega); break;
+    }
+    HTG_CUDA(cudaGetLastError());
+    count_launch();
+}
+
+// ---------------------------------------------------------------- K4
+// y = A_c x: per coarse cell the QSFEM weights q_{|dx|+|dy|} minus the i eps
+// p=1 mass, minus the Robin p=1 edge mass, Dirichlet rows/cols identity
+// (proj/core/src/qsfem.cpp:118-149).
+__global__ void k_coarse_apply(FineGeom g, int m, const double4* __restrict__ qtab, const double2* __restrict__ x,
+                               double2* __restrict__ y) {
+    const int CX = g.nx * m, CY = g.ny * m;
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t >= (long long)(CX + 1) * (CY + 1)) return;
+    const int X = int(t % (CX + 1)), Y = int(t / (CX + 1));
+    const bool dir = g.has_dirichlet;
+    if (dir && coarse_dir(g, m, X, Y)) {
+        y[t] = x[t];
+        return;
+    }
+    auto xv = [&](int a, int b) -> double2 {
+        if (dir && coarse_dir(g, m, a, b)) return make_double2(0.0, 0.0);
+        return x[(size_t)b * (CX + 1) + a];
+    };
+    double2 s = make_double2(0.0, 0.0);
+    for (int cy = Y - 1; cy <= Y; ++cy) {
+        if (cy < 0 || cy >= CY) continue;
+        for (int cx = X - 1; cx <= X; ++cx) {
+            if (cx < 0 || cx >= CX) continue;
+            const double4 q = qtab[g.cls ? g.cls[(size_t)(cy / m) * g.nx + cx / m] : 0];
+            for (int wy = cy; wy <= cy + 1; ++wy)
+                for (int wx = cx; wx <= cx + 1; ++wx) {
+                    const int dx = abs(wx - X), dy = abs(wy - Y);
+                    const double qw = (dx + dy == 0) ? q.x : (dx + dy == 1 ? q.y : q.z);
+                    const double mass = double((dx == 0 ? 2 : 1) * (dy == 0 ? 2 : 1)) / 36.0;
+                    const double2 v = xv(wx, wy);
+                    // (qw - i eps hc^2 mass) v
+                    const double em = q.w * mass;
+                    s.x += qw * v.x + em * v.y;
+                    s.y += qw * v.y - em * v.x;
+                }
+        }
+    }
+    // absorbing coarse edges (k hc = (k h) / m of the parent fine edge)
+    auto edge = [&](double khc, int ax, int ay, int bx, int by) {
+        // edge with endpoints (ax, ay) == (X, Y) and (bx, by)
+        const double2 vs = xv(ax, ay), vo = xv(bx, by);
+        const double2 c = make_double2(vs.x / 3.0 + vo.x / 6.0, vs.y / 3.0 + vo.y / 6.0);
+        s = cadd(s, mik(khc, c));
+    };
+    if (Y == 0 || Y == CY) {
+        const double* kh = Y == 0 ? g.kh_b : g.kh_t;
+        if (X > 0) edge(kh[(X - 1) / m] / m, X, Y, X - 1, Y);
+        if (X < CX) edge(kh[X / m] / m, X, Y, X + 1, Y);
+    }
+    if (X == 0 || X == CX) {
+        const double* kh = X == 0 ? g.kh_l : g.kh_r;
+        if (Y > 0) edge(kh[(Y - 1) / m] / m, X, Y, X, Y - 1);
+        if (Y < CY) edge(kh[Y / m] / m, X, Y, X, Y + 1);
+    }
+    y[t] = s;
+}
+
+void coarse_apply_launch(const FineGeom& g, const double4* qtab, double hc, const double2* x, double2* y,
+                         cudaStream_t st) {
+    (void)hc;
+    const int m = g.p / 2;
+    const long long n = (long long)(g.nx * m + 1) * (g.ny * m + 1);
+    k_coarse_apply<<<unsigned((n + 255) / 256), 256, 0, st>>>(g, m, qtab, x, y);
+    HTG_CUDA(cudaGetLastError());
+    count_launch();
+}
+
+// ---------------------------------------------------------------- vectors
+__global__ void k_axpy(double2* __restrict__ y, const double2* __restrict__ x, double a, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        y[i] = rfma(a, x[i], y[i]);
+}
+__global__ void k_copy(double2* __restrict__ y, const double2* __restrict__ x, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        y[i] = x[i];
+}
+__global__ void k_zero(double2* __restrict__ y, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        y[i] = make_double2(0.0, 0.0);
+}
+static unsigned vec_blocks(long long n) { return unsigned(std::min<long long>((n + 255) / 256, 148 * 8)); }
+void vec_axpy(double2* y, const double2* x, double a, long long n, cudaStream_t st) {
+    k_axpy<<<vec_blocks(n), 256, 0, st>>>(y, x, a, n);
+    HTG_CUDA(cudaGetLastError());
+    count_launch();
+}
+void vec_copy(double2* y, const double2* x, long long n, cudaStream_t st) {
+    k_copy<<<vec_blocks(n), 256, 0, st>>>(y, x, n);
+    HTG_CUDA(cudaGetLastError());
+    count_launch();
+}
+void vec_zero(double2* y, long long n, cudaStream_t st) {
+    k_zero<<<vec_blocks(n), 256, 0, st>>>(y, n);
+    HTG_CUDA(cudaGetLastError());
+    count_launch();
+}
+
+// partial[b] = (re, im) of sum conj(x) y over block b's fixed slice; then one
+// block folds them in a fixed order
+__global__ void k_dot_part(const double2* __restrict__ x, const double2* __restrict__ y, long long n, double* part) {
+    __shared__ double sr[256], si[256];
+    double ar = 0.0, ai = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const double2 a = x[i], b = y[i];
+        ar += a.x * b.x + a.y * b.y;
+        ai += a.x * b.y - a.y * b.x;
+    }
+    sr[threadIdx.x] = ar;
+    si[threadIdx.x] = ai;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) {
+            sr[threadIdx.x] += sr[threadIdx.x + w];
+            si[threadIdx.x] += si[threadIdx.x + w];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = sr[0];
+        part[2 * blockIdx.x + 1] = si[0];
+    }
+}
+__global__ void k_dot_fold(const double* part, int nb, double2* out) {
+    if (threadIdx.x == 0) {
+        double r = 0.0, i = 0.0;
+        for (int b = 0; b < nb; ++b) {
+            r += part[2 * b];
+            i += part[2 * b + 1];
+        }
+        out[0] = make_double2(r, i);
+    }
+}
+void vec_dot(const double2* x, const double2* y, long long n, double* partial, double2* out, cudaStream_t st) {
+    const unsigned nb = vec_blocks(n);
+    k_dot_part<<<nb, 256, 0, st>>>(x, y, n, partial);
+    k_dot_fold<<<1, 32, 0, st>>>(partial, int(nb), out);
+    HTG_CUDA(cudaGetLastError());
+    count_launch(2);
+}
+__global__ void k_caxpy_dev(double2* __restrict__ y, const double2* __restrict__ x, const double2* a, int neg,
+                            long long n) {
+    double2 c = a[0];
+    if (neg) c = make_double2(-c.x, -c.y);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        y[i] = cadd(y[i], cmul(c, x[i]));
+}
+void vec_caxpy_dev(double2* y, const double2* x, const double2* a, int negate, long long n, cudaStream_t st) {
+    k_caxpy_dev<<<vec_blocks(n), 256, 0, st>>>(y, x, a, negate, n);
+    HTG_CUDA(cudaGetLastError());
+    count_launch();
+}
+__global__ void k_scale_dev(double2* __restrict__ y, const double* s, int inv, long long n) {
+    const double c = inv ? 1.0 / s[0] : s[0];
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        y[i] = rmul(c, y[i]);
+}
+void vec_scale_dev(double2* y, const double* s, int invert, long long n, cudaStream_t st) {
+    k_scale_dev<<<vec_blocks(n), 256, 0, st>>>(y, s, invert, n);
+    HTG_CUDA(cudaGetLastError());
+    count_launch();
+}
+
+}  // namespace htg

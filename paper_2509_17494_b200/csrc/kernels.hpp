@@ -1,0 +1,71 @@
+// kernels.hpp -- launch interfaces of the helmtg_b200 CUDA kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "common.hpp"
+
+namespace htg {
+
+enum K1Mode { kK1Write = 0, kK1Norm = 1, kK1Restrict = 2 };
+
+struct K1Args {
+    FineGeom g;
+    const double2* __restrict__ u;
+    const double2* __restrict__ f;
+    double2* r;        // kK1Write
+    double* partial;   // kK1Norm: one partial sum per CTA
+    double2* rc;       // kK1Restrict
+    int rows;          // lattice rows per CTA
+    int shifted;       // use A_s (alpha_s) instead of A
+};
+
+// launch accounting (htg_launch_count)
+void count_launch(int n = 1);
+
+void upload_basis_tables(const double* M, const double* S, const double* E, int slot);
+
+// K1: r = f - A u; returns the number of partial sums for kK1Norm
+int k1_launch(int mode, const K1Args& a, cudaStream_t st);
+int k1_partials(const FineGeom& g, int rows);
+void reduce_partials(const double* partial, int n, double* out, cudaStream_t st);
+
+// K3b: u += omega IP uc
+void prolong_add_launch(const FineGeom& g, double2* u, const double2* uc, double omega, cudaStream_t st);
+// K4: y = A_c x (QSFEM)
+void coarse_apply_launch(const FineGeom& g, const double4* qtab, double hc, const double2* x, double2* y,
+                         cudaStream_t st);
+
+// vectors
+void vec_axpy(double2* y, const double2* x, double a, long long n, cudaStream_t st);  // y += a x
+void vec_copy(double2* y, const double2* x, long long n, cudaStream_t st);
+void vec_zero(double2* y, long long n, cudaStream_t st);
+// complex dot sum conj(x) y and squared norm, deterministic two-pass
+void vec_dot(const double2* x, const double2* y, long long n, double* partial, double2* out, cudaStream_t st);
+// y = a*x + y with complex a read from device memory (optionally negated)
+void vec_caxpy_dev(double2* y, const double2* x, const double2* a, int negate, long long n, cudaStream_t st);
+void vec_scale_dev(double2* y, const double* s, int invert, long long n, cudaStream_t st);
+
+// ---------------------------------------------------------------- K2 (DD smoother)
+struct DDDevice {
+    int nclass = 0, nsub = 0, nbx = 0, nby = 0, l_dd = 0;
+    int nu_max = 0;           // staging stride per subdomain
+    int ntiles = 0;
+    // per class
+    const int* cls_info;      // [nclass][8]: onx, ony, nloc, nu, kpad, b_off(lo), b_off(hi), loc_off
+    const double2* Bmat;      // all classes, [rows_pad][kpad] each
+    const int* loc_g;         // per class per local dof: lgx | lgy << 16
+    const int* rowmap;        // per class per local dof: U row or -1
+    // per subdomain
+    const int* sub_class;
+    const int* sub_o;         // ox | oy << 16
+    // per tile: class, m0, n0, sub list offset
+    const int4* tiles;
+    const int* class_subs;    // subdomains of each class, contiguous
+};
+void dd_gemm_launch(const FineGeom& g, const DDDevice& d, const double2* r, double2* ystage, cudaStream_t st);
+// out = u + sum_i y_i / L (u may be null -> 0); out may alias u
+void dd_combine_launch(const FineGeom& g, const DDDevice& d, const double2* ystage, const double2* u, double2* out,
+                       cudaStream_t st);
+
+}  // namespace htg

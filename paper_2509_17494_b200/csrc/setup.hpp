@@ -1,0 +1,75 @@
+// setup.hpp -- host-side setup of the two-grid operators (runs once per handle).
+#pragma once
+
+#include <complex>
+#include <memory>
+#include <vector>
+
+#include "common.hpp"
+#include "helmtg_b200.h"
+
+namespace htg {
+
+using cplx = std::complex<double>;
+
+// 1-D hierarchical basis on [0,1]: N0 = 1-x, N1 = x, N_d (d >= 2) the
+// normalised integrated Legendre functions (proj/core/src/basis.cpp:98-114).
+// Every square-element matrix is a tensor product of these (p+1)x(p+1)
+// factors: K_e = S (x) M + M (x) S, M_e = M (x) M, and the Robin edge mass is M
+// (proj/core/src/basis.cpp:197-214,284-300).
+struct Basis1D {
+    int p = 0, m = 0;  // m = p/2, the coarsening factor
+    double M[kMaxP + 1][kMaxP + 1] = {};
+    double S[kMaxP + 1][kMaxP + 1] = {};
+    // E[d][j]: coefficient of N_d in the degree-m interpolant of the values at
+    // the m+1 points j/m (zero for d > m). Tensor products of E give the
+    // staged interpolation of proj/core/src/fespace.cpp:260-378.
+    double E[kMaxP + 1][kMaxP / 2 + 1] = {};
+};
+Basis1D make_basis(int p);
+
+// Validated copy of the C-ABI problem plus per-cell / per-edge tables.
+struct HostProblem {
+    int p = 0, nx = 0, ny = 0;
+    double h = 0.0;
+    std::vector<double> k, eps;           // per cell, (y, x) order
+    std::vector<int8_t> tb, tt, tl, tr;   // tags per boundary edge
+    std::vector<double> khb, kht, khl, khr;  // Robin k*h (0 unless absorbing)
+    bool has_dirichlet = false;
+    // unique (k, eps) coefficient classes
+    std::vector<uint16_t> cls;  // per cell
+    std::vector<double> cls_k, cls_eps;
+    bool uniform = true;
+    long long ndof() const { return (long long)(nx * p + 1) * (ny * p + 1); }
+    double kc(int x, int y) const { return k[(size_t)y * nx + x]; }
+    double ec(int x, int y) const { return eps[(size_t)y * nx + x]; }
+    int8_t tag(char side, int i) const;
+};
+HostProblem make_problem(const htg_problem& prob);
+void validate_config(const htg_config& cfg, const HostProblem& hp);
+
+// ------------------------------------------------------------------ subdomains
+// Non-overlapping l_dd blocks U_i grown by one cell to Omega_i
+// (proj/core/src/twogrid.cpp:17-74). Subdomains whose local operator, Omega
+// shape and U position coincide form one class; each class stores the
+// restricted inverse B_c = (A_s^(i))^-1 [Dofs(U_i), :] (|U| x |Omega| complex).
+struct DDClass {
+    int onx = 0, ony = 0;       // Omega cells
+    int ux = 0, uy = 0, unx = 0, uny = 0;  // U position inside Omega
+    int nloc = 0, nu = 0;       // |Omega dofs|, |U dofs|
+    std::vector<int> umem;      // local Omega index of each U row
+    std::vector<cplx> B;        // nu x nloc, row-major
+};
+struct DDSetup {
+    int l_dd = 4;
+    int nbx = 0, nby = 0;  // blocks per direction
+    std::vector<DDClass> classes;
+    std::vector<int> sub_class;   // per subdomain (by * nbx + bx)
+    std::vector<int> sub_ox, sub_oy;  // Omega origin (cells)
+};
+DDSetup build_dd(const HostProblem& hp, const Basis1D& b, double alpha_s, int l_dd);
+
+// Dense complex LU with partial pivoting (setup only).
+void dense_lu_solve_multi(int n, std::vector<cplx>& A, std::vector<cplx>& X, int nrhs);
+
+}  // namespace htg

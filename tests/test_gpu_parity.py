@@ -1,0 +1,143 @@
+"""GPU parity: every hot-path entry point of the C-ABI against the CPU oracle.
+
+Tolerance (BASELINE.json north_star): relative l2 difference <= 1e-10 for each
+residual, smoother sweep and transfer application; iteration counts to a 1e-6
+relative residual equal to the oracle's within +-1.
+"""
+import numpy as np
+import pytest
+
+from oracle import pyoracle as po
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+A_, N_, D_ = po.ABSORBING, po.NEUMANN, po.DIRICHLET
+
+CASES = {
+    # name: (order, wavelengths, ppw, side tags L R B T, layer sides, extra cfg)
+    "p2_abs": (2, 3, 8, (A_, A_, A_, A_), (), {}),
+    "p4_abs": (4, 4, 10, (A_, A_, A_, A_), (), {}),
+    "p4_dir_neu": (4, 3, 10, (D_, A_, N_, A_), (), {}),
+    "p4_layer": (4, 5, 10, (N_, A_, N_, A_), (po.LEFT, po.BOTTOM), {"layer_width_dofs": 12}),
+    "p2_ns2": (2, 4, 10, (A_, D_, A_, N_), (), {"n_s": 2}),
+    "p4_ldd3": (4, 3, 12, (A_, A_, A_, A_), (), {"l_dd": 3}),
+    "p6_abs": (6, 3, 12, (A_, A_, A_, A_), (), {}),
+    "p4_ndd2": (4, 3, 10, (A_, A_, A_, A_), (), {"n_dd": 2}),
+}
+
+
+def _torch():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(np.asarray(b)), 1e-300)
+
+
+def make(name):
+    import paper_2509_17494_b200 as hb
+    p, W, ppw, sides, layers, extra = CASES[name]
+    lw = extra.get("layer_width_dofs", 40.0)
+    cfg_kw = {k: v for k, v in extra.items() if k != "layer_width_dofs"}
+    ospec = po.ProblemSpec(order=p, wavelengths=W, ppw=ppw, side_tags=sides, layer_sides=layers, layer_width_dofs=lw)
+    oses = po.Session(ospec, po.SolverConfig(**cfg_kw))
+    hspec = hb.ProblemSpec(order=p, wavelengths=W, ppw=ppw, side_tags=sides, layer_sides=layers, layer_width_dofs=lw)
+    prob = hb.build_problem(hspec)
+    ops = hb.setup_two_grid(prob, hb.SolverConfig(**cfg_kw))
+    return oses, prob, ops
+
+
+@pytest.fixture(scope="module", params=list(CASES))
+def case(request):
+    _torch()
+    return request.param, make(request.param)
+
+
+def dev(x):
+    torch = _torch()
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.complex128)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+def test_problem_tables(case):
+    name, (oses, prob, ops) = case
+    k, eps = oses.coeffs()
+    assert np.array_equal(k, prob.k_cells) and np.allclose(eps, prob.eps_cells, rtol=1e-15, atol=0)
+    assert np.array_equal(oses.rhs(), prob.rhs)
+    assert ops.ndof == oses.ndof and ops.coarse_ndof == oses.coarse_ndof
+
+
+def test_residual(case):
+    name, (oses, prob, ops) = case
+    n = oses.ndof
+    f, u = po.random_vector(n, 101), po.random_vector(n, 102)
+    r = dev(np.zeros(n))
+    for shifted in (False, True):
+        ops.residual(dev(f), dev(u), r, shifted=shifted)
+        assert rel(host(r), oses.residual(f, u, shifted=shifted)) <= TOL
+    want = np.linalg.norm(oses.residual(f, u))
+    assert abs(ops.residual_norm(dev(f), dev(u)) - want) <= TOL * want
+
+
+def test_transfers(case):
+    name, (oses, prob, ops) = case
+    n, nc = oses.ndof, oses.coarse_ndof
+    r, uc, u, f = po.random_vector(n, 201), po.random_vector(nc, 202), po.random_vector(n, 203), po.random_vector(n, 204)
+    rc = dev(np.zeros(nc))
+    ops.restrict(dev(r), rc)
+    assert rel(host(rc), oses.apply(4, r)) <= TOL
+    ops.residual_restrict(dev(f), dev(u), rc)
+    assert rel(host(rc), oses.apply(4, oses.residual(f, u))) <= TOL
+    ud = dev(u)
+    ops.prolong_add(ud, dev(uc), 0.7)
+    assert rel(host(ud), u + 0.7 * oses.apply(3, uc)) <= TOL
+
+
+def test_coarse(case):
+    name, (oses, prob, ops) = case
+    nc = oses.coarse_ndof
+    x = po.random_vector(nc, 301)
+    y = dev(np.zeros(nc))
+    ops.coarse_apply(dev(x), y)
+    assert rel(host(y), oses.apply(2, x)) <= TOL
+    ops.coarse_solve(dev(x), y)
+    assert rel(host(y), oses.coarse_solve(x)) <= TOL
+
+
+def test_dd_step_and_smoother(case):
+    name, (oses, prob, ops) = case
+    n = oses.ndof
+    u, f = po.random_vector(n, 401), po.random_vector(n, 402)
+    out = dev(np.zeros(n))
+    ops.dd_step(dev(u), dev(f), out)
+    assert rel(host(out), oses.dd_step(u, f)) <= TOL
+    ud = dev(u)
+    ops.csdd_smoother(ud, dev(f))
+    assert rel(host(ud), oses.csdd_smoother(u, f)) <= TOL
+
+
+def test_two_grid_step(case):
+    name, (oses, prob, ops) = case
+    n = oses.ndof
+    u, f = po.random_vector(n, 501), po.random_vector(n, 502)
+    ud = dev(u)
+    ops.two_grid_step(ud, dev(f))
+    assert rel(host(ud), oses.two_grid_step(u, f)) <= TOL
+
+
+def test_solve_iterations(case):
+    name, (oses, prob, ops) = case
+    f = prob.rhs
+    ro = oses.solve(f)
+    rg = ops.solve(dev(f))
+    assert rg.converged == ro.converged
+    assert abs(rg.iterations - ro.iterations) <= 1
+    assert rel(host(rg.u), ro.u) <= 1e-8
+    rh = ops.solve_host(f)
+    assert rh.iterations == rg.iterations and rel(rh.u, host(rg.u)) <= 1e-12
