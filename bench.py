@@ -1,0 +1,338 @@
+#!/usr/bin/env python
+"""bench.py -- two-grid Helmholtz hot path on B200 (BASELINE.json metric).
+
+metric: smoother+residual DoF/s (one CSDD smoother sweep = K1 residual + K2
+batched subdomain solves + PoU combine, over all fine dofs), plus seconds per
+two-grid iteration and kernel roofline fractions.
+
+Workload (config.workload): BASELINE config 4 -- unit square, Q4, 160
+wavelengths at 10 dofs/wavelength (400 x 400 cells, 2,563,201 complex-fp64
+dofs), all-absorbing boundary, seeded complex Gaussian RHS, CSDD smoother with
+the reference defaults (alpha_s = 0.2, l_dd = 4, n_dd = 1), QSFEM coarse level.
+A step is one smoother sweep. L2 (126 MB) is flushed before every timed step.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the reference algorithm's CPU implementation (the C++
+oracle restatement in oracle/, the reference itself needs Eigen3 and is not
+buildable here) on the host cores, on a bounded sample of the same workload.
+N > 1 runs N independent replicas (the path is single-GPU by the north star).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOAD = dict(order=4, wavelengths=160.0, ppw=10.0)
+WORKLOAD_NAME = ("BASELINE cfg4: unit square, Q4 hierarchical quads, 160 wavelengths at 10 dofs/wavelength "
+                 "(400x400 cells, 2,563,201 complex-fp64 dofs), all-absorbing, seeded complex Gaussian RHS "
+                 "(numpy default_rng(1004)), CSDD alpha_s=0.2 l_dd=4 n_dd=1, QSFEM coarse level")
+# CPU sample: the same element, subdomain size and k*h (identical interior subdomain
+# operators), 100x100 cells -- cfg3/cfg4 per-dof work on a bounded problem
+CPU_SAMPLE = dict(order=4, wavelengths=40.0, ppw=10.0)
+METRIC = "smoother+residual DoF/s"
+UNIT = "DoF/s"
+BYTES_PER_DOF_RESIDUAL = 48  # read u, f; write r (complex fp64)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled while the timed regions run."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.rows = []
+        self.active = False
+        self.lock = threading.Lock()
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        threading.Thread(target=self._reader, daemon=True).start()
+
+    def _reader(self):
+        for line in self.proc.stdout:
+            with self.lock:
+                if self.active:
+                    self.rows.append(line.strip())
+
+    def mark(self, on: bool):
+        with self.lock:
+            self.active = on
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            f = [x.strip() for x in r.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def seeded_rhs(ndof: int, seed: int) -> np.ndarray:
+    g = np.random.default_rng(seed)
+    re = g.standard_normal(ndof)
+    im = g.standard_normal(ndof)
+    return re + 1j * im
+
+
+# ------------------------------------------------------------------ CPU (oracle) leg
+def cpu_sample(steps: int, seconds: float):
+    """Oracle smoother sweeps on CPU_SAMPLE; returns (DoF/s, cores, sample text, per-step s)."""
+    from oracle import pyoracle as po
+    po.build()
+    cores = os.cpu_count() or 1
+    po.set_threads(cores)
+    ses = po.Session(po.ProblemSpec(**CPU_SAMPLE), po.SolverConfig(coarsening=2))
+    f = seeded_rhs(ses.ndof, 1004)
+    u = np.zeros(ses.ndof, np.complex128)
+    u = ses.csdd_smoother(u, f)  # warm
+    times = []
+    t_end = time.perf_counter() + seconds
+    for _ in range(max(1, steps)):
+        t0 = time.perf_counter()
+        u = ses.csdd_smoother(u, f)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() > t_end and len(times) >= 3:
+            break
+    per = statistics.median(times)
+    sample = (f"oracle (C++ restatement, reference thread model: single-thread CSR SpMV, per-subdomain LU solves "
+              f"in parallel_for over {cores} threads) csdd_smoother sweeps on a 100x100-cell Q4 problem "
+              f"({ses.ndof} dofs, same k*h and l_dd as cfg4), {len(times)} sweeps, median {per * 1e3:.1f} ms/sweep")
+    return ses.ndof / per, cores, sample, per, len(times)
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if ws > 1 and rank != 0:
+        return 0
+    warm = max(0, args.warmup)
+    from oracle import pyoracle as po
+    po.build()
+    cores = os.cpu_count() or 1
+    po.set_threads(cores)
+    ses = po.Session(po.ProblemSpec(**CPU_SAMPLE), po.SolverConfig(coarsening=2))
+    f = seeded_rhs(ses.ndof, 1004)
+    u = np.zeros(ses.ndof, np.complex128)
+    for _ in range(warm):
+        u = ses.csdd_smoother(u, f)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        u = ses.csdd_smoother(u, f)
+    T = time.perf_counter() - t0
+    value = ses.ndof * args.steps / T
+    sample = (f"oracle csdd_smoother sweeps on a 100x100-cell Q4 problem ({ses.ndof} dofs, same k*h and l_dd as "
+              f"cfg4), {args.steps} timed sweeps after {warm} warm-up")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": warm, "ms_per_step": T / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": WORKLOAD_NAME, "sample": "100x100 cells of the cfg4 per-dof work"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU leg
+def run_ours(args):
+    import torch
+    import paper_2509_17494_b200 as hb
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local)
+    prob = hb.build_problem(hb.ProblemSpec(**WORKLOAD))
+    t_setup = time.perf_counter()
+    ops = hb.setup_two_grid(prob, hb.SolverConfig())
+    t_setup = time.perf_counter() - t_setup
+    n = ops.ndof
+    f_h = seeded_rhs(n, 1004)
+    f = torch.from_numpy(f_h).to(dev)
+    u = torch.zeros(n, dtype=torch.complex128, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MB > L2
+    stream = torch.cuda.current_stream()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+
+    for _ in range(max(args.warmup, 3)):
+        ops.csdd_smoother(u, f)
+    torch.cuda.synchronize()
+
+    def timed(fn, k):
+        evs = []
+        for _ in range(k):
+            flush.fill_(1.0)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            evs.append((e0, e1))
+        torch.cuda.synchronize()
+        return sum(a.elapsed_time(b) for a, b in evs)
+
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.mark(True)
+    hb.reset_launch_count()
+    T_ms = timed(lambda: ops.csdd_smoother(u, f), args.steps)
+    launches = hb.launch_count()
+    torch.cuda.synchronize()
+    if dist:
+        t = torch.tensor([T_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        T_ms = float(t.item())
+        dist.barrier()
+    value = ws * n * args.steps / (T_ms * 1e-3)
+
+    # seconds per two-grid iteration (coarse solve included), same flush protocol
+    k2 = max(3, min(args.steps, 20))
+    for _ in range(2):
+        ops.two_grid_step(u, f)
+    T2 = timed(lambda: ops.two_grid_step(u, f), k2)
+    s_per_iter = T2 / k2 * 1e-3
+
+    # end to end through the public host-buffer API (pinned host memory)
+    uh = torch.zeros(n, dtype=torch.complex128).pin_memory().numpy()
+    fh = torch.from_numpy(f_h.copy()).pin_memory().numpy()
+    ke = max(3, min(args.steps, 20))
+    ops.csdd_smoother_host(uh, fh)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(ke):
+        ops.csdd_smoother_host(uh, fh)
+    Te = time.perf_counter() - t0
+    sampler.mark(False)
+    e2e = {"value": ws * n * ke / Te, "unit": UNIT, "h2d_bytes_per_step": 2 * n * 16, "d2h_bytes_per_step": n * 16,
+           "api": "htg_csdd_smoother_host (pinned host f, u in; u out)"}
+
+    # per-kernel device times and rooflines
+    prof = ops.profile(u, f, reps=10)
+    fp64_peak = hb.fp64_tensor_peak_tflops()
+    gemm_tf = ops.dd_flops / (prof["dd_gemm"] * 1e-3) / 1e12
+    hbm_peak, hbm_src = peaks()
+    res_gbs = BYTES_PER_DOF_RESIDUAL * n / (prof["residual"] * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh_:
+            traffic = json.load(fh_).get("dd_gemm_dram_bytes_per_launch")
+    except Exception:
+        pass
+    sampler.stop()
+    clocks = sampler.summary()
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": T_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": WORKLOAD_NAME, "parallelism": "replicas" if ws > 1 else "single GPU",
+                   "ndof": n, "subdomains": ops.n_subdomains, "subdomain_classes": ops.n_classes,
+                   "l2": "flushed (256 MB write) before every timed step"},
+        "s_per_two_grid_iteration": s_per_iter,
+        "kernel_ms": {k: round(v, 5) for k, v in prof.items()},
+        "roofline": {"bound": "tensor", "kernel": "k_dd_gemm (batched subdomain solves, DMMA f64)",
+                     "achieved": gemm_tf, "peak": fp64_peak, "unit": "TFLOP/s", "frac": gemm_tf / fp64_peak,
+                     "traffic": traffic,
+                     "peak_source": "measured in this run: DMMA m8n8k4 f64 microbenchmark (no FP64 entry in "
+                                    "MEASURED_PEAKS.json)",
+                     "algorithmic_flops_per_launch": ops.dd_flops},
+        "roofline_residual": {"bound": "hbm", "kernel": "k1_residual", "achieved": res_gbs, "peak": hbm_peak,
+                              "unit": "GB/s", "frac": res_gbs / hbm_peak, "peak_source": hbm_src,
+                              "algorithmic_bytes_per_launch": BYTES_PER_DOF_RESIDUAL * n},
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "setup_s": t_setup,
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        v, cores, sample, per, nsw = cpu_sample(args.steps, args.cpu_seconds)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

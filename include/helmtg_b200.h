@@ -79,7 +79,9 @@ int htg_create(const htg_problem* prob, const htg_config* cfg, void* stream, htg
 int htg_destroy(htg_handle* h);
 
 /* out[0] ndof, [1] coarse ndof, [2] subdomains, [3] subdomain classes,
- * [4] device bytes held, [5] coarse factor bytes, [6] nx, [7] ny, [8] order */
+ * [4] device bytes held, [5] coarse factor bytes, [6] nx, [7] ny, [8] order,
+ * [9] algorithmic flops of one batched subdomain sweep (8 |U_i| |Omega_i| summed),
+ * [10] nested-dissection levels of the coarse solver. out must hold 11 entries. */
 int htg_info(const htg_handle* h, long long* out);
 int htg_set_stream(htg_handle* h, void* stream);
 
@@ -118,6 +120,12 @@ int htg_csdd_smoother_host(htg_handle* h, double* u_host, const double* f_host);
 /* Measured FP64 tensor-core (DMMA) throughput of this GPU, TFLOP/s (the
  * roofline denominator of the dense subdomain batch). */
 int htg_measure_fp64_tensor_peak(double* tflops);
+/* Per-phase device time (ms, CUDA events on the handle's stream, mean of reps):
+ * [0] K1 residual, [1] K2 batched subdomain GEMM, [2] K2 PoU combine,
+ * [3] K1+K3a residual-restrict, [4] coarse solve, [5] K3b prolongation,
+ * [6] K1 residual norm, [7] csdd_smoother sweep, [8] two_grid_step,
+ * [9] K4 coarse stencil. u is overwritten. ms must hold 10 entries. */
+int htg_profile(htg_handle* h, double* u, const double* f, int reps, double* ms);
 /* Kernel-launch accounting: launches of this library's kernels since the last reset. */
 long long htg_launch_count(void);
 void htg_reset_launch_count(void);

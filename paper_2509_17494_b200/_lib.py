@@ -21,7 +21,7 @@ EXPORTS = (
     "htg_residual", "htg_residual_norm", "htg_dd_step", "htg_csdd_smoother", "htg_restrict",
     "htg_residual_restrict", "htg_prolong_add", "htg_coarse_apply", "htg_coarse_solve", "htg_two_grid_step",
     "htg_solve", "htg_solve_host", "htg_two_grid_step_host", "htg_csdd_smoother_host",
-    "htg_measure_fp64_tensor_peak", "htg_launch_count", "htg_reset_launch_count",
+    "htg_measure_fp64_tensor_peak", "htg_profile", "htg_launch_count", "htg_reset_launch_count",
 )
 
 
@@ -79,6 +79,7 @@ def lib():
     L.htg_two_grid_step_host.argtypes = [vp, dp, dp]
     L.htg_csdd_smoother_host.argtypes = [vp, dp, dp]
     L.htg_measure_fp64_tensor_peak.argtypes = [C.POINTER(C.c_double)]
+    L.htg_profile.argtypes = [vp, dp, dp, C.c_int, C.POINTER(C.c_double)]
     L.htg_launch_count.restype = C.c_longlong
     L.htg_config_default.argtypes = [C.POINTER(Config)]
     _lib = L

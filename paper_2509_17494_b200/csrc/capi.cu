@@ -103,6 +103,7 @@ struct htg_handle {
     // subdomain solver
     DDDevice dd{};
     int nclasses = 0;
+    double dd_flops = 0.0;  // algorithmic 8 |U| |Omega| per subdomain, summed
     // coarse solver
     std::unique_ptr<CoarseSolver> coarse;
     // pinned host scalars
@@ -178,6 +179,10 @@ void build_handle(htg_handle* H, const htg_problem& prob, const htg_config& cfg)
     if (cfg.smoother == HTG_SMOOTHER_CSDD) {
         DDSetup dd = build_dd(hp, H->basis, cfg.alpha_s, cfg.l_dd);
         H->nclasses = int(dd.classes.size());
+        for (int sI = 0; sI < int(dd.sub_class.size()); ++sI) {
+            const DDClass& c = dd.classes[dd.sub_class[sI]];
+            H->dd_flops += 8.0 * c.nu * c.nloc;
+        }
         H->dd = upload_dd_impl(dd, hp, M.ptrs, M.bytes, st, H->ystage);
     }
     if (cfg.coarsening == HTG_COARSE_OPTIMIZED_FD) H->coarse = make_coarse_solver(hp, st);
@@ -342,6 +347,8 @@ int htg_info(const htg_handle* h, long long* out) {
         out[6] = h->hp.nx;
         out[7] = h->hp.ny;
         out[8] = h->hp.p;
+        out[9] = (long long)h->dd_flops;
+        out[10] = h->coarse ? h->coarse->levels() : 0;
     });
 }
 
@@ -452,6 +459,39 @@ int htg_csdd_smoother_host(htg_handle* h, double* u_host, const double* f_host) 
         csdd(h, h->uio, h->fio);
         HTG_CUDA(cudaMemcpyAsync(u_host, h->uio, nb, cudaMemcpyDeviceToHost, h->st));
         HTG_CUDA(cudaStreamSynchronize(h->st));
+    });
+}
+
+int htg_profile(htg_handle* h, double* u, const double* f, int reps, double* ms) {
+    return guard([&] {
+        if (!h->dd.nsub) throw InvalidArgument("handle has no CSDD smoother");
+        double2* U = D2(u);
+        const double2* Fv = CD2(f);
+        cudaEvent_t e0, e1;
+        HTG_CUDA(cudaEventCreate(&e0));
+        HTG_CUDA(cudaEventCreate(&e1));
+        auto timeit = [&](auto&& fn) {
+            fn();  // warm
+            HTG_CUDA(cudaEventRecord(e0, h->st));
+            for (int i = 0; i < reps; ++i) fn();
+            HTG_CUDA(cudaEventRecord(e1, h->st));
+            HTG_CUDA(cudaEventSynchronize(e1));
+            float t = 0.f;
+            HTG_CUDA(cudaEventElapsedTime(&t, e0, e1));
+            return double(t) / reps;
+        };
+        ms[0] = timeit([&] { residual(h, Fv, U, h->r, 0); });
+        ms[1] = timeit([&] { dd_gemm_launch(h->g, h->dd, h->r, h->ystage, h->st); });
+        ms[2] = timeit([&] { dd_combine_launch(h->g, h->dd, h->ystage, U, h->v, h->st); });
+        ms[3] = h->coarse ? timeit([&] { residual_restrict(h, Fv, U, h->rc); }) : 0.0;
+        ms[4] = h->coarse ? timeit([&] { h->coarse->solve(h->rc, h->uc, h->st); }) : 0.0;
+        ms[5] = h->coarse ? timeit([&] { prolong_add_launch(h->g, h->v, h->uc, 1.0, h->st); }) : 0.0;
+        ms[6] = timeit([&] { residual_norm2(h, Fv, U, 0); });
+        ms[7] = timeit([&] { csdd(h, U, Fv); });
+        ms[8] = timeit([&] { two_grid_step(h, U, Fv); });
+        ms[9] = h->coarse ? timeit([&] { coarse_apply_launch(h->g, h->qtab, 0.0, h->rc, h->uc, h->st); }) : 0.0;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
     });
 }
 

@@ -197,10 +197,12 @@ class TwoGridOperators:
         st = C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
         check(L.htg_create(C.byref(cp), C.byref(cfg), st, C.byref(h)))
         self._h = h
-        info = (C.c_longlong * 9)()
+        info = (C.c_longlong * 11)()
         check(L.htg_info(h, info))
         (self.ndof, self.coarse_ndof, self.n_subdomains, self.n_classes, self.device_bytes,
          self.coarse_factor_bytes) = (int(v) for v in info[:6])
+        self.dd_flops = int(info[9])
+        self.coarse_levels = int(info[10])
 
     def close(self):
         if getattr(self, "_h", None):
@@ -268,6 +270,14 @@ class TwoGridOperators:
         check(lib().htg_solve(self._h, _dptr(f), _dptr(u), hist.ctypes.data_as(C.c_void_p), cap, C.byref(it),
                               C.byref(conv)), allow_not_converged=True)
         return SolveResult(u, it.value, list(hist[: it.value]), bool(conv.value))
+
+    def profile(self, u, f, reps: int = 10) -> dict:
+        """Mean device time (ms) of each hot-path phase (CUDA events, handle stream)."""
+        ms = (C.c_double * 10)()
+        check(lib().htg_profile(self._h, _dptr(u), _dptr(f), int(reps), ms))
+        keys = ("residual", "dd_gemm", "dd_combine", "residual_restrict", "coarse_solve", "prolong",
+                "residual_norm", "smoother_sweep", "two_grid_step", "coarse_apply")
+        return dict(zip(keys, list(ms)))
 
     # ---------------------------------------------------------------- host API
     def solve_host(self, f: np.ndarray) -> SolveResult:
