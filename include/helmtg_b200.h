@@ -124,7 +124,9 @@ int htg_measure_fp64_tensor_peak(double* tflops);
  * [0] K1 residual, [1] K2 batched subdomain GEMM, [2] K2 PoU combine,
  * [3] K1+K3a residual-restrict, [4] coarse solve, [5] K3b prolongation,
  * [6] K1 residual norm, [7] csdd_smoother sweep, [8] two_grid_step,
- * [9] K4 coarse stencil. u is overwritten. ms must hold 10 entries. */
+ * [9] K4 coarse stencil, [10] smoother sweep, [11] two_grid_step and [12]
+ * coarse solve replayed as CUDA graphs (the form the public entry points use).
+ * u is overwritten. ms must hold 13 entries. */
 int htg_profile(htg_handle* h, double* u, const double* f, int reps, double* ms);
 /* Kernel-launch accounting: launches of this library's kernels since the last reset. */
 long long htg_launch_count(void);

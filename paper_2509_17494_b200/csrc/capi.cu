@@ -7,8 +7,11 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <tuple>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -108,7 +111,21 @@ struct htg_handle {
     std::unique_ptr<CoarseSolver> coarse;
     // pinned host scalars
     double* hscal = nullptr;
+    // CUDA graphs of the launch sequences, keyed by (kind, u, f); replayed on
+    // an internal capture stream that is event-ordered with the user stream
+    struct GraphEntry {
+        cudaGraphExec_t exec;
+        long long launches;
+    };
+    std::map<std::tuple<int, const void*, const void*>, GraphEntry> graphs;
+    cudaStream_t cap = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    bool use_graphs = true;
     ~htg_handle() {
+        for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
+        if (cap) cudaStreamDestroy(cap);
+        if (ev_in) cudaEventDestroy(ev_in);
+        if (ev_out) cudaEventDestroy(ev_out);
         coarse.reset();
         if (hscal) cudaFreeHost(hscal);
         if (own_stream && st) cudaStreamDestroy(st);
@@ -186,7 +203,52 @@ void build_handle(htg_handle* H, const htg_problem& prob, const htg_config& cfg)
         H->dd = upload_dd_impl(dd, hp, M.ptrs, M.bytes, st, H->ystage);
     }
     if (cfg.coarsening == HTG_COARSE_OPTIMIZED_FD) H->coarse = make_coarse_solver(hp, st);
+    HTG_CUDA(cudaStreamCreateWithFlags(&H->cap, cudaStreamNonBlocking));
+    HTG_CUDA(cudaEventCreateWithFlags(&H->ev_in, cudaEventDisableTiming));
+    HTG_CUDA(cudaEventCreateWithFlags(&H->ev_out, cudaEventDisableTiming));
+    if (const char* e = std::getenv("HTG_NO_GRAPHS")) H->use_graphs = e[0] == '0';
     HTG_CUDA(cudaStreamSynchronize(st));
+}
+
+// Run body() as a CUDA graph: captured once per (kind, u, f), then replayed.
+template <class F>
+void run_graph(htg_handle* H, int kind, const void* u, const void* f, F&& body) {
+    if (!H->use_graphs) {
+        body();
+        return;
+    }
+    const auto key = std::make_tuple(kind, u, f);
+    auto it = H->graphs.find(key);
+    if (it == H->graphs.end()) {
+        cudaStream_t user = H->st;
+        const long long c0 = launch_count();
+        H->st = H->cap;
+        HTG_CUDA(cudaStreamBeginCapture(H->cap, cudaStreamCaptureModeThreadLocal));
+        cudaGraph_t graph = nullptr;
+        try {
+            body();
+        } catch (...) {
+            cudaStreamEndCapture(H->cap, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            H->st = user;
+            throw;
+        }
+        H->st = user;
+        HTG_CUDA(cudaStreamEndCapture(H->cap, &graph));
+        cudaGraphExec_t exec = nullptr;
+        const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        HTG_CUDA(e);
+        const long long n = launch_count() - c0;
+        count_launch(int(-n));  // captured, not launched
+        it = H->graphs.emplace(key, htg_handle::GraphEntry{exec, n}).first;
+    }
+    HTG_CUDA(cudaEventRecord(H->ev_in, H->st));
+    HTG_CUDA(cudaStreamWaitEvent(H->cap, H->ev_in, 0));
+    HTG_CUDA(cudaGraphLaunch(it->second.exec, H->cap));
+    HTG_CUDA(cudaEventRecord(H->ev_out, H->cap));
+    HTG_CUDA(cudaStreamWaitEvent(H->st, H->ev_out, 0));
+    count_launch(int(it->second.launches));
 }
 
 K1Args k1args(htg_handle* H, const double2* f, const double2* u, int shifted) {
@@ -272,7 +334,7 @@ int solve(htg_handle* H, const double2* f, double2* u, double* hist, int cap, in
     if (nf == 0.0) return HTG_OK;
     if (H->cfg.outer == HTG_OUTER_RICHARDSON) {
         for (int it = 1; it <= H->cfg.max_iters; ++it) {
-            two_grid_step(H, u, f);
+            run_graph(H, 2, u, f, [&] { two_grid_step(H, u, f); });
             residual_norm2(H, f, u, 0);
             const double rr = std::sqrt(host_norm2(H, 0)) / nf;
             if (it - 1 < cap) hist[it - 1] = rr;
@@ -384,7 +446,7 @@ int htg_dd_step(htg_handle* h, const double* u, const double* f, double* out) {
 int htg_csdd_smoother(htg_handle* h, double* u, const double* f) {
     return guard([&] {
         if (!h->dd.nsub) throw InvalidArgument("handle has no CSDD smoother");
-        csdd(h, D2(u), CD2(f));
+        run_graph(h, 1, u, f, [&] { csdd(h, D2(u), CD2(f)); });
     });
 }
 
@@ -411,12 +473,12 @@ int htg_coarse_apply(htg_handle* h, const double* x, double* y) {
 int htg_coarse_solve(htg_handle* h, const double* rc, double* uc) {
     return guard([&] {
         if (!h->coarse) throw InvalidArgument("handle has no coarse level");
-        h->coarse->solve(CD2(rc), D2(uc), h->st);
+        run_graph(h, 3, rc, uc, [&] { h->coarse->solve(CD2(rc), D2(uc), h->st); });
     });
 }
 
 int htg_two_grid_step(htg_handle* h, double* u, const double* f) {
-    return guard([&] { two_grid_step(h, D2(u), CD2(f)); });
+    return guard([&] { run_graph(h, 2, u, f, [&] { two_grid_step(h, D2(u), CD2(f)); }); });
 }
 
 int htg_solve(htg_handle* h, const double* f, double* u, double* history, int hist_cap, int* iterations,
@@ -444,7 +506,7 @@ int htg_two_grid_step_host(htg_handle* h, double* u_host, const double* f_host) 
         const size_t nb = size_t(h->ndof) * sizeof(double2);
         HTG_CUDA(cudaMemcpyAsync(h->fio, f_host, nb, cudaMemcpyHostToDevice, h->st));
         HTG_CUDA(cudaMemcpyAsync(h->uio, u_host, nb, cudaMemcpyHostToDevice, h->st));
-        two_grid_step(h, h->uio, h->fio);
+        run_graph(h, 2, h->uio, h->fio, [&] { two_grid_step(h, h->uio, h->fio); });
         HTG_CUDA(cudaMemcpyAsync(u_host, h->uio, nb, cudaMemcpyDeviceToHost, h->st));
         HTG_CUDA(cudaStreamSynchronize(h->st));
     });
@@ -456,7 +518,7 @@ int htg_csdd_smoother_host(htg_handle* h, double* u_host, const double* f_host) 
         const size_t nb = size_t(h->ndof) * sizeof(double2);
         HTG_CUDA(cudaMemcpyAsync(h->fio, f_host, nb, cudaMemcpyHostToDevice, h->st));
         HTG_CUDA(cudaMemcpyAsync(h->uio, u_host, nb, cudaMemcpyHostToDevice, h->st));
-        csdd(h, h->uio, h->fio);
+        run_graph(h, 1, h->uio, h->fio, [&] { csdd(h, h->uio, h->fio); });
         HTG_CUDA(cudaMemcpyAsync(u_host, h->uio, nb, cudaMemcpyDeviceToHost, h->st));
         HTG_CUDA(cudaStreamSynchronize(h->st));
     });
@@ -490,6 +552,10 @@ int htg_profile(htg_handle* h, double* u, const double* f, int reps, double* ms)
         ms[7] = timeit([&] { csdd(h, U, Fv); });
         ms[8] = timeit([&] { two_grid_step(h, U, Fv); });
         ms[9] = h->coarse ? timeit([&] { coarse_apply_launch(h->g, h->qtab, 0.0, h->rc, h->uc, h->st); }) : 0.0;
+        // graph replays of the same sequences
+        ms[10] = timeit([&] { run_graph(h, 1, U, Fv, [&] { csdd(h, U, Fv); }); });
+        ms[11] = timeit([&] { run_graph(h, 2, U, Fv, [&] { two_grid_step(h, U, Fv); }); });
+        ms[12] = h->coarse ? timeit([&] { run_graph(h, 3, h->rc, h->uc, [&] { h->coarse->solve(h->rc, h->uc, h->st); }); }) : 0.0;
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
     });

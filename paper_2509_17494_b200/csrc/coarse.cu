@@ -313,92 +313,197 @@ struct NodeDev {
     int child0, nchild;                    // into child list
 };
 
-constexpr int kCT = 256;  // threads per task CTA (8 warps)
+constexpr int kCT = 256;                   // threads per CTA (8 warps)
+constexpr int kSmallS = 32, kSmallU = 64;  // warp-per-node fronts
+constexpr int kMidF = 384;                 // CTA-per-node fronts (s + u)
 
 __device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {
     return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
 }
+__device__ __forceinline__ double2 warp_sum(double2 a) {
+    for (int o = 16; o > 0; o >>= 1) {
+        a.x += __shfl_xor_sync(0xffffffffu, a.x, o);
+        a.y += __shfl_xor_sync(0xffffffffu, a.y, o);
+    }
+    return a;
+}
 
-// forward phase 1: gather the front vector, y1 rows = Finv v1
-__global__ void __launch_bounds__(kCT) k_nd_fwd1(const Task* tasks, const NodeDev* nodes, const int* idx,
-                                                 const int* children, const int* cmaps, const long long* cmap_off,
-                                                 const double2* __restrict__ fac, const double2* __restrict__ rc,
-                                                 const double2* __restrict__ contrib, double2* front, double2* Y) {
-    extern __shared__ double2 sv[];
-    const Task tk = tasks[blockIdx.x];
-    const NodeDev nd = nodes[tk.node];
+struct NDArgs {
+    const NodeDev* nodes;
+    const int* idx;
+    const int* children;
+    const int* cmaps;
+    const long long* cmap_off;
+    const double2* fac;
+    const double2* rc;
+    double2* contrib;
+    double2* front;
+    double2* Y;
+    double2* X;
+};
+
+// gather the front vector v = [rc(vars); 0] + extend-add of the children's
+// contribution vectors (children summed in a fixed order)
+template <int STRIDE>
+__device__ void gather_front(const NDArgs& a, const NodeDev& nd, double2* sv, int lane, void (*sync)()) {
     const int F = nd.s + nd.u;
-    for (int i = threadIdx.x; i < F; i += kCT) sv[i] = i < nd.s ? rc[idx[nd.off_var + i]] : make_double2(0.0, 0.0);
-    __syncthreads();
+    for (int i = lane; i < F; i += STRIDE) sv[i] = i < nd.s ? a.rc[a.idx[nd.off_var + i]] : make_double2(0.0, 0.0);
+    sync();
     for (int c = 0; c < nd.nchild; ++c) {
-        const int ch = children[nd.child0 + c];
-        const NodeDev cn = nodes[ch];
-        const int* mp = cmaps + cmap_off[ch];
-        for (int a = threadIdx.x; a < cn.u; a += kCT) {
-            const double2 v = contrib[cn.off_contrib + a];
-            double2& d = sv[mp[a]];
+        const int ch = a.children[nd.child0 + c];
+        const NodeDev cn = a.nodes[ch];
+        const int* mp = a.cmaps + a.cmap_off[ch];
+        for (int k = lane; k < cn.u; k += STRIDE) {
+            const double2 v = a.contrib[cn.off_contrib + k];
+            double2& d = sv[mp[k]];
             d.x += v.x;
             d.y += v.y;
         }
-        __syncthreads();
+        sync();
     }
-    if (tk.r0 == 0)
-        for (int i = nd.s + threadIdx.x; i < F; i += kCT) front[nd.off_front + i] = sv[i];
+}
+__device__ void sync_warp() { __syncwarp(); }
+__device__ void sync_cta() { __syncthreads(); }
+
+// forward, small fronts: one warp per node, lanes own rows
+__global__ void __launch_bounds__(kCT) k_nd_fwd_small(const int* __restrict__ list, int n, NDArgs a) {
+    __shared__ double2 sv[kCT / 32][kSmallS + kSmallU];
+    __shared__ double2 sy[kCT / 32][kSmallS];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int id = blockIdx.x * (kCT / 32) + w;
+    if (id >= n) return;
+    const NodeDev nd = a.nodes[list[id]];
+    gather_front<32>(a, nd, sv[w], lane, sync_warp);
+    const double2* Fi = a.fac + nd.off_F;
+    if (lane < nd.s) {
+        double2 acc = make_double2(0.0, 0.0);
+        for (int k = 0; k < nd.s; ++k) acc = cfma(Fi[lane * nd.s + k], sv[w][k], acc);
+        sy[w][lane] = acc;
+        a.Y[a.idx[nd.off_var + lane]] = acc;
+    }
+    __syncwarp();
+    const double2* L = a.fac + nd.off_L;
+    for (int r = lane; r < nd.u; r += 32) {
+        double2 acc = sv[w][nd.s + r];
+        for (int k = 0; k < nd.s; ++k) {
+            const double2 l = L[r * nd.s + k], y = sy[w][k];
+            acc.x -= l.x * y.x - l.y * y.y;
+            acc.y -= l.x * y.y + l.y * y.x;
+        }
+        a.contrib[nd.off_contrib + r] = acc;
+    }
+}
+
+// forward, mid fronts: one CTA per node, warp per row, both phases
+__global__ void __launch_bounds__(kCT) k_nd_fwd_mid(const int* __restrict__ list, NDArgs a) {
+    extern __shared__ double2 smem[];
+    const NodeDev nd = a.nodes[list[blockIdx.x]];
+    double2* sv = smem;
+    double2* sy = smem + nd.s + nd.u;
+    gather_front<kCT>(a, nd, sv, threadIdx.x, sync_cta);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const double2* Fi = fac + nd.off_F;
-    for (int r = tk.r0 + warp; r < tk.r0 + tk.nr; r += kCT / 32) {
+    const double2* Fi = a.fac + nd.off_F;
+    for (int r = warp; r < nd.s; r += kCT / 32) {
         double2 acc = make_double2(0.0, 0.0);
         const double2* row = Fi + (size_t)r * nd.s;
         for (int k = lane; k < nd.s; k += 32) acc = cfma(row[k], sv[k], acc);
-        for (int o = 16; o > 0; o >>= 1) {
-            acc.x += __shfl_down_sync(0xffffffffu, acc.x, o);
-            acc.y += __shfl_down_sync(0xffffffffu, acc.y, o);
+        acc = warp_sum(acc);
+        if (lane == 0) {
+            sy[r] = acc;
+            a.Y[a.idx[nd.off_var + r]] = acc;
         }
-        if (lane == 0) Y[idx[nd.off_var + r]] = acc;
+    }
+    __syncthreads();
+    const double2* L = a.fac + nd.off_L;
+    for (int r = warp; r < nd.u; r += kCT / 32) {
+        double2 acc = make_double2(0.0, 0.0);
+        const double2* row = L + (size_t)r * nd.s;
+        for (int k = lane; k < nd.s; k += 32) acc = cfma(row[k], sy[k], acc);
+        acc = warp_sum(acc);
+        if (lane == 0) {
+            const double2 v2 = sv[nd.s + r];
+            a.contrib[nd.off_contrib + r] = make_double2(v2.x - acc.x, v2.y - acc.y);
+        }
     }
 }
 
-// forward phase 2: contribution rows c = v2 - L21 y1
-__global__ void __launch_bounds__(kCT) k_nd_fwd2(const Task* tasks, const NodeDev* nodes, const int* idx,
-                                                 const double2* __restrict__ fac, const double2* __restrict__ front,
-                                                 const double2* __restrict__ Y, double2* contrib) {
-    extern __shared__ double2 sv[];
+// forward, large fronts, phase 1: y1 rows = Finv v1 (v2 stashed by the r0 == 0 task)
+__global__ void __launch_bounds__(kCT) k_nd_fwd1(const Task* tasks, NDArgs a) {
+    extern __shared__ double2 smem[];
     const Task tk = tasks[blockIdx.x];
-    const NodeDev nd = nodes[tk.node];
-    for (int i = threadIdx.x; i < nd.s; i += kCT) sv[i] = Y[idx[nd.off_var + i]];
+    const NodeDev nd = a.nodes[tk.node];
+    gather_front<kCT>(a, nd, smem, threadIdx.x, sync_cta);
+    if (tk.r0 == 0)
+        for (int i = nd.s + threadIdx.x; i < nd.s + nd.u; i += kCT) a.front[nd.off_front + i] = smem[i];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const double2* Fi = a.fac + nd.off_F;
+    for (int r = tk.r0 + warp; r < tk.r0 + tk.nr; r += kCT / 32) {
+        double2 acc = make_double2(0.0, 0.0);
+        const double2* row = Fi + (size_t)r * nd.s;
+        for (int k = lane; k < nd.s; k += 32) acc = cfma(row[k], smem[k], acc);
+        acc = warp_sum(acc);
+        if (lane == 0) a.Y[a.idx[nd.off_var + r]] = acc;
+    }
+}
+
+// forward, large fronts, phase 2: contribution rows c = v2 - L21 y1
+__global__ void __launch_bounds__(kCT) k_nd_fwd2(const Task* tasks, NDArgs a) {
+    extern __shared__ double2 smem[];
+    const Task tk = tasks[blockIdx.x];
+    const NodeDev nd = a.nodes[tk.node];
+    for (int i = threadIdx.x; i < nd.s; i += kCT) smem[i] = a.Y[a.idx[nd.off_var + i]];
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const double2* L = fac + nd.off_L;
+    const double2* L = a.fac + nd.off_L;
     for (int r = tk.r0 + warp; r < tk.r0 + tk.nr; r += kCT / 32) {
         double2 acc = make_double2(0.0, 0.0);
         const double2* row = L + (size_t)r * nd.s;
-        for (int k = lane; k < nd.s; k += 32) acc = cfma(row[k], sv[k], acc);
-        for (int o = 16; o > 0; o >>= 1) {
-            acc.x += __shfl_down_sync(0xffffffffu, acc.x, o);
-            acc.y += __shfl_down_sync(0xffffffffu, acc.y, o);
-        }
+        for (int k = lane; k < nd.s; k += 32) acc = cfma(row[k], smem[k], acc);
+        acc = warp_sum(acc);
         if (lane == 0) {
-            const double2 v2 = front[nd.off_front + nd.s + r];
-            contrib[nd.off_contrib + r] = make_double2(v2.x - acc.x, v2.y - acc.y);
+            const double2 v2 = a.front[nd.off_front + nd.s + r];
+            a.contrib[nd.off_contrib + r] = make_double2(v2.x - acc.x, v2.y - acc.y);
         }
     }
 }
 
-// backward: x1 rows = Uinv y1 - Z x2
-__global__ void __launch_bounds__(kCT) k_nd_bwd(const Task* tasks, const NodeDev* nodes, const int* idx,
-                                                const double2* __restrict__ fac, const double2* __restrict__ Y,
-                                                double2* X) {
-    extern __shared__ double2 sv[];
+// backward, small fronts: warp per node, x1 = Uinv y1 - Z x2
+__global__ void __launch_bounds__(kCT) k_nd_bwd_small(const int* __restrict__ list, int n, NDArgs a) {
+    __shared__ double2 sv[kCT / 32][kSmallS + kSmallU];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int id = blockIdx.x * (kCT / 32) + w;
+    if (id >= n) return;
+    const NodeDev nd = a.nodes[list[id]];
+    for (int i = lane; i < nd.s; i += 32) sv[w][i] = a.Y[a.idx[nd.off_var + i]];
+    for (int i = lane; i < nd.u; i += 32) sv[w][nd.s + i] = a.X[a.idx[nd.off_ring + i]];
+    __syncwarp();
+    if (lane < nd.s) {
+        const double2* U = a.fac + nd.off_U + (size_t)lane * nd.s;
+        const double2* Z = a.fac + nd.off_Z + (size_t)lane * nd.u;
+        double2 acc = make_double2(0.0, 0.0);
+        for (int k = 0; k < nd.s; ++k) acc = cfma(U[k], sv[w][k], acc);
+        for (int k = 0; k < nd.u; ++k) {
+            const double2 z = Z[k], x = sv[w][nd.s + k];
+            acc.x -= z.x * x.x - z.y * x.y;
+            acc.y -= z.x * x.y + z.y * x.x;
+        }
+        a.X[a.idx[nd.off_var + lane]] = acc;
+    }
+}
+
+// backward, CTA tasks (mid: whole node, large: 8 rows): warp per row
+__global__ void __launch_bounds__(kCT) k_nd_bwd(const Task* tasks, NDArgs a) {
+    extern __shared__ double2 smem[];
     const Task tk = tasks[blockIdx.x];
-    const NodeDev nd = nodes[tk.node];
-    double2* y1 = sv;
-    double2* x2 = sv + nd.s;
-    for (int i = threadIdx.x; i < nd.s; i += kCT) y1[i] = Y[idx[nd.off_var + i]];
-    for (int i = threadIdx.x; i < nd.u; i += kCT) x2[i] = X[idx[nd.off_ring + i]];
+    const NodeDev nd = a.nodes[tk.node];
+    double2* y1 = smem;
+    double2* x2 = smem + nd.s;
+    for (int i = threadIdx.x; i < nd.s; i += kCT) y1[i] = a.Y[a.idx[nd.off_var + i]];
+    for (int i = threadIdx.x; i < nd.u; i += kCT) x2[i] = a.X[a.idx[nd.off_ring + i]];
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const double2* U = fac + nd.off_U;
-    const double2* Zm = fac + nd.off_Z;
+    const double2* U = a.fac + nd.off_U;
+    const double2* Zm = a.fac + nd.off_Z;
     for (int r = tk.r0 + warp; r < tk.r0 + tk.nr; r += kCT / 32) {
         double2 acc = make_double2(0.0, 0.0);
         const double2* ur = U + (size_t)r * nd.s;
@@ -408,11 +513,8 @@ __global__ void __launch_bounds__(kCT) k_nd_bwd(const Task* tasks, const NodeDev
         for (int k = lane; k < nd.u; k += 32) az = cfma(zr[k], x2[k], az);
         acc.x -= az.x;
         acc.y -= az.y;
-        for (int o = 16; o > 0; o >>= 1) {
-            acc.x += __shfl_down_sync(0xffffffffu, acc.x, o);
-            acc.y += __shfl_down_sync(0xffffffffu, acc.y, o);
-        }
-        if (lane == 0) X[idx[nd.off_var + r]] = acc;
+        acc = warp_sum(acc);
+        if (lane == 0) a.X[a.idx[nd.off_var + r]] = acc;
     }
 }
 
@@ -425,7 +527,7 @@ class NDSolver : public CoarseSolver {
         t.CY = hp.ny * m;
         const int nv = (t.CX + 1) * (t.CY + 1);
         nv_ = nv;
-        build_nd(t, 0, t.CX, 0, t.CY, 0, 64);
+        build_nd(t, 0, t.CX, 0, t.CY, 0, 9);
         const std::vector<cplx> A9 = coarse_stencil(hp);
         // factor bottom-up by depth; nodes of one depth in parallel
         const int nthr = std::max(1, int(std::thread::hardware_concurrency()));
@@ -463,23 +565,36 @@ class NDSolver : public CoarseSolver {
     int levels() const override { return int(levels_.size()); }
 
     void solve(const double2* rc, double2* uc, cudaStream_t st) override {
-        // forward: deepest level first
-        for (int L = int(levels_.size()) - 1; L >= 0; --L) {
+        NDArgs a = args_;
+        a.rc = rc;
+        a.X = uc;
+        for (int L = int(levels_.size()) - 1; L >= 0; --L) {  // forward: deepest level first
             const Level& lv = levels_[L];
+            if (lv.nsmall) {
+                k_nd_fwd_small<<<(lv.nsmall + 7) / 8, kCT, 0, st>>>(lv.small, lv.nsmall, a);
+                count_launch();
+            }
+            if (lv.nmid) {
+                k_nd_fwd_mid<<<lv.nmid, kCT, lv.smem_mid, st>>>(lv.mid, a);
+                count_launch();
+            }
             if (lv.nf1) {
-                k_nd_fwd1<<<lv.nf1, kCT, lv.smem_f, st>>>(lv.f1, nodes_, idx_, children_, cmaps_, cmap_off_, fac_, rc,
-                                                         contrib_, front_, Y_);
+                k_nd_fwd1<<<lv.nf1, kCT, lv.smem_big, st>>>(lv.f1, a);
                 count_launch();
             }
             if (lv.nf2) {
-                k_nd_fwd2<<<lv.nf2, kCT, lv.smem_f, st>>>(lv.f2, nodes_, idx_, fac_, front_, Y_, contrib_);
+                k_nd_fwd2<<<lv.nf2, kCT, lv.smem_big, st>>>(lv.f2, a);
                 count_launch();
             }
         }
-        for (int L = 0; L < int(levels_.size()); ++L) {
+        for (int L = 0; L < int(levels_.size()); ++L) {  // backward: root first
             const Level& lv = levels_[L];
+            if (lv.nsmall) {
+                k_nd_bwd_small<<<(lv.nsmall + 7) / 8, kCT, 0, st>>>(lv.small, lv.nsmall, a);
+                count_launch();
+            }
             if (lv.nb) {
-                k_nd_bwd<<<lv.nb, kCT, lv.smem_f, st>>>(lv.b, nodes_, idx_, fac_, Y_, uc);
+                k_nd_bwd<<<lv.nb, kCT, lv.smem_b, st>>>(lv.b, a);
                 count_launch();
             }
         }
@@ -488,19 +603,16 @@ class NDSolver : public CoarseSolver {
 
   private:
     struct Level {
+        const int *small = nullptr, *mid = nullptr;
         const Task *f1 = nullptr, *f2 = nullptr, *b = nullptr;
-        int nf1 = 0, nf2 = 0, nb = 0;
-        size_t smem_f = 0;
+        int nsmall = 0, nmid = 0, nf1 = 0, nf2 = 0, nb = 0;
+        size_t smem_mid = 0, smem_big = 0, smem_b = 0;
     };
     std::vector<Level> levels_;
     std::vector<void*> allocs_;
     size_t bytes_ = 0;
     int nv_ = 0;
-    const NodeDev* nodes_ = nullptr;
-    const int *idx_ = nullptr, *children_ = nullptr, *cmaps_ = nullptr;
-    const long long* cmap_off_ = nullptr;
-    const double2* fac_ = nullptr;
-    double2 *contrib_ = nullptr, *front_ = nullptr, *Y_ = nullptr;
+    NDArgs args_{};
 
     template <class T>
     T* up(const std::vector<T>& v, cudaStream_t st) {
@@ -547,66 +659,79 @@ class NDSolver : public CoarseSolver {
             cmap_off[i] = (long long)cmaps.size();
             cmaps.insert(cmaps.end(), n.cmap.begin(), n.cmap.end());
         }
-        // factor buffer assembled in chunks to bound host memory
         void* facp = nullptr;
         HTG_CUDA(cudaMalloc(&facp, std::max<long long>(1, fac_total) * sizeof(double2)));
         allocs_.push_back(facp);
         bytes_ += fac_total * sizeof(double2);
-        fac_ = static_cast<const double2*>(facp);
         for (int i = 0; i < nn; ++i) {
             NDNode& n = t.nodes[i];
             const NodeDev& d = nd[i];
-            auto put = [&](const std::vector<cplx>& v, long long off) {
+            auto put = [&](std::vector<cplx>& v, long long off) {
                 if (v.empty()) return;
                 HTG_CUDA(cudaMemcpy(static_cast<double2*>(facp) + off, v.data(), v.size() * sizeof(cplx),
                                     cudaMemcpyHostToDevice));
+                std::vector<cplx>().swap(v);
             };
             put(n.Finv, d.off_F);
             put(n.L21, d.off_L);
             put(n.Uinv, d.off_U);
             put(n.Z, d.off_Z);
-            std::vector<cplx>().swap(n.Finv);
-            std::vector<cplx>().swap(n.L21);
-            std::vector<cplx>().swap(n.Uinv);
-            std::vector<cplx>().swap(n.Z);
         }
-        nodes_ = up(nd, st);
-        idx_ = up(idx, st);
-        children_ = up(children, st);
-        cmaps_ = up(cmaps, st);
-        cmap_off_ = up(cmap_off, st);
-        contrib_ = up(std::vector<double2>(std::max(contrib_total, 1)), st);
-        front_ = up(std::vector<double2>(std::max(front_total, 1)), st);
-        Y_ = up(std::vector<double2>(nv_), st);
-        // task lists per depth
-        const int rows_per_task = 32;
-        levels_.resize(t.max_depth + 1);
-        std::vector<std::vector<Task>> f1(t.max_depth + 1), f2(t.max_depth + 1), bw(t.max_depth + 1);
-        std::vector<size_t> smem(t.max_depth + 1, 0);
+        args_.fac = static_cast<const double2*>(facp);
+        args_.nodes = up(nd, st);
+        args_.idx = up(idx, st);
+        args_.children = up(children, st);
+        args_.cmaps = up(cmaps, st);
+        args_.cmap_off = up(cmap_off, st);
+        args_.contrib = up(std::vector<double2>(std::max(contrib_total, 1)), st);
+        args_.front = up(std::vector<double2>(std::max(front_total, 1)), st);
+        args_.Y = up(std::vector<double2>(nv_), st);
+        // per depth: small (warp per node), mid (CTA per node), large (8-row tasks)
+        const int D = t.max_depth + 1;
+        levels_.resize(D);
+        std::vector<std::vector<int>> sm(D), md(D);
+        std::vector<std::vector<Task>> f1(D), f2(D), bw(D);
+        size_t max_smem = 0;
         for (int i = 0; i < nn; ++i) {
             const int dep = t.nodes[i].depth;
             const NodeDev& d = nd[i];
-            for (int r = 0; r < d.s; r += rows_per_task) {
-                f1[dep].push_back({i, r, std::min(rows_per_task, d.s - r), 0});
-                bw[dep].push_back({i, r, std::min(rows_per_task, d.s - r), 0});
+            Level& lv = levels_[dep];
+            const int F = d.s + d.u;
+            if (d.s <= kSmallS && d.u <= kSmallU) {
+                sm[dep].push_back(i);
+            } else if (F <= kMidF) {
+                md[dep].push_back(i);
+                bw[dep].push_back({i, 0, d.s, 0});
+                lv.smem_mid = std::max(lv.smem_mid, size_t(F + d.s) * sizeof(double2));
+                lv.smem_b = std::max(lv.smem_b, size_t(F) * sizeof(double2));
+            } else {
+                const int rpt = kCT / 32;
+                for (int r = 0; r < d.s; r += rpt) {
+                    f1[dep].push_back({i, r, std::min(rpt, d.s - r), 0});
+                    bw[dep].push_back({i, r, std::min(rpt, d.s - r), 0});
+                }
+                for (int r = 0; r < d.u; r += rpt) f2[dep].push_back({i, r, std::min(rpt, d.u - r), 0});
+                lv.smem_big = std::max(lv.smem_big, size_t(F) * sizeof(double2));
+                lv.smem_b = std::max(lv.smem_b, size_t(F) * sizeof(double2));
             }
-            for (int r = 0; r < d.u; r += rows_per_task) f2[dep].push_back({i, r, std::min(rows_per_task, d.u - r), 0});
-            smem[dep] = std::max(smem[dep], size_t(d.s + d.u) * sizeof(double2));
         }
-        size_t max_smem = 0;
-        for (int L = 0; L <= t.max_depth; ++L) {
+        for (int L = 0; L < D; ++L) {
             Level& lv = levels_[L];
+            lv.nsmall = int(sm[L].size());
+            lv.nmid = int(md[L].size());
             lv.nf1 = int(f1[L].size());
             lv.nf2 = int(f2[L].size());
             lv.nb = int(bw[L].size());
+            lv.small = up(sm[L], st);
+            lv.mid = up(md[L], st);
             lv.f1 = up(f1[L], st);
             lv.f2 = up(f2[L], st);
             lv.b = up(bw[L], st);
-            lv.smem_f = smem[L];
-            max_smem = std::max(max_smem, smem[L]);
+            max_smem = std::max({max_smem, lv.smem_mid, lv.smem_big, lv.smem_b});
         }
+        if (max_smem > 227 * 1024) throw InvalidArgument("coarse front too large for shared memory");
         if (max_smem > 48 * 1024) {
-            if (max_smem > 227 * 1024) throw InvalidArgument("coarse front too large for shared memory");
+            HTG_CUDA(cudaFuncSetAttribute(k_nd_fwd_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, int(max_smem)));
             HTG_CUDA(cudaFuncSetAttribute(k_nd_fwd1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(max_smem)));
             HTG_CUDA(cudaFuncSetAttribute(k_nd_fwd2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(max_smem)));
             HTG_CUDA(cudaFuncSetAttribute(k_nd_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, int(max_smem)));

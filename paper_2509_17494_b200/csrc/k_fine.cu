@@ -102,24 +102,87 @@ __device__ __forceinline__ int lidx(int xc, int a) {
 }
 
 // ---------------------------------------------------------------- K1
+// Data movement: per lattice row the strip's unit cells are one contiguous
+// byte range of u / f / r (the reference layout keeps each unit cell's p^2
+// dofs together), so rows are staged with 1-D TMA bulk copies
+// (cp.async.bulk + mbarrier, prefetched two rows ahead) and r is written back
+// with bulk stores; threads only touch shared memory.
 constexpr int kK1Threads = 128;
 
 template <int P>
-struct K1Smem {
-    static constexpr int B = P + 1, MM = P / 2;
-    double2 T[kK1Threads][B];
-    double2 Va[kK1Threads][B];  // V - m(cell right of / containing gx) T
-    double2 Vb[kK1Threads][B];  // V - m(cell left of vertex gx) T
-    double2 Z[kK1Threads][2];
-    double2 Rt[kK1Threads][MM];
-    double M[B][B], S[B][B], E[B][MM + 1];
-    double red[kK1Threads / 32];
+struct K1Cfg {
+    static constexpr int B = P + 1, MM = P / 2, W = (kK1Threads - 1 - P) / P;
+    static constexpr int SEG = (W + 2) * P * P;  // max dofs of one staged row segment
 };
+
+template <int P>
+struct K1Smem {
+    using C = K1Cfg<P>;
+    double2 U[3][C::SEG];  // u rows y, y+1, y+2 (ring)
+    double2 F[2][C::SEG];  // f rows (ring)
+    double2 R[2][C::SEG];  // r rows staged for the bulk store (ring)
+    double2 T[kK1Threads][C::B];
+    double2 V[kK1Threads][C::B];
+    double2 Z[kK1Threads][2];
+    double2 Rt[kK1Threads][C::MM];
+    double M[C::B][C::B], S[C::B][C::B], E[C::B][C::MM + 1];
+    double red[kK1Threads / 32];
+    unsigned long long barU[3], barF[2];
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes));
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(b)),
+        "r"(parity));
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_1d(void* dst, const void* src, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+// offset and size of unit cell (x, y) in the reference layout
+template <int P>
+__device__ __forceinline__ long long unit_off(int nx, int ny, int x, int y) {
+    return (long long)y * ((long long)nx * P * P + P) + (y < ny ? (long long)x * P * P : (long long)x * P);
+}
+template <int P>
+__device__ __forceinline__ int unit_size(int nx, int ny, int x, int y) {
+    return y < ny ? (x < nx ? P * P : P) : (x < nx ? P : 1);
+}
 
 template <int P, int MODE>
 __global__ void __launch_bounds__(kK1Threads) k1_residual(K1Args a) {
-    constexpr int B = P + 1, MM = P / 2, W = (kK1Threads - 1 - P) / P;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    using Cf = K1Cfg<P>;
+    constexpr int B = Cf::B, MM = Cf::MM, W = Cf::W;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     K1Smem<P>& sm = *reinterpret_cast<K1Smem<P>*>(smem_raw);
     const FineGeom& g = a.g;
     const int tid = threadIdx.x;
@@ -127,8 +190,8 @@ __global__ void __launch_bounds__(kK1Threads) k1_residual(K1Args a) {
         sm.M[i / B][i % B] = c_M[P / 2 - 1][i / B][i % B];
         sm.S[i / B][i % B] = c_S[P / 2 - 1][i / B][i % B];
     }
-    for (int i = tid; i < B * (MM + 1); i += kK1Threads) sm.E[i / (MM + 1)][i % (MM + 1)] = c_E[P / 2 - 1][i / (MM + 1)][i % (MM + 1)];
-    __syncthreads();
+    for (int i = tid; i < B * (MM + 1); i += kK1Threads)
+        sm.E[i / (MM + 1)][i % (MM + 1)] = c_E[P / 2 - 1][i / (MM + 1)][i % (MM + 1)];
 
     const int nx = g.nx, ny = g.ny, NG = nx * P + 1;
     const int x0 = blockIdx.x * W;
@@ -147,51 +210,81 @@ __global__ void __launch_bounds__(kK1Threads) k1_residual(K1Args a) {
     const double2* mt = a.shifted ? g.mtabS : g.mtab0;
     auto coef = [&](int xc, int y) -> double2 { return mt[g.cls ? g.cls[(size_t)y * nx + xc] : 0]; };
     const double2 zero = make_double2(0.0, 0.0);
+    const int xa = max(x0 - 1, 0), xb = min(x0 + W, nx);                  // staged unit cells (u, f)
+    const int xo = (x0 + W >= nx) ? nx : x0 + W - 1;                      // last owned unit cell
+    auto seg_lo = [&](int yy) { return unit_off<P>(nx, ny, xa, yy); };
+    auto seg_bytes = [&](int yy) {
+        return unsigned((unit_off<P>(nx, ny, xb, yy) + unit_size<P>(nx, ny, xb, yy) - seg_lo(yy)) * 16);
+    };
+    // u row yy -> ring slot (yy - ystart) % 3; k-th use of a slot has parity k & 1
+    auto issue_u = [&](int yy) {
+        const int s = (yy - ystart) % 3;
+        mbar_expect_tx(&sm.barU[s], seg_bytes(yy));
+        tma_load_1d(sm.U[s], a.u + seg_lo(yy), seg_bytes(yy), &sm.barU[s]);
+    };
+    const int yout0 = MODE == kK1Restrict ? max(ys - 1, 0) : ys;  // first lattice row with outputs
+    const bool top = ye == ny;
+    const int ylast = top ? ny : ye - 1;                              // last output lattice row
+    auto issue_f = [&](int yy) {
+        const int s = (yy - yout0) & 1;
+        mbar_expect_tx(&sm.barF[s], seg_bytes(yy));
+        tma_load_1d(sm.F[s], a.f + seg_lo(yy), seg_bytes(yy), &sm.barF[s]);
+    };
+    if (tid == 0) {
+        for (int s = 0; s < 3; ++s) mbar_init(&sm.barU[s], 1);
+        for (int s = 0; s < 2; ++s) mbar_init(&sm.barF[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {
+        issue_u(ystart);
+        if (ystart + 1 <= ny) issue_u(ystart + 1);
+        if (ystart + 2 <= ny && ystart + 2 <= ye) issue_u(ystart + 2);
+        issue_f(yout0);
+        if (yout0 + 1 <= ylast) issue_f(yout0 + 1);
+    }
+    auto uval = [&](int yy, int gy) -> double2 {
+        return valid ? sm.U[(yy - ystart) % 3][dofp<P>(nx, ny, gx, gy) - seg_lo(yy)] : zero;
+    };
+    auto wait_u = [&](int yy) { mbar_wait(&sm.barU[(yy - ystart) % 3], unsigned(((yy - ystart) / 3) & 1)); };
+    auto wait_f = [&](int yy) { mbar_wait(&sm.barF[(yy - yout0) & 1], unsigned(((yy - yout0) >> 1) & 1)); };
 
-    // coarse x-contraction bookkeeping (restriction)
-    const int cX0 = x0 * MM;
-    const int cXend = (x0 + W >= nx) ? nx * MM + 1 : (x0 + W) * MM;
-
-    double2 zraw0 = valid ? a.u[dofp<P>(nx, ny, gx, ystart * P)] : zero;
     double2 carryO = zero, sprev = zero;
     double acc = 0.0;
-
-    auto add_cell = [&](int xc, int al, int y, double2* O) {
-        // contributions of cell (xc, y), gx acting as local x-index al
-        for (int cl = 0; cl <= P; ++cl) {
-            const double s = sm.S[al][cl], mm = sm.M[al][cl];
-            if (s == 0.0 && mm == 0.0) continue;
-            const int li = lidx<P>(xc, cl) - G0;
-            const double2* T = sm.T[li];
-            const double2* V = (cl == 1) ? sm.Vb[li] : sm.Va[li];
-#pragma unroll
-            for (int bp = 0; bp < B; ++bp) O[bp] = rfma(mm, V[bp], rfma(s, T[bp], O[bp]));
-        }
-        (void)y;
-    };
-    auto horiz_robin = [&](int xc, int al, double kh, int zb, double2& out) {
-        double2 s = zero;
-        for (int cl = 0; cl <= P; ++cl) {
-            const double mm = sm.M[al][cl];
-            if (mm != 0.0) s = rfma(mm, sm.Z[lidx<P>(xc, cl) - G0][zb], s);
-        }
-        out = cadd(out, mik(kh, s));
+    const int r_lo_cell = x0;
+    auto rseg_lo = [&](int yy) { return unit_off<P>(nx, ny, r_lo_cell, yy); };
+    auto rseg_bytes = [&](int yy) {
+        return unsigned((unit_off<P>(nx, ny, xo, yy) + unit_size<P>(nx, ny, xo, yy) - rseg_lo(yy)) * 16);
     };
 
-    // emit one lattice row of residual values r[jy], jy < nj
-    auto finish_row = [&](int y, int nj, const double2* Au_in, const double2* uraw, double2* rr) {
+    // r rows: lattice row yy -> R slot; write into smem, bulk store by thread 0
+    auto emit_row = [&](int yy, int nj, const double2* Au, const double2* ur, double2* rr) {
+        wait_f(yy);
+        const double2* Fs = sm.F[(yy - yout0) & 1];
         for (int jy = 0; jy < nj; ++jy) {
-            const int gy = y * P + jy;
-            double2 Au = Au_in[jy];
-            if (g.has_dirichlet && fine_dir<P>(g, gx, gy)) Au = uraw[jy];
-            const double2 fv = a.f[dofp<P>(nx, ny, gx, gy)];
-            rr[jy] = csub(fv, Au);
+            const int gy = yy * P + jy;
+            const long long d = dofp<P>(nx, ny, gx, gy);
+            double2 A = Au[jy];
+            if (g.has_dirichlet && fine_dir<P>(g, gx, gy)) A = ur[jy];
+            const double2 fv = Fs[d - seg_lo(yy)];
+            rr[jy] = csub(fv, A);
+        }
+        if (MODE == kK1Write && owned) {
+            double2* Rs = sm.R[(yy - yout0) & 1];
+            for (int jy = 0; jy < nj; ++jy) Rs[dofp<P>(nx, ny, gx, yy * P + jy) - rseg_lo(yy)] = rr[jy];
+        }
+    };
+    auto store_row = [&](int yy) {
+        // all threads: make smem writes visible to the async proxy, then one thread stores
+        fence_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+            tma_store_1d(a.r + rseg_lo(yy), sm.R[(yy - yout0) & 1], rseg_bytes(yy));
+            bulk_commit();
         }
     };
 
-    // restriction of one lattice row: rows Y = y*MM + i, i < nrow (1 at the top)
     auto restrict_row = [&](int y, int nj, const double2* rr, bool write) {
-        // y-contraction for this gx
         double2 t[MM];
         double2 snext = zero;
 #pragma unroll
@@ -200,7 +293,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_residual(K1Args a) {
             for (int jy = 0; jy < nj; ++jy) {
                 const int gy = y * P + jy;
                 double2 rv = rr[jy];
-                if (g.has_dirichlet && fine_dir<P>(g, gx, gy)) rv = zero;  // zero IP rows
+                if (g.has_dirichlet && fine_dir<P>(g, gx, gy)) rv = zero;
                 if (jy == 0) {
                     t[0] = cadd(t[0], rv);
                 } else if (jy + 1 <= MM) {
@@ -216,6 +309,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_residual(K1Args a) {
 #pragma unroll
         for (int i = 0; i < MM; ++i) sm.Rt[tid][i] = t[i];
         __syncthreads();
+        const int cX0 = x0 * MM, cXend = (x0 + W >= nx) ? nx * MM + 1 : (x0 + W) * MM;
         const int ncx = cXend - cX0;
         const int nrow = (nj == 1 && y == ny) ? 1 : MM;
         for (int w = tid; w < ncx * nrow; w += kK1Threads) {
@@ -223,7 +317,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_residual(K1Args a) {
             const int xc = X / MM, ip = X - xc * MM;
             double2 s = zero;
             if (ip == 0) {
-                if (xc * P - G0 >= 0) s = sm.Rt[xc * P - G0][i];  // vertex xc
+                s = sm.Rt[xc * P - G0][i];
                 if (xc < nx)
                     for (int d = 2; d <= MM; ++d) s = rfma(sm.E[d][0], sm.Rt[xc * P + d - 1 - G0][i], s);
                 if (xc > 0)
@@ -231,17 +325,19 @@ __global__ void __launch_bounds__(kK1Threads) k1_residual(K1Args a) {
             } else {
                 for (int d = 2; d <= MM; ++d) s = rfma(sm.E[d][ip], sm.Rt[xc * P + d - 1 - G0][i], s);
             }
-            if (g.has_dirichlet && coarse_dir(g, MM, X, Y)) s = zero;  // zero IP columns
+            if (g.has_dirichlet && coarse_dir(g, MM, X, Y)) s = zero;
             a.rc[(size_t)Y * (nx * MM + 1) + X] = s;
         }
     };
 
     for (int y = ystart; y < ye; ++y) {
+        wait_u(y);
+        wait_u(y + 1);
         double2 zr[B], z[B];
-        zr[0] = zraw0;
-        zr[1] = valid ? a.u[dofp<P>(nx, ny, gx, (y + 1) * P)] : zero;
+        zr[0] = uval(y, y * P);
+        zr[1] = uval(y + 1, (y + 1) * P);
 #pragma unroll
-        for (int jy = 1; jy < P; ++jy) zr[jy + 1] = valid ? a.u[dofp<P>(nx, ny, gx, y * P + jy)] : zero;
+        for (int jy = 1; jy < P; ++jy) zr[jy + 1] = uval(y, y * P + jy);
 #pragma unroll
         for (int b = 0; b < B; ++b) {
             z[b] = zr[b];
@@ -251,36 +347,64 @@ __global__ void __launch_bounds__(kK1Threads) k1_residual(K1Args a) {
             }
         }
         // y contraction: T = Z M, V = Z S (M, S symmetric)
-        double2 T[B], V[B];
+        double2 T[B];
 #pragma unroll
         for (int bp = 0; bp < B; ++bp) {
-            T[bp] = zero;
-            V[bp] = zero;
+            double2 t = zero, v = zero;
 #pragma unroll
             for (int b = 0; b < B; ++b) {
-                T[bp] = rfma(sm.M[bp][b], z[b], T[bp]);
-                V[bp] = rfma(sm.S[bp][b], z[b], V[bp]);
+                t = rfma(sm.M[bp][b], z[b], t);
+                v = rfma(sm.S[bp][b], z[b], v);
+            }
+            T[bp] = t;
+            if (valid) {
+                sm.T[tid][bp] = t;
+                sm.V[tid][bp] = v;
             }
         }
         if (valid) {
-            const double2 mr = (x < nx) ? coef(x, y) : zero;
-            const double2 ml = (j == 0 && x >= 1) ? coef(x - 1, y) : zero;
-#pragma unroll
-            for (int bp = 0; bp < B; ++bp) {
-                sm.T[tid][bp] = T[bp];
-                sm.Va[tid][bp] = csub(V[bp], cmul(mr, T[bp]));
-                sm.Vb[tid][bp] = csub(V[bp], cmul(ml, T[bp]));
-            }
             sm.Z[tid][0] = z[0];
             sm.Z[tid][1] = z[1];
         }
         __syncthreads();
+        // the slot of row y-1 is free now: prefetch row y+2 (u) and the next f row
+        if (tid == 0) {
+            if (y + 2 <= ny && y + 2 <= ye && y + 2 > ystart + 2) issue_u(y + 2);
+        }
         double2 O[B];
 #pragma unroll
         for (int bp = 0; bp < B; ++bp) O[bp] = zero;
         if (emit) {
-            if (x < nx) add_cell(x, j == 0 ? 0 : j + 1, y, O);
-            if (j == 0 && x >= 1) add_cell(x - 1, 1, y, O);
+            // cell (xc, y), gx as local x-index al: O += sum_c S T + M V - m sum_c M T
+            auto add_cell = [&](int xc, int al) {
+                double2 A1[B], A2[B];
+#pragma unroll
+                for (int bp = 0; bp < B; ++bp) A1[bp] = A2[bp] = zero;
+                for (int cl = 0; cl <= P; ++cl) {
+                    const double s = sm.S[al][cl], mm = sm.M[al][cl];
+                    if (s == 0.0 && mm == 0.0) continue;
+                    const int li = lidx<P>(xc, cl) - G0;
+#pragma unroll
+                    for (int bp = 0; bp < B; ++bp) {
+                        const double2 tv = sm.T[li][bp];
+                        A1[bp] = rfma(mm, sm.V[li][bp], rfma(s, tv, A1[bp]));
+                        A2[bp] = rfma(mm, tv, A2[bp]);
+                    }
+                }
+                const double2 m = coef(xc, y);
+#pragma unroll
+                for (int bp = 0; bp < B; ++bp) O[bp] = cadd(O[bp], csub(A1[bp], cmul(m, A2[bp])));
+            };
+            auto horiz_robin = [&](int xc, int al, double kh, int zb, double2& out) {
+                double2 s = zero;
+                for (int cl = 0; cl <= P; ++cl) {
+                    const double mm = sm.M[al][cl];
+                    if (mm != 0.0) s = rfma(mm, sm.Z[lidx<P>(xc, cl) - G0][zb], s);
+                }
+                out = cadd(out, mik(kh, s));
+            };
+            if (x < nx) add_cell(x, j == 0 ? 0 : j + 1);
+            if (j == 0 && x >= 1) add_cell(x - 1, 1);
             if (gx == 0) {
                 const double kh = g.kh_l[y];
 #pragma unroll
@@ -300,44 +424,49 @@ __global__ void __launch_bounds__(kK1Threads) k1_residual(K1Args a) {
                 if (j == 0 && x >= 1) horiz_robin(x - 1, 1, g.kh_t[x - 1], 1, O[1]);
             }
         }
-        const bool out_row = MODE == kK1Restrict ? (y >= ys - 1) : (y >= ys);
+        const bool out_row = y >= yout0;
         double2 rr[P];
 #pragma unroll
         for (int jy = 0; jy < P; ++jy) rr[jy] = zero;
-        if (out_row && emit) {
-            double2 Au[P], ur[P];
-            Au[0] = cadd(O[0], carryO);
-            ur[0] = zr[0];
+        if (out_row) {
+            if (MODE == kK1Write && y - 2 >= yout0 && tid == 0) bulk_wait_read<1>();  // R slot reuse
+            if (MODE == kK1Write) __syncthreads();
+            if (emit) {
+                double2 Au[P], ur[P];
+                Au[0] = cadd(O[0], carryO);
+                ur[0] = zr[0];
 #pragma unroll
-            for (int jy = 1; jy < P; ++jy) {
-                Au[jy] = O[jy + 1];
-                ur[jy] = zr[jy + 1];
+                for (int jy = 1; jy < P; ++jy) {
+                    Au[jy] = O[jy + 1];
+                    ur[jy] = zr[jy + 1];
+                }
+                emit_row(y, P, Au, ur, rr);
+                if (MODE == kK1Norm && y >= ys && owned) {
+#pragma unroll
+                    for (int jy = 0; jy < P; ++jy) acc += rr[jy].x * rr[jy].x + rr[jy].y * rr[jy].y;
+                }
             }
-            finish_row(y, P, Au, ur, rr);
-            if (MODE == kK1Write && y >= ys) {
-#pragma unroll
-                for (int jy = 0; jy < P; ++jy) a.r[dofp<P>(nx, ny, gx, y * P + jy)] = rr[jy];
-            } else if (MODE == kK1Norm && y >= ys && owned) {
-#pragma unroll
-                for (int jy = 0; jy < P; ++jy) acc += rr[jy].x * rr[jy].x + rr[jy].y * rr[jy].y;
-            }
+            if (MODE == kK1Write) store_row(y);
+            if (MODE == kK1Restrict) restrict_row(y, P, rr, y >= ys);
         }
-        if (MODE == kK1Restrict && out_row) restrict_row(y, P, rr, y >= ys);
         carryO = O[1];
-        zraw0 = zr[1];
-        __syncthreads();
+        __syncthreads();  // F slot of row y and U slot of row y are free after this
+        if (tid == 0 && out_row && y + 2 <= ylast) issue_f(y + 2);
     }
-    // top lattice row (only vertex / h-edge dofs): carried b = 1 contributions
-    if (ye == ny) {
+    // top lattice row (vertex / h-edge dofs only): the carried b = 1 contributions
+    if (top) {
         double2 rr[1] = {zero};
+        if (MODE == kK1Write && ny - 2 >= yout0 && tid == 0) bulk_wait_read<1>();
+        if (MODE == kK1Write) __syncthreads();
         if (emit) {
-            double2 Au[1] = {carryO}, ur[1] = {zraw0};
-            finish_row(ny, 1, Au, ur, rr);
-            if (MODE == kK1Write) a.r[dofp<P>(nx, ny, gx, ny * P)] = rr[0];
+            double2 Au[1] = {carryO}, ur[1] = {uval(ny, ny * P)};
+            emit_row(ny, 1, Au, ur, rr);
             if (MODE == kK1Norm && owned) acc += rr[0].x * rr[0].x + rr[0].y * rr[0].y;
         }
+        if (MODE == kK1Write) store_row(ny);
         if (MODE == kK1Restrict) restrict_row(ny, 1, rr, true);
     }
+    if (MODE == kK1Write && tid == 0) bulk_wait_read<0>();
     if (MODE == kK1Norm) {
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
         if ((tid & 31) == 0) sm.red[tid >> 5] = acc;
@@ -377,7 +506,7 @@ static int k1_gx(const FineGeom& g) {
 static int k1_rows(const FineGeom& g, int rows) {
     if (rows > 0) return rows;
     const long long strips = k1_gx(g);
-    long long r = (g.ny * strips + 443) / 444;
+    long long r = (g.ny * strips + 295) / 296;  // about two CTAs per SM
     return int(std::max<long long>(4, std::min<long long>(r, g.ny)));
 }
 

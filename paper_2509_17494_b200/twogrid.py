@@ -273,10 +273,11 @@ class TwoGridOperators:
 
     def profile(self, u, f, reps: int = 10) -> dict:
         """Mean device time (ms) of each hot-path phase (CUDA events, handle stream)."""
-        ms = (C.c_double * 10)()
+        ms = (C.c_double * 13)()
         check(lib().htg_profile(self._h, _dptr(u), _dptr(f), int(reps), ms))
         keys = ("residual", "dd_gemm", "dd_combine", "residual_restrict", "coarse_solve", "prolong",
-                "residual_norm", "smoother_sweep", "two_grid_step", "coarse_apply")
+                "residual_norm", "smoother_sweep", "two_grid_step", "coarse_apply", "smoother_sweep_graph",
+                "two_grid_step_graph", "coarse_solve_graph")
         return dict(zip(keys, list(ms)))
 
     # ---------------------------------------------------------------- host API
