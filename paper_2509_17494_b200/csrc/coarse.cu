@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cmath>
 #include <functional>
 #include <thread>
@@ -306,26 +307,23 @@ struct Task {
 };
 struct NodeDev {
     int s, u;
-    long long off_F, off_L, off_U, off_Z;  // into the factor buffer
+    long long off_F, off_L, off_U, off_Z;  // into the factor buffer (row-major blocks)
     int off_var, off_ring;                 // into idx
     int off_front;                         // front scratch (s+u)
     int off_contrib;                       // contribution vector (u)
     int child0, nchild;                    // into child list
 };
 
-constexpr int kCT = 256;                   // threads per CTA (8 warps)
-constexpr int kSmallS = 32, kSmallU = 64;  // warp-per-node fronts
-constexpr int kMidF = 384;                 // CTA-per-node fronts (s + u)
+constexpr int kCT = 256;     // threads per CTA (8 warps)
+constexpr int kWarpFMax = 128;  // warp-tier shared buffers (fronts with s + u <= g_warpF)
+static int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+// tier thresholds (overridable for tuning: HTG_ND_LEAF, HTG_ND_WARPF, HTG_ND_MIDDATA, HTG_ND_RPT)
 
 __device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {
     return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
-}
-__device__ __forceinline__ double2 warp_sum(double2 a) {
-    for (int o = 16; o > 0; o >>= 1) {
-        a.x += __shfl_xor_sync(0xffffffffu, a.x, o);
-        a.y += __shfl_xor_sync(0xffffffffu, a.y, o);
-    }
-    return a;
 }
 
 struct NDArgs {
@@ -342,18 +340,58 @@ struct NDArgs {
     double2* X;
 };
 
-// gather the front vector v = [rc(vars); 0] + extend-add of the children's
-// contribution vectors (children summed in a fixed order)
-template <int STRIDE>
-__device__ void gather_front(const NDArgs& a, const NodeDev& nd, double2* sv, int lane, void (*sync)()) {
+// Rows [r0, r1) of a row-major (rows x len) complex block times v, by lane
+// groups of G lanes (G = power of two >= min(len, 32)): consecutive lanes read
+// consecutive entries of a row and consecutive groups consecutive rows, so a
+// warp's loads are contiguous even for short rows. out(r, value) on the
+// group's first lane. warps/nw: this warp's index among the nw warps sharing the rows.
+template <class Out>
+__device__ __forceinline__ void rows_dot(const double2* __restrict__ M, int len, const double2* v, int r0, int r1,
+                                         int warp, int nw, int lane, Out&& out) {
+    int G = 32;
+    if (len <= 4) G = 4;
+    else if (len <= 8) G = 8;
+    else if (len <= 16) G = 16;
+    const int rpw = 32 / G, gl = lane & (G - 1), gi = lane / G;
+    constexpr int U = 4;  // independent rows in flight per lane group
+    const int step = nw * rpw;
+    for (int rb = r0 + warp * rpw; rb < r1; rb += U * step) {
+        double2 acc[U];
+        int rr[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+            acc[q] = make_double2(0.0, 0.0);
+            rr[q] = rb + q * step + gi;
+        }
+        for (int k = gl; k < len; k += G) {
+            const double2 vk = v[k];
+#pragma unroll
+            for (int q = 0; q < U; ++q)
+                if (rr[q] < r1) acc[q] = cfma(M[(size_t)rr[q] * len + k], vk, acc[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+            for (int o = G >> 1; o > 0; o >>= 1) {
+                acc[q].x += __shfl_xor_sync(0xffffffffu, acc[q].x, o);
+                acc[q].y += __shfl_xor_sync(0xffffffffu, acc[q].y, o);
+            }
+            if (gl == 0 && rr[q] < r1) out(rr[q], acc[q]);
+        }
+    }
+}
+
+// front vector v = [rc(vars); 0] + extend-add of the children's contribution
+// vectors, children summed in a fixed order
+template <int STRIDE, class Sync>
+__device__ void gather_front(const NDArgs& a, const NodeDev& nd, double2* sv, int t, Sync&& sync) {
     const int F = nd.s + nd.u;
-    for (int i = lane; i < F; i += STRIDE) sv[i] = i < nd.s ? a.rc[a.idx[nd.off_var + i]] : make_double2(0.0, 0.0);
+    for (int i = t; i < F; i += STRIDE) sv[i] = i < nd.s ? a.rc[a.idx[nd.off_var + i]] : make_double2(0.0, 0.0);
     sync();
     for (int c = 0; c < nd.nchild; ++c) {
         const int ch = a.children[nd.child0 + c];
         const NodeDev cn = a.nodes[ch];
         const int* mp = a.cmaps + a.cmap_off[ch];
-        for (int k = lane; k < cn.u; k += STRIDE) {
+        for (int k = t; k < cn.u; k += STRIDE) {
             const double2 v = a.contrib[cn.off_contrib + k];
             double2& d = sv[mp[k]];
             d.x += v.x;
@@ -362,91 +400,62 @@ __device__ void gather_front(const NDArgs& a, const NodeDev& nd, double2* sv, in
         sync();
     }
 }
-__device__ void sync_warp() { __syncwarp(); }
-__device__ void sync_cta() { __syncthreads(); }
 
-// forward, small fronts: one warp per node, lanes own rows
-__global__ void __launch_bounds__(kCT) k_nd_fwd_small(const int* __restrict__ list, int n, NDArgs a) {
-    __shared__ double2 sv[kCT / 32][kSmallS + kSmallU];
-    __shared__ double2 sy[kCT / 32][kSmallS];
+// forward: y1 = (L^-1 P) v1, c = v2 - L21 y1. Warp tier: one warp per front.
+__global__ void __launch_bounds__(kCT) k_nd_fwd_warp(const int* __restrict__ list, int n, NDArgs a) {
+    __shared__ double2 sv[kCT / 32][kWarpFMax];
+    __shared__ double2 sy[kCT / 32][kWarpFMax];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int id = blockIdx.x * (kCT / 32) + w;
     if (id >= n) return;
     const NodeDev nd = a.nodes[list[id]];
-    gather_front<32>(a, nd, sv[w], lane, sync_warp);
-    const double2* Fi = a.fac + nd.off_F;
-    if (lane < nd.s) {
-        double2 acc = make_double2(0.0, 0.0);
-        for (int k = 0; k < nd.s; ++k) acc = cfma(Fi[lane * nd.s + k], sv[w][k], acc);
-        sy[w][lane] = acc;
-        a.Y[a.idx[nd.off_var + lane]] = acc;
-    }
+    double2* v = sv[w];
+    double2* y = sy[w];
+    gather_front<32>(a, nd, v, lane, [] { __syncwarp(); });
+    rows_dot(a.fac + nd.off_F, nd.s, v, 0, nd.s, 0, 1, lane, [&](int r, double2 acc) {
+        y[r] = acc;
+        a.Y[a.idx[nd.off_var + r]] = acc;
+    });
     __syncwarp();
-    const double2* L = a.fac + nd.off_L;
-    for (int r = lane; r < nd.u; r += 32) {
-        double2 acc = sv[w][nd.s + r];
-        for (int k = 0; k < nd.s; ++k) {
-            const double2 l = L[r * nd.s + k], y = sy[w][k];
-            acc.x -= l.x * y.x - l.y * y.y;
-            acc.y -= l.x * y.y + l.y * y.x;
-        }
-        a.contrib[nd.off_contrib + r] = acc;
-    }
+    rows_dot(a.fac + nd.off_L, nd.s, y, 0, nd.u, 0, 1, lane, [&](int r, double2 acc) {
+        const double2 v2 = v[nd.s + r];
+        a.contrib[nd.off_contrib + r] = make_double2(v2.x - acc.x, v2.y - acc.y);
+    });
 }
 
-// forward, mid fronts: one CTA per node, warp per row, both phases
+// forward, CTA tier: one CTA per front, both phases
 __global__ void __launch_bounds__(kCT) k_nd_fwd_mid(const int* __restrict__ list, NDArgs a) {
     extern __shared__ double2 smem[];
     const NodeDev nd = a.nodes[list[blockIdx.x]];
-    double2* sv = smem;
-    double2* sy = smem + nd.s + nd.u;
-    gather_front<kCT>(a, nd, sv, threadIdx.x, sync_cta);
+    double2* v = smem;
+    double2* y = smem + nd.s + nd.u;
+    gather_front<kCT>(a, nd, v, threadIdx.x, [] { __syncthreads(); });
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const double2* Fi = a.fac + nd.off_F;
-    for (int r = warp; r < nd.s; r += kCT / 32) {
-        double2 acc = make_double2(0.0, 0.0);
-        const double2* row = Fi + (size_t)r * nd.s;
-        for (int k = lane; k < nd.s; k += 32) acc = cfma(row[k], sv[k], acc);
-        acc = warp_sum(acc);
-        if (lane == 0) {
-            sy[r] = acc;
-            a.Y[a.idx[nd.off_var + r]] = acc;
-        }
-    }
+    rows_dot(a.fac + nd.off_F, nd.s, v, 0, nd.s, warp, kCT / 32, lane, [&](int r, double2 acc) {
+        y[r] = acc;
+        a.Y[a.idx[nd.off_var + r]] = acc;
+    });
     __syncthreads();
-    const double2* L = a.fac + nd.off_L;
-    for (int r = warp; r < nd.u; r += kCT / 32) {
-        double2 acc = make_double2(0.0, 0.0);
-        const double2* row = L + (size_t)r * nd.s;
-        for (int k = lane; k < nd.s; k += 32) acc = cfma(row[k], sy[k], acc);
-        acc = warp_sum(acc);
-        if (lane == 0) {
-            const double2 v2 = sv[nd.s + r];
-            a.contrib[nd.off_contrib + r] = make_double2(v2.x - acc.x, v2.y - acc.y);
-        }
-    }
+    rows_dot(a.fac + nd.off_L, nd.s, y, 0, nd.u, warp, kCT / 32, lane, [&](int r, double2 acc) {
+        const double2 v2 = v[nd.s + r];
+        a.contrib[nd.off_contrib + r] = make_double2(v2.x - acc.x, v2.y - acc.y);
+    });
 }
 
-// forward, large fronts, phase 1: y1 rows = Finv v1 (v2 stashed by the r0 == 0 task)
+// forward, large tier phase 1: y1 rows of a task (v2 stashed by the r0 == 0 task)
 __global__ void __launch_bounds__(kCT) k_nd_fwd1(const Task* tasks, NDArgs a) {
     extern __shared__ double2 smem[];
     const Task tk = tasks[blockIdx.x];
     const NodeDev nd = a.nodes[tk.node];
-    gather_front<kCT>(a, nd, smem, threadIdx.x, sync_cta);
+    gather_front<kCT>(a, nd, smem, threadIdx.x, [] { __syncthreads(); });
     if (tk.r0 == 0)
         for (int i = nd.s + threadIdx.x; i < nd.s + nd.u; i += kCT) a.front[nd.off_front + i] = smem[i];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const double2* Fi = a.fac + nd.off_F;
-    for (int r = tk.r0 + warp; r < tk.r0 + tk.nr; r += kCT / 32) {
-        double2 acc = make_double2(0.0, 0.0);
-        const double2* row = Fi + (size_t)r * nd.s;
-        for (int k = lane; k < nd.s; k += 32) acc = cfma(row[k], smem[k], acc);
-        acc = warp_sum(acc);
-        if (lane == 0) a.Y[a.idx[nd.off_var + r]] = acc;
-    }
+    rows_dot(a.fac + nd.off_F, nd.s, smem, tk.r0, tk.r0 + tk.nr, warp, kCT / 32, lane,
+             [&](int r, double2 acc) { a.Y[a.idx[nd.off_var + r]] = acc; });
 }
 
-// forward, large fronts, phase 2: contribution rows c = v2 - L21 y1
+// forward, large tier phase 2: contribution rows c = v2 - L21 y1
 __global__ void __launch_bounds__(kCT) k_nd_fwd2(const Task* tasks, NDArgs a) {
     extern __shared__ double2 smem[];
     const Task tk = tasks[blockIdx.x];
@@ -454,68 +463,57 @@ __global__ void __launch_bounds__(kCT) k_nd_fwd2(const Task* tasks, NDArgs a) {
     for (int i = threadIdx.x; i < nd.s; i += kCT) smem[i] = a.Y[a.idx[nd.off_var + i]];
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const double2* L = a.fac + nd.off_L;
-    for (int r = tk.r0 + warp; r < tk.r0 + tk.nr; r += kCT / 32) {
-        double2 acc = make_double2(0.0, 0.0);
-        const double2* row = L + (size_t)r * nd.s;
-        for (int k = lane; k < nd.s; k += 32) acc = cfma(row[k], smem[k], acc);
-        acc = warp_sum(acc);
-        if (lane == 0) {
-            const double2 v2 = a.front[nd.off_front + nd.s + r];
-            a.contrib[nd.off_contrib + r] = make_double2(v2.x - acc.x, v2.y - acc.y);
-        }
-    }
+    rows_dot(a.fac + nd.off_L, nd.s, smem, tk.r0, tk.r0 + tk.nr, warp, kCT / 32, lane, [&](int r, double2 acc) {
+        const double2 v2 = a.front[nd.off_front + nd.s + r];
+        a.contrib[nd.off_contrib + r] = make_double2(v2.x - acc.x, v2.y - acc.y);
+    });
 }
 
-// backward, small fronts: warp per node, x1 = Uinv y1 - Z x2
-__global__ void __launch_bounds__(kCT) k_nd_bwd_small(const int* __restrict__ list, int n, NDArgs a) {
-    __shared__ double2 sv[kCT / 32][kSmallS + kSmallU];
+// backward: x1 = U^-1 y1 - (U^-1 U12) x2. Z rows are computed into sz first.
+__device__ __forceinline__ void bwd_rows(const NDArgs& a, const NodeDev& nd, const double2* y1, const double2* x2,
+                                         double2* sz, int r0, int r1, int warp, int nw, int lane,
+                                         void (*sync)()) {
+    if (nd.u > 0) {
+        rows_dot(a.fac + nd.off_Z, nd.u, x2, r0, r1, warp, nw, lane, [&](int r, double2 acc) { sz[r - r0] = acc; });
+        sync();
+    }
+    rows_dot(a.fac + nd.off_U, nd.s, y1, r0, r1, warp, nw, lane, [&](int r, double2 acc) {
+        if (nd.u > 0) {
+            acc.x -= sz[r - r0].x;
+            acc.y -= sz[r - r0].y;
+        }
+        a.X[a.idx[nd.off_var + r]] = acc;
+    });
+}
+__device__ void sync_warp_fn() { __syncwarp(); }
+__device__ void sync_cta_fn() { __syncthreads(); }
+
+__global__ void __launch_bounds__(kCT) k_nd_bwd_warp(const int* __restrict__ list, int n, NDArgs a) {
+    __shared__ double2 sv[kCT / 32][kWarpFMax];
+    __shared__ double2 sz[kCT / 32][kWarpFMax];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int id = blockIdx.x * (kCT / 32) + w;
     if (id >= n) return;
     const NodeDev nd = a.nodes[list[id]];
-    for (int i = lane; i < nd.s; i += 32) sv[w][i] = a.Y[a.idx[nd.off_var + i]];
-    for (int i = lane; i < nd.u; i += 32) sv[w][nd.s + i] = a.X[a.idx[nd.off_ring + i]];
+    double2* v = sv[w];
+    for (int i = lane; i < nd.s; i += 32) v[i] = a.Y[a.idx[nd.off_var + i]];
+    for (int i = lane; i < nd.u; i += 32) v[nd.s + i] = a.X[a.idx[nd.off_ring + i]];
     __syncwarp();
-    if (lane < nd.s) {
-        const double2* U = a.fac + nd.off_U + (size_t)lane * nd.s;
-        const double2* Z = a.fac + nd.off_Z + (size_t)lane * nd.u;
-        double2 acc = make_double2(0.0, 0.0);
-        for (int k = 0; k < nd.s; ++k) acc = cfma(U[k], sv[w][k], acc);
-        for (int k = 0; k < nd.u; ++k) {
-            const double2 z = Z[k], x = sv[w][nd.s + k];
-            acc.x -= z.x * x.x - z.y * x.y;
-            acc.y -= z.x * x.y + z.y * x.x;
-        }
-        a.X[a.idx[nd.off_var + lane]] = acc;
-    }
+    bwd_rows(a, nd, v, v + nd.s, sz[w], 0, nd.s, 0, 1, lane, sync_warp_fn);
 }
 
-// backward, CTA tasks (mid: whole node, large: 8 rows): warp per row
+// backward, CTA tasks (whole front for the CTA tier, row blocks for the large tier)
 __global__ void __launch_bounds__(kCT) k_nd_bwd(const Task* tasks, NDArgs a) {
     extern __shared__ double2 smem[];
     const Task tk = tasks[blockIdx.x];
     const NodeDev nd = a.nodes[tk.node];
     double2* y1 = smem;
     double2* x2 = smem + nd.s;
+    double2* sz = smem + nd.s + nd.u;
     for (int i = threadIdx.x; i < nd.s; i += kCT) y1[i] = a.Y[a.idx[nd.off_var + i]];
     for (int i = threadIdx.x; i < nd.u; i += kCT) x2[i] = a.X[a.idx[nd.off_ring + i]];
     __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const double2* U = a.fac + nd.off_U;
-    const double2* Zm = a.fac + nd.off_Z;
-    for (int r = tk.r0 + warp; r < tk.r0 + tk.nr; r += kCT / 32) {
-        double2 acc = make_double2(0.0, 0.0);
-        const double2* ur = U + (size_t)r * nd.s;
-        for (int k = lane; k < nd.s; k += 32) acc = cfma(ur[k], y1[k], acc);
-        const double2* zr = Zm + (size_t)r * nd.u;
-        double2 az = make_double2(0.0, 0.0);
-        for (int k = lane; k < nd.u; k += 32) az = cfma(zr[k], x2[k], az);
-        acc.x -= az.x;
-        acc.y -= az.y;
-        acc = warp_sum(acc);
-        if (lane == 0) a.X[a.idx[nd.off_var + r]] = acc;
-    }
+    bwd_rows(a, nd, y1, x2, sz, tk.r0, tk.r0 + tk.nr, threadIdx.x >> 5, kCT / 32, threadIdx.x & 31, sync_cta_fn);
 }
 
 class NDSolver : public CoarseSolver {
@@ -527,7 +525,7 @@ class NDSolver : public CoarseSolver {
         t.CY = hp.ny * m;
         const int nv = (t.CX + 1) * (t.CY + 1);
         nv_ = nv;
-        build_nd(t, 0, t.CX, 0, t.CY, 0, 9);
+        build_nd(t, 0, t.CX, 0, t.CY, 0, env_int("HTG_ND_LEAF", 16));
         const std::vector<cplx> A9 = coarse_stencil(hp);
         // factor bottom-up by depth; nodes of one depth in parallel
         const int nthr = std::max(1, int(std::thread::hardware_concurrency()));
@@ -570,8 +568,8 @@ class NDSolver : public CoarseSolver {
         a.X = uc;
         for (int L = int(levels_.size()) - 1; L >= 0; --L) {  // forward: deepest level first
             const Level& lv = levels_[L];
-            if (lv.nsmall) {
-                k_nd_fwd_small<<<(lv.nsmall + 7) / 8, kCT, 0, st>>>(lv.small, lv.nsmall, a);
+            if (lv.nwarp) {
+                k_nd_fwd_warp<<<(lv.nwarp + 7) / 8, kCT, 0, st>>>(lv.warp, lv.nwarp, a);
                 count_launch();
             }
             if (lv.nmid) {
@@ -589,12 +587,12 @@ class NDSolver : public CoarseSolver {
         }
         for (int L = 0; L < int(levels_.size()); ++L) {  // backward: root first
             const Level& lv = levels_[L];
-            if (lv.nsmall) {
-                k_nd_bwd_small<<<(lv.nsmall + 7) / 8, kCT, 0, st>>>(lv.small, lv.nsmall, a);
-                count_launch();
-            }
             if (lv.nb) {
                 k_nd_bwd<<<lv.nb, kCT, lv.smem_b, st>>>(lv.b, a);
+                count_launch();
+            }
+            if (lv.nwarp) {
+                k_nd_bwd_warp<<<(lv.nwarp + 7) / 8, kCT, 0, st>>>(lv.warp, lv.nwarp, a);
                 count_launch();
             }
         }
@@ -603,9 +601,9 @@ class NDSolver : public CoarseSolver {
 
   private:
     struct Level {
-        const int *small = nullptr, *mid = nullptr;
+        const int *warp = nullptr, *mid = nullptr;
         const Task *f1 = nullptr, *f2 = nullptr, *b = nullptr;
-        int nsmall = 0, nmid = 0, nf1 = 0, nf2 = 0, nb = 0;
+        int nwarp = 0, nmid = 0, nf1 = 0, nf2 = 0, nb = 0;
         size_t smem_mid = 0, smem_big = 0, smem_b = 0;
     };
     std::vector<Level> levels_;
@@ -686,43 +684,45 @@ class NDSolver : public CoarseSolver {
         args_.contrib = up(std::vector<double2>(std::max(contrib_total, 1)), st);
         args_.front = up(std::vector<double2>(std::max(front_total, 1)), st);
         args_.Y = up(std::vector<double2>(nv_), st);
-        // per depth: small (warp per node), mid (CTA per node), large (8-row tasks)
+        // per depth: warp tier, CTA tier, large tier (8 rows per CTA task)
         const int D = t.max_depth + 1;
         levels_.resize(D);
-        std::vector<std::vector<int>> sm(D), md(D);
+        std::vector<std::vector<int>> wp(D), md(D);
         std::vector<std::vector<Task>> f1(D), f2(D), bw(D);
         size_t max_smem = 0;
+        const int warpF = std::min(kWarpFMax, env_int("HTG_ND_WARPF", 64));
+        const long long midData = env_int("HTG_ND_MIDDATA", 16384);
         for (int i = 0; i < nn; ++i) {
             const int dep = t.nodes[i].depth;
             const NodeDev& d = nd[i];
             Level& lv = levels_[dep];
             const int F = d.s + d.u;
-            if (d.s <= kSmallS && d.u <= kSmallU) {
-                sm[dep].push_back(i);
-            } else if (F <= kMidF) {
+            if (F <= warpF) {
+                wp[dep].push_back(i);
+            } else if ((long long)d.s * F <= midData) {
                 md[dep].push_back(i);
                 bw[dep].push_back({i, 0, d.s, 0});
                 lv.smem_mid = std::max(lv.smem_mid, size_t(F + d.s) * sizeof(double2));
-                lv.smem_b = std::max(lv.smem_b, size_t(F) * sizeof(double2));
+                lv.smem_b = std::max(lv.smem_b, size_t(F + d.s) * sizeof(double2));
             } else {
-                const int rpt = kCT / 32;
+                const int rpt = env_int("HTG_ND_RPT", 8);
                 for (int r = 0; r < d.s; r += rpt) {
                     f1[dep].push_back({i, r, std::min(rpt, d.s - r), 0});
                     bw[dep].push_back({i, r, std::min(rpt, d.s - r), 0});
                 }
                 for (int r = 0; r < d.u; r += rpt) f2[dep].push_back({i, r, std::min(rpt, d.u - r), 0});
                 lv.smem_big = std::max(lv.smem_big, size_t(F) * sizeof(double2));
-                lv.smem_b = std::max(lv.smem_b, size_t(F) * sizeof(double2));
+                lv.smem_b = std::max(lv.smem_b, size_t(F + rpt) * sizeof(double2));
             }
         }
         for (int L = 0; L < D; ++L) {
             Level& lv = levels_[L];
-            lv.nsmall = int(sm[L].size());
+            lv.nwarp = int(wp[L].size());
             lv.nmid = int(md[L].size());
             lv.nf1 = int(f1[L].size());
             lv.nf2 = int(f2[L].size());
             lv.nb = int(bw[L].size());
-            lv.small = up(sm[L], st);
+            lv.warp = up(wp[L], st);
             lv.mid = up(md[L], st);
             lv.f1 = up(f1[L], st);
             lv.f2 = up(f2[L], st);

@@ -22,7 +22,7 @@ namespace htg {
 
 namespace {
 
-constexpr int kTM = 64, kTN = 64, kKC = 8, kLD = kKC + 4, kStages = 4, kThreads = 128;
+constexpr int kTM = 64, kTN = 64, kKC = 8, kLD = kKC + 4, kStages = 4, kThreads = 256;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -46,9 +46,10 @@ struct GemmSmem {
     double2 B[kStages][kTN][kLD];
 };
 
+// 8 warps, warp tile 32 (rows) x 16 (subdomains): 4 x 2 DMMA accumulator tiles
 template <int P>
-__global__ void __launch_bounds__(kThreads) k_dd_gemm(FineGeom g, DDDevice d, const double2* __restrict__ r,
-                                                      double2* __restrict__ ystage) {
+__global__ void __launch_bounds__(kThreads, 2) k_dd_gemm(FineGeom g, DDDevice d, const double2* __restrict__ r,
+                                                         double2* __restrict__ ystage) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     GemmSmem& sm = *reinterpret_cast<GemmSmem*>(smem_raw);
     const int4 tile = d.tiles[blockIdx.x];
@@ -59,10 +60,10 @@ __global__ void __launch_bounds__(kThreads) k_dd_gemm(FineGeom g, DDDevice d, co
     const double2* Bc = d.Bmat + (size_t)boff;
     const int* locg = d.loc_g + loff;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wm = warp >> 1, wn = warp & 1;
+    const int wm = warp >> 2, wn = warp & 3;
 
-    // producer assignment: A: rows tid/2, 4 k each; B: col tid/2, 4 k each
-    const int prow = tid >> 1, pk = (tid & 1) * 4;
+    // producer assignment: row/col tid/4, 2 k values each
+    const int prow = tid >> 2, pk = (tid & 3) * 2;
     const double2* arow = Bc + (size_t)(m0 + prow) * kpad;
     const int col = n0 + prow;
     const bool colok = col < ncol;
@@ -73,13 +74,16 @@ __global__ void __launch_bounds__(kThreads) k_dd_gemm(FineGeom g, DDDevice d, co
         oy = (so >> 16) * P;
     }
     const int nkc = kpad / kKC;
+    // m8 tiles of this warp that hold real U rows (the last M-tile is partial)
+    const int mt_valid = max(0, min(4, (nu - (m0 + wm * 32) + 7) / 8));
+    const bool nt_any = n0 + wn * 16 < ncol;
 
     auto load_stage = [&](int stage, int kc) {
         const int k0 = kc * kKC + pk;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) cp_async16(&sm.A[stage][prow][pk + i], arow + k0 + i, true);
+        for (int i = 0; i < 2; ++i) cp_async16(&sm.A[stage][prow][pk + i], arow + k0 + i, true);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < 2; ++i) {
             const int lg = locg[k0 + i];
             const bool ok = colok && lg >= 0;
             const double2* src = r;
@@ -88,11 +92,11 @@ __global__ void __launch_bounds__(kThreads) k_dd_gemm(FineGeom g, DDDevice d, co
         }
     };
 
-    double cr[4][4][2], cim[4][4][2];
+    double cr[4][2][2], cim[4][2][2];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
+        for (int b = 0; b < 2; ++b) {
             cr[a][b][0] = cr[a][b][1] = 0.0;
             cim[a][b][0] = cim[a][b][1] = 0.0;
         }
@@ -106,30 +110,39 @@ __global__ void __launch_bounds__(kThreads) k_dd_gemm(FineGeom g, DDDevice d, co
         cp_wait<kStages - 2>();
         __syncthreads();
         const int stage = kc % kStages;
-#pragma unroll
-        for (int ks = 0; ks < kKC / 4; ++ks) {
-            const int kk = ks * 4 + (lane & 3);
-            double2 af[4], bf[4];
-#pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                af[t] = sm.A[stage][wm * 32 + t * 8 + (lane >> 2)][kk];
-                bf[t] = sm.B[stage][wn * 32 + t * 8 + (lane >> 2)][kk];
-            }
-#pragma unroll
-            for (int mt = 0; mt < 4; ++mt) {
-                const double ar = af[mt].x, ai = af[mt].y, nai = -af[mt].y;
-#pragma unroll
-                for (int nt = 0; nt < 4; ++nt) {
-                    dmma(cr[mt][nt][0], cr[mt][nt][1], ar, bf[nt].x);
-                    dmma(cr[mt][nt][0], cr[mt][nt][1], nai, bf[nt].y);
-                    dmma(cim[mt][nt][0], cim[mt][nt][1], ar, bf[nt].y);
-                    dmma(cim[mt][nt][0], cim[mt][nt][1], ai, bf[nt].x);
-                }
-            }
-        }
         const int nxt = kc + kStages - 1;
         if (nxt < nkc) load_stage(nxt % kStages, nxt);
         cp_commit();
+        if (nt_any) {
+#pragma unroll
+            for (int ks = 0; ks < kKC / 4; ++ks) {
+                const int kk = ks * 4 + (lane & 3);
+                double2 af[4], bf[2];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) af[t] = sm.A[stage][wm * 32 + t * 8 + (lane >> 2)][kk];
+#pragma unroll
+                for (int t = 0; t < 2; ++t) bf[t] = sm.B[stage][wn * 16 + t * 8 + (lane >> 2)][kk];
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt) {
+                    if (mt >= mt_valid) break;
+#pragma unroll
+                    for (int nt = 0; nt < 2; ++nt) {
+                        dmma(cr[mt][nt][0], cr[mt][nt][1], af[mt].x, bf[nt].x);
+                        dmma(cim[mt][nt][0], cim[mt][nt][1], af[mt].x, bf[nt].y);
+                    }
+                }
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt) {
+                    if (mt >= mt_valid) break;
+                    const double nai = -af[mt].y;
+#pragma unroll
+                    for (int nt = 0; nt < 2; ++nt) {
+                        dmma(cr[mt][nt][0], cr[mt][nt][1], nai, bf[nt].y);
+                        dmma(cim[mt][nt][0], cim[mt][nt][1], af[mt].y, bf[nt].x);
+                    }
+                }
+            }
+        }
     }
     cp_wait<0>();
     // epilogue: C[row][col], row = lane/4, col = 2 (lane%4) + i
@@ -138,10 +151,10 @@ __global__ void __launch_bounds__(kThreads) k_dd_gemm(FineGeom g, DDDevice d, co
         const int row = m0 + wm * 32 + mt * 8 + (lane >> 2);
         if (row >= nu) continue;
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt)
+        for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
-                const int cc = n0 + wn * 32 + nt * 8 + 2 * (lane & 3) + i;
+                const int cc = n0 + wn * 16 + nt * 8 + 2 * (lane & 3) + i;
                 if (cc >= ncol) continue;
                 const int s = d.class_subs[sub0 + cc];
                 ystage[(size_t)s * d.nu_max + row] = make_double2(cr[mt][nt][i], cim[mt][nt][i]);
