@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <complex>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -121,6 +122,9 @@ struct htg_handle {
     cudaStream_t cap = nullptr;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
     bool use_graphs = true;
+    // GMRES workspace (allocated on first Krylov solve)
+    std::vector<double2*> krylov;
+    double2 *zero = nullptr, *hcol = nullptr, *gz = nullptr, *gt = nullptr;
     ~htg_handle() {
         for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
         if (cap) cudaStreamDestroy(cap);
@@ -347,10 +351,128 @@ int solve(htg_handle* H, const double2* f, double2* u, double* hist, int cap, in
     return gmres_solve(H, f, u, nf, hist, cap, iters, conv);
 }
 
+// Householder least squares min || H y - beta e1 || for the (m+1) x m
+// Hessenberg matrix (columns), the small solve of twogrid.cpp:318-320.
+std::vector<std::complex<double>> hessenberg_lstsq(std::vector<std::vector<std::complex<double>>> H, int rows,
+                                                   double beta) {
+    using C = std::complex<double>;
+    const int cols = int(H.size());
+    std::vector<C> b(rows, C(0.0));
+    b[0] = beta;
+    for (int k = 0; k < cols; ++k) {
+        double nrm = 0.0;
+        for (int i = k; i < rows; ++i) nrm += std::norm(H[k][i]);
+        nrm = std::sqrt(nrm);
+        if (nrm == 0.0) continue;
+        const C a = H[k][k];
+        const C alpha = (std::abs(a) > 0 ? -a / std::abs(a) : C(-1.0)) * nrm;
+        std::vector<C> v(rows, C(0.0));
+        for (int i = k; i < rows; ++i) v[i] = H[k][i];
+        v[k] -= alpha;
+        double vn = 0.0;
+        for (int i = k; i < rows; ++i) vn += std::norm(v[i]);
+        if (vn == 0.0) continue;
+        auto reflect = [&](std::vector<C>& x) {
+            C d = 0.0;
+            for (int i = k; i < rows; ++i) d += std::conj(v[i]) * x[i];
+            d *= 2.0 / vn;
+            for (int i = k; i < rows; ++i) x[i] -= d * v[i];
+        };
+        for (int j = k; j < cols; ++j) reflect(H[j]);
+        reflect(b);
+    }
+    std::vector<C> y(cols, C(0.0));
+    for (int k = cols - 1; k >= 0; --k) {
+        C s = b[k];
+        for (int j = k + 1; j < cols; ++j) s -= H[j][k] * y[j];
+        y[k] = (H[k][k] != C(0.0)) ? s / H[k][k] : C(0.0);
+    }
+    return y;
+}
+
+// GMRES on M A u = M f, M = one two-grid step from zero, no restart, true
+// residual every iteration (proj/core/src/twogrid.cpp:296-331). Krylov
+// vectors and the Gram-Schmidt coefficients stay on the device; one host
+// round trip per iteration reads the new Hessenberg column.
 int gmres_solve(htg_handle* H, const double2* f, double2* u, double nf, double* hist, int cap, int* iters,
                 int* conv) {
-    (void)H, (void)f, (void)u, (void)nf, (void)hist, (void)cap, (void)iters, (void)conv;
-    throw InvalidArgument("outer = krylov: GMRES not implemented on the GPU yet");
+    const int mmax = H->cfg.max_iters;
+    const long long n = H->ndof;
+    cudaStream_t st = H->st;
+    auto Qv = [&](int i) -> double2* {
+        while (int(H->krylov.size()) <= i) H->krylov.push_back(H->mem.alloc<double2>(n));
+        return H->krylov[i];
+    };
+    if (!H->zero) {
+        H->zero = H->mem.alloc<double2>(n);
+        H->gz = H->mem.alloc<double2>(n);
+        H->gt = H->mem.alloc<double2>(n);
+        H->hcol = H->mem.alloc<double2>(size_t(mmax) + 2);
+    }
+    vec_zero(H->zero, n, st);
+    double2* z = H->gz;  // preconditioner output (the step's own scratch is r, v, tmp)
+    double2* t = H->gt;  // -A q
+    // b = M f
+    vec_zero(z, n, st);
+    run_graph(H, 2, z, f, [&] { two_grid_step(H, z, f); });
+    vec_dot(z, z, n, H->partial, reinterpret_cast<double2*>(H->dscal + 8), st);
+    const double beta = std::sqrt(host_norm2(H, 8));
+    double2* q0 = Qv(0);
+    vec_zero(q0, n, st);
+    vec_axpy(q0, z, 1.0 / beta, n, st);
+    std::vector<std::vector<std::complex<double>>> Hcols;
+    std::vector<double2> hh(size_t(mmax) + 2);
+    for (int it = 1; it <= mmax; ++it) {
+        // w = M (A q_{it-1}) = -M(-A q)
+        residual(H, H->zero, Qv(it - 1), t, 0);  // t = -A q
+        vec_zero(z, n, st);
+        run_graph(H, 2, z, t, [&] { two_grid_step(H, z, t); });
+        double2* w = Qv(it);
+        vec_zero(w, n, st);
+        vec_axpy(w, z, -1.0, n, st);
+        // modified Gram-Schmidt, coefficients on the device
+        for (int i = 0; i < it; ++i) {
+            vec_dot(Qv(i), w, n, H->partial, H->hcol + i, st);  // conj(q_i) . w
+            vec_caxpy_dev(w, Qv(i), H->hcol + i, 1, n, st);     // w -= h_i q_i
+        }
+        vec_dot(w, w, n, H->partial, H->hcol + it, st);
+        HTG_CUDA(cudaMemcpyAsync(hh.data(), H->hcol, sizeof(double2) * (it + 1), cudaMemcpyDeviceToHost, st));
+        HTG_CUDA(cudaStreamSynchronize(st));
+        const double hn = std::sqrt(hh[it].x);
+        std::vector<std::complex<double>> col(it + 1);
+        for (int i = 0; i < it; ++i) col[i] = {hh[i].x, hh[i].y};
+        col[it] = hn;
+        if (hn > 1e-300) {
+            vec_zero(z, n, st);
+            vec_axpy(z, w, 1.0 / hn, n, st);
+            vec_copy(w, z, n, st);
+        } else {
+            vec_zero(w, n, st);
+        }
+        Hcols.push_back(col);
+        std::vector<std::vector<std::complex<double>>> Hs(it);
+        for (int c = 0; c < it; ++c) {
+            Hs[c] = Hcols[c];
+            Hs[c].resize(it + 1, 0.0);
+        }
+        const auto y = hessenberg_lstsq(Hs, it + 1, beta);
+        // u = sum y_i q_i; true residual
+        vec_zero(u, n, st);
+        std::vector<double2> yd(it);
+        for (int i = 0; i < it; ++i) yd[i] = make_double2(y[i].real(), y[i].imag());
+        HTG_CUDA(cudaMemcpyAsync(H->hcol, yd.data(), sizeof(double2) * it, cudaMemcpyHostToDevice, st));
+        for (int i = 0; i < it; ++i) vec_caxpy_dev(u, Qv(i), H->hcol + i, 0, n, st);
+        residual_norm2(H, f, u, 0);
+        const double rr = std::sqrt(host_norm2(H, 0)) / nf;
+        if (it - 1 < cap) hist[it - 1] = rr;
+        *iters = it;
+        if (rr <= H->cfg.stop_rel_residual || it == mmax) {
+            *conv = rr <= H->cfg.stop_rel_residual ? 1 : 0;
+            return *conv ? HTG_OK : HTG_NOT_CONVERGED;
+        }
+    }
+    *conv = 0;
+    return HTG_NOT_CONVERGED;
 }
 
 }  // namespace

@@ -23,6 +23,8 @@ CASES = {
     "p4_ldd3": (4, 3, 12, (A_, A_, A_, A_), (), {"l_dd": 3}),
     "p6_abs": (6, 3, 12, (A_, A_, A_, A_), (), {}),
     "p4_ndd2": (4, 3, 10, (A_, A_, A_, A_), (), {"n_dd": 2}),
+    "p4_krylov": (4, 4, 10, (A_, A_, A_, A_), (), {"outer": 1}),
+    "p2_krylov_dir": (2, 4, 8, (D_, A_, A_, A_), (), {"outer": 1}),
 }
 
 
@@ -141,3 +143,14 @@ def test_solve_iterations(case):
     assert rel(host(rg.u), ro.u) <= 1e-8
     rh = ops.solve_host(f)
     assert rh.iterations == rg.iterations and rel(rh.u, host(rg.u)) <= 1e-12
+
+
+@pytest.mark.parametrize("W", [20])
+def test_readme_krylov_iters_7(W):
+    """proj/README.md:89-102: Q4, 20 wavelengths, 10 ppw, krylov -> dofs=40401 iters=7."""
+    import paper_2509_17494_b200 as hb
+    torch = _torch()
+    prob = hb.build_problem(hb.ProblemSpec(order=4, wavelengths=W, ppw=10))
+    ops = hb.setup_two_grid(prob, hb.SolverConfig(outer=hb.KRYLOV))
+    res = ops.solve(torch.from_numpy(prob.rhs).cuda())
+    assert ops.ndof == 40401 and res.converged and res.iterations == 7
