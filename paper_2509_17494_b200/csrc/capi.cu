@@ -27,7 +27,7 @@ namespace htg {
 long long launch_count();
 void reset_launch_count();
 DDDevice upload_dd_impl(const DDSetup& dd, const HostProblem& hp, std::vector<void*>& allocs, size_t& bytes,
-                        cudaStream_t st, double2*& ystage);
+                        cudaStream_t st, double2*& ystage, std::vector<FdmClassDev>& fdm);
 }  // namespace htg
 
 using namespace htg;
@@ -106,6 +106,9 @@ struct htg_handle {
     int npart = 0;
     // subdomain solver
     DDDevice dd{};
+    std::vector<FdmClassDev> fdm;  // separable classes (fast diagonalisation)
+    FdmLaunch fdm_launch{};
+    double fdm_err = 0.0;
     int nclasses = 0;
     double dd_flops = 0.0;  // algorithmic 8 |U| |Omega| per subdomain, summed
     // coarse solver
@@ -204,7 +207,17 @@ void build_handle(htg_handle* H, const htg_problem& prob, const htg_config& cfg)
             const DDClass& c = dd.classes[dd.sub_class[sI]];
             H->dd_flops += 8.0 * c.nu * c.nloc;
         }
-        H->dd = upload_dd_impl(dd, hp, M.ptrs, M.bytes, st, H->ystage);
+        H->dd = upload_dd_impl(dd, hp, M.ptrs, M.bytes, st, H->ystage, H->fdm);
+        for (const DDClass& c : dd.classes)
+            if (c.fdm) H->fdm_err = std::max(H->fdm_err, c.fdm_err);
+        if (!H->fdm.empty()) {
+            int nsm = 0;
+            HTG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
+            const std::vector<int4> work = fdm_work_table(H->fdm, nsm);  // sets FdmClassDev::first
+            H->fdm_launch.classes = M.upload(H->fdm, st);
+            H->fdm_launch.work = M.upload(work, st);
+            H->fdm_launch.nwork = int(work.size());
+        }
     }
     if (cfg.coarsening == HTG_COARSE_OPTIMIZED_FD) H->coarse = make_coarse_solver(hp, st);
     HTG_CUDA(cudaStreamCreateWithFlags(&H->cap, cudaStreamNonBlocking));
@@ -285,6 +298,13 @@ void residual_restrict(htg_handle* H, const double2* f, const double2* u, double
     k1_launch(kK1Restrict, a, H->st);
 }
 
+// all subdomain solves of a sweep: dense classes as one batched GEMM, separable
+// classes by fast diagonalisation; outputs land in the U-row staging buffer
+void subdomain_solves(htg_handle* H, const double2* gvec) {
+    dd_gemm_launch(H->g, H->dd, gvec, H->ystage, H->st);
+    dd_fdm_launch(H->g, H->fdm_launch, gvec, H->ystage, H->dd.nu_max, H->st);
+}
+
 // out = dd_step(u, f): g = f - A_s u (skipped when u is null, i.e. zero)
 void dd_step(htg_handle* H, const double2* u, const double2* f, double2* out) {
     const double2* gvec = f;
@@ -292,7 +312,7 @@ void dd_step(htg_handle* H, const double2* u, const double2* f, double2* out) {
         residual(H, f, u, H->tmp, 1);
         gvec = H->tmp;
     }
-    dd_gemm_launch(H->g, H->dd, gvec, H->ystage, H->st);
+    subdomain_solves(H, gvec);
     dd_combine_launch(H->g, H->dd, H->ystage, u, out, H->st);
 }
 
@@ -301,7 +321,7 @@ void csdd(htg_handle* H, double2* u, const double2* f) {
     residual(H, f, u, H->r, 0);
     if (H->cfg.n_dd == 1) {
         // v = dd_step(0, r) and u += v fused into the combine
-        dd_gemm_launch(H->g, H->dd, H->r, H->ystage, H->st);
+        subdomain_solves(H, H->r);
         dd_combine_launch(H->g, H->dd, H->ystage, u, u, H->st);
         return;
     }
@@ -665,7 +685,7 @@ int htg_profile(htg_handle* h, double* u, const double* f, int reps, double* ms)
             return double(t) / reps;
         };
         ms[0] = timeit([&] { residual(h, Fv, U, h->r, 0); });
-        ms[1] = timeit([&] { dd_gemm_launch(h->g, h->dd, h->r, h->ystage, h->st); });
+        ms[1] = timeit([&] { subdomain_solves(h, h->r); });
         ms[2] = timeit([&] { dd_combine_launch(h->g, h->dd, h->ystage, U, h->v, h->st); });
         ms[3] = h->coarse ? timeit([&] { residual_restrict(h, Fv, U, h->rc); }) : 0.0;
         ms[4] = h->coarse ? timeit([&] { h->coarse->solve(h->rc, h->uc, h->st); }) : 0.0;

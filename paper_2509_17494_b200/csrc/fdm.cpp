@@ -1,0 +1,296 @@
+// fdm.cpp -- fast diagonalisation of separable subdomain operators (host setup).
+//
+// A subdomain class whose Omega cells share one (k, eps) and whose sides are
+// absorbing or Neumann has the exact tensor form
+//   A_s^(Omega) = Kx (x) My + Mx (x) Ky,
+//   Kx = Sx - i k h Ex,  Ky = Sy - i k h Ey - m My,  m = (k^2 (1 + i alpha_s) + i eps) h^2,
+// (Ex, Ey: the absorbing end points; S, M: the 1-D hierarchical stiffness and
+// mass assembled over the Omega cells). With the generalised eigenpairs
+// K V = M V Lambda, V^T M V = I in each direction,
+//   A^-1 = (Vx (x) Vy) diag(1 / (lx_i + ly_j)) (Vx (x) Vy)^T,
+// so the U rows of A^-1 g cost four small dense products instead of one
+// |U| x |Omega| product. The factors are validated against the dense
+// restricted inverse of the same class before use.
+#include <algorithm>
+#include <cmath>
+#include <complex>
+
+#include "setup.hpp"
+
+namespace htg {
+
+namespace {
+
+using Mat = std::vector<cplx>;  // row-major n x n
+
+// Eigen-decomposition of a general complex matrix: Householder Hessenberg
+// reduction, shifted QR (Wilkinson shifts, deflation) to the complex Schur
+// form, eigenvectors of the triangular factor by back substitution.
+bool complex_eig(int n, Mat A, std::vector<cplx>& lam, Mat& X) {
+    auto at = [n](Mat& M, int i, int j) -> cplx& { return M[size_t(i) * n + j]; };
+    Mat Q(size_t(n) * n, cplx(0.0));
+    for (int i = 0; i < n; ++i) at(Q, i, i) = 1.0;
+    // Hessenberg reduction
+    for (int k = 0; k < n - 2; ++k) {
+        double alpha2 = 0.0;
+        for (int i = k + 1; i < n; ++i) alpha2 += std::norm(at(A, i, k));
+        const double alpha = std::sqrt(alpha2);
+        if (alpha == 0.0) continue;
+        std::vector<cplx> v(n, cplx(0.0));
+        const cplx x0 = at(A, k + 1, k);
+        const cplx ph = std::abs(x0) > 0 ? x0 / std::abs(x0) : cplx(1.0);
+        for (int i = k + 1; i < n; ++i) v[i] = at(A, i, k);
+        v[k + 1] += ph * alpha;
+        double vn = 0.0;
+        for (int i = k + 1; i < n; ++i) vn += std::norm(v[i]);
+        if (vn == 0.0) continue;
+        // A = H A H, H = I - 2 v v^H / vn ; Q = Q H
+        for (int j = 0; j < n; ++j) {
+            cplx d = 0.0;
+            for (int i = k + 1; i < n; ++i) d += std::conj(v[i]) * at(A, i, j);
+            d *= 2.0 / vn;
+            for (int i = k + 1; i < n; ++i) at(A, i, j) -= d * v[i];
+        }
+        for (int i = 0; i < n; ++i) {
+            cplx d = 0.0;
+            for (int j = k + 1; j < n; ++j) d += at(A, i, j) * v[j];
+            d *= 2.0 / vn;
+            for (int j = k + 1; j < n; ++j) at(A, i, j) -= d * std::conj(v[j]);
+        }
+        for (int i = 0; i < n; ++i) {
+            cplx d = 0.0;
+            for (int j = k + 1; j < n; ++j) d += at(Q, i, j) * v[j];
+            d *= 2.0 / vn;
+            for (int j = k + 1; j < n; ++j) at(Q, i, j) -= d * std::conj(v[j]);
+        }
+    }
+    // shifted QR on the Hessenberg matrix with Givens rotations
+    int hi = n - 1, iter = 0;
+    while (hi > 0) {
+        if (++iter > 100 * n) return false;
+        int lo = hi;
+        while (lo > 0) {
+            const double s = std::abs(at(A, lo - 1, lo - 1)) + std::abs(at(A, lo, lo));
+            if (std::abs(at(A, lo, lo - 1)) <= 1e-15 * (s > 0 ? s : 1.0)) {
+                at(A, lo, lo - 1) = 0.0;
+                break;
+            }
+            --lo;
+        }
+        if (lo == hi) {
+            --hi;
+            iter = 0;
+            continue;
+        }
+        // Wilkinson shift from the trailing 2x2 block
+        const cplx a = at(A, hi - 1, hi - 1), b = at(A, hi - 1, hi), c = at(A, hi, hi - 1), d = at(A, hi, hi);
+        const cplx tr = a + d, det = a * d - b * c;
+        const cplx disc = std::sqrt(tr * tr / 4.0 - det);
+        cplx mu1 = tr / 2.0 + disc, mu2 = tr / 2.0 - disc;
+        cplx mu = std::abs(mu1 - d) < std::abs(mu2 - d) ? mu1 : mu2;
+        if (iter % 11 == 10) mu += std::abs(at(A, hi, hi - 1));  // exceptional shift
+        for (int i = lo; i <= hi; ++i) at(A, i, i) -= mu;
+        std::vector<cplx> cs(hi - lo), sn(hi - lo);
+        for (int k = lo; k < hi; ++k) {
+            const cplx x = at(A, k, k), y = at(A, k + 1, k);
+            const double r = std::sqrt(std::norm(x) + std::norm(y));
+            cplx cc = 1.0, ss = 0.0;
+            if (r > 0) {
+                cc = x / r;
+                ss = y / r;
+            }
+            cs[k - lo] = cc;
+            sn[k - lo] = ss;
+            // rows k, k+1: G^H applied from the left
+            for (int j = k; j < n; ++j) {
+                const cplx p = at(A, k, j), q = at(A, k + 1, j);
+                at(A, k, j) = std::conj(cc) * p + std::conj(ss) * q;
+                at(A, k + 1, j) = -ss * p + cc * q;
+            }
+        }
+        for (int k = lo; k < hi; ++k) {
+            const cplx cc = cs[k - lo], ss = sn[k - lo];
+            for (int i = 0; i <= std::min(k + 2, n - 1); ++i) {
+                const cplx p = at(A, i, k), q = at(A, i, k + 1);
+                at(A, i, k) = p * cc + q * ss;
+                at(A, i, k + 1) = -p * std::conj(ss) + q * std::conj(cc);
+            }
+            for (int i = 0; i < n; ++i) {
+                const cplx p = at(Q, i, k), q = at(Q, i, k + 1);
+                at(Q, i, k) = p * cc + q * ss;
+                at(Q, i, k + 1) = -p * std::conj(ss) + q * std::conj(cc);
+            }
+        }
+        for (int i = lo; i <= hi; ++i) at(A, i, i) += mu;
+    }
+    lam.resize(n);
+    for (int i = 0; i < n; ++i) lam[i] = at(A, i, i);
+    // eigenvectors of the upper triangular T, then X = Q Y
+    Mat Y(size_t(n) * n, cplx(0.0));
+    double tnorm = 0.0;
+    for (auto& z : A) tnorm = std::max(tnorm, std::abs(z));
+    for (int k = 0; k < n; ++k) {
+        at(Y, k, k) = 1.0;
+        for (int j = k - 1; j >= 0; --j) {
+            cplx s = 0.0;
+            for (int l = j + 1; l <= k; ++l) s += at(A, j, l) * at(Y, l, k);
+            cplx den = at(A, j, j) - lam[k];
+            if (std::abs(den) < 1e-14 * tnorm) den = 1e-14 * tnorm;
+            at(Y, j, k) = -s / den;
+        }
+    }
+    X.assign(size_t(n) * n, cplx(0.0));
+    for (int i = 0; i < n; ++i)
+        for (int k = 0; k < n; ++k) {
+            cplx s = 0.0;
+            for (int l = 0; l <= k; ++l) s += at(Q, i, l) * at(Y, l, k);
+            at(X, i, k) = s;
+        }
+    return true;
+}
+
+// K V = M V Lambda with V^T M V = I (M real SPD, K complex symmetric)
+bool gen_eig(int n, const Mat& K, const std::vector<double>& M, std::vector<cplx>& lam, Mat& V) {
+    // Cholesky M = L L^T
+    std::vector<double> L(size_t(n) * n, 0.0);
+    for (int j = 0; j < n; ++j) {
+        double s = M[size_t(j) * n + j];
+        for (int k = 0; k < j; ++k) s -= L[size_t(j) * n + k] * L[size_t(j) * n + k];
+        if (s <= 0.0) return false;
+        L[size_t(j) * n + j] = std::sqrt(s);
+        for (int i = j + 1; i < n; ++i) {
+            double t = M[size_t(i) * n + j];
+            for (int k = 0; k < j; ++k) t -= L[size_t(i) * n + k] * L[size_t(j) * n + k];
+            L[size_t(i) * n + j] = t / L[size_t(j) * n + j];
+        }
+    }
+    // C = L^-1 K L^-T
+    Mat C = K;
+    for (int col = 0; col < n; ++col)  // C <- L^-1 C (forward substitution per column)
+        for (int i = 0; i < n; ++i) {
+            cplx s = C[size_t(i) * n + col];
+            for (int k = 0; k < i; ++k) s -= L[size_t(i) * n + k] * C[size_t(k) * n + col];
+            C[size_t(i) * n + col] = s / L[size_t(i) * n + i];
+        }
+    for (int row = 0; row < n; ++row)  // C <- C L^-T (per row)
+        for (int j = 0; j < n; ++j) {
+            cplx s = C[size_t(row) * n + j];
+            for (int k = 0; k < j; ++k) s -= C[size_t(row) * n + k] * L[size_t(j) * n + k];
+            C[size_t(row) * n + j] = s / L[size_t(j) * n + j];
+        }
+    Mat X;
+    if (!complex_eig(n, C, lam, X)) return false;
+    // V = L^-T X, then V^T M V = I normalisation (transpose, not adjoint)
+    V.assign(size_t(n) * n, cplx(0.0));
+    for (int k = 0; k < n; ++k)
+        for (int i = n - 1; i >= 0; --i) {
+            cplx s = X[size_t(i) * n + k];
+            for (int j = i + 1; j < n; ++j) s -= L[size_t(j) * n + i] * V[size_t(j) * n + k];
+            V[size_t(i) * n + k] = s / L[size_t(i) * n + i];
+        }
+    for (int k = 0; k < n; ++k) {
+        cplx q = 0.0;
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j) q += V[size_t(i) * n + k] * M[size_t(i) * n + j] * V[size_t(j) * n + k];
+        if (std::abs(q) < 1e-12) return false;  // quasi-null vector: not diagonalisable this way
+        const cplx s = 1.0 / std::sqrt(q);
+        for (int i = 0; i < n; ++i) V[size_t(i) * n + k] *= s;
+    }
+    return true;
+}
+
+}  // namespace
+
+bool build_fdm(const HostProblem& hp, const Basis1D& b, double alpha_s, int ox, int oy, DDClass& c) {
+    const int p = hp.p;
+    // separable: one (k, eps) in Omega, no Dirichlet side
+    const double k0 = hp.kc(ox, oy), e0 = hp.ec(ox, oy);
+    for (int y = oy; y < oy + c.ony; ++y)
+        for (int x = ox; x < ox + c.onx; ++x)
+            if (hp.kc(x, y) != k0 || hp.ec(x, y) != e0) return false;
+    auto side_tag = [&](char s, int i) -> int8_t {
+        switch (s) {
+            case 'b': return oy == 0 ? hp.tb[ox + i] : kAbsorbing;
+            case 't': return oy + c.ony == hp.ny ? hp.tt[ox + i] : kAbsorbing;
+            case 'l': return ox == 0 ? hp.tl[oy + i] : kAbsorbing;
+            default: return ox + c.onx == hp.nx ? hp.tr[oy + i] : kAbsorbing;
+        }
+    };
+    int8_t sides[4];
+    const char names[4] = {'l', 'r', 'b', 't'};
+    for (int s = 0; s < 4; ++s) {
+        const int cnt = s < 2 ? c.ony : c.onx;
+        sides[s] = side_tag(names[s], 0);
+        for (int i = 1; i < cnt; ++i)
+            if (side_tag(names[s], i) != sides[s]) return false;
+        if (sides[s] == kDirichlet) return false;
+    }
+    const double kh = k0 * hp.h;
+    const cplx m = cplx(k0 * k0, k0 * k0 * alpha_s + e0) * hp.h * hp.h;
+    auto assemble1d = [&](int ncell, std::vector<double>& S, std::vector<double>& M) {
+        const int n = ncell * p + 1;
+        S.assign(size_t(n) * n, 0.0);
+        M.assign(size_t(n) * n, 0.0);
+        for (int cI = 0; cI < ncell; ++cI) {
+            auto li = [&](int a) { return a == 0 ? cI * p : (a == 1 ? (cI + 1) * p : cI * p + a - 1); };
+            for (int a = 0; a <= p; ++a)
+                for (int d = 0; d <= p; ++d) {
+                    S[size_t(li(a)) * n + li(d)] += b.S[a][d];
+                    M[size_t(li(a)) * n + li(d)] += b.M[a][d];
+                }
+        }
+    };
+    std::vector<double> Sx, Mx, Sy, My;
+    assemble1d(c.onx, Sx, Mx);
+    assemble1d(c.ony, Sy, My);
+    const int nx = c.onx * p + 1, ny = c.ony * p + 1;
+    Mat Kx(size_t(nx) * nx), Ky(size_t(ny) * ny);
+    for (size_t i = 0; i < Kx.size(); ++i) Kx[i] = Sx[i];
+    for (size_t i = 0; i < Ky.size(); ++i) Ky[i] = Sy[i] - m * My[i];
+    if (sides[0] == kAbsorbing) Kx[0] += cplx(0.0, -kh);
+    if (sides[1] == kAbsorbing) Kx[size_t(nx) * nx - 1] += cplx(0.0, -kh);
+    if (sides[2] == kAbsorbing) Ky[0] += cplx(0.0, -kh);
+    if (sides[3] == kAbsorbing) Ky[size_t(ny) * ny - 1] += cplx(0.0, -kh);
+    std::vector<cplx> lx, ly;
+    Mat Vx, Vy;
+    if (!gen_eig(nx, Kx, Mx, lx, Vx) || !gen_eig(ny, Ky, My, ly, Vy)) return false;
+    c.fdm_nx = nx;
+    c.fdm_ny = ny;
+    c.fdm_ux0 = c.ux * p;
+    c.fdm_uy0 = c.uy * p;
+    c.fdm_nux = c.unx * p + 1;
+    c.fdm_nuy = c.uny * p + 1;
+    c.Vx = Vx;
+    c.Vy = Vy;
+    c.Dinv.assign(size_t(nx) * ny, cplx(0.0));
+    for (int i = 0; i < nx; ++i)
+        for (int j = 0; j < ny; ++j) c.Dinv[size_t(i) * ny + j] = 1.0 / (lx[i] + ly[j]);
+    // validate against the dense restricted inverse: B = Vx_U (x) Vy_U Dinv (Vx (x) Vy)^T
+    double err = 0.0, ref = 0.0;
+    for (int rI = 0; rI < c.nu; ++rI) {
+        const int l = c.umem[rI];
+        int gx = -1, gy = -1;
+        for (int yy = 0; yy < ny && gx < 0; ++yy)
+            for (int xx = 0; xx < nx; ++xx)
+                if (dof_index(c.onx, c.ony, p, xx, yy) == l) {
+                    gx = xx;
+                    gy = yy;
+                    break;
+                }
+        for (int jy = 0; jy < ny; ++jy)
+            for (int jx = 0; jx < nx; ++jx) {
+                cplx s = 0.0;
+                for (int i = 0; i < nx; ++i)
+                    for (int j = 0; j < ny; ++j)
+                        s += Vx[size_t(gx) * nx + i] * Vy[size_t(gy) * ny + j] * c.Dinv[size_t(i) * ny + j] *
+                             Vx[size_t(jx) * nx + i] * Vy[size_t(jy) * ny + j];
+                const cplx want = c.B[size_t(rI) * c.nloc + dof_index(c.onx, c.ony, p, jx, jy)];
+                err = std::max(err, std::abs(s - want));
+                ref = std::max(ref, std::abs(want));
+            }
+    }
+    c.fdm_err = err / ref;
+    return c.fdm_err < 1e-11;
+}
+
+}  // namespace htg

@@ -238,6 +238,7 @@ __global__ void k_dd_combine(FineGeom g, DDDevice d, const double2* __restrict__
 }  // namespace
 
 void dd_gemm_launch(const FineGeom& g, const DDDevice& d, const double2* r, double2* ystage, cudaStream_t st) {
+    if (d.ntiles == 0) return;
     const size_t smem = sizeof(GemmSmem);
     static bool attr[9] = {};
     auto go = [&](auto kern, int p) {
@@ -274,7 +275,7 @@ void dd_combine_launch(const FineGeom& g, const DDDevice& d, const double2* ysta
 // Host: lay the classes out for the kernels (padded B_c, local gather tables,
 // U-row maps, tile list) and upload.
 DDDevice upload_dd_impl(const DDSetup& dd, const HostProblem& hp, std::vector<void*>& allocs, size_t& bytes,
-                        cudaStream_t st, double2*& ystage) {
+                        cudaStream_t st, double2*& ystage, std::vector<FdmClassDev>& fdm) {
     DDDevice d;
     const int nc = int(dd.classes.size());
     d.nclass = nc;
@@ -319,6 +320,38 @@ DDDevice upload_dd_impl(const DDSetup& dd, const HostProblem& hp, std::vector<vo
         rowmap.insert(rowmap.end(), rm.begin(), rm.end());
         const int off = int(class_subs.size());
         class_subs.insert(class_subs.end(), subs[ci].begin(), subs[ci].end());
+        if (c.fdm && c.fdm_nx <= 32 && c.fdm_ny <= 32 && p <= 4) {
+            FdmClassDev f{};
+            f.nx = c.fdm_nx;
+            f.ny = c.fdm_ny;
+            f.nux = c.fdm_nux;
+            f.nuy = c.fdm_nuy;
+            f.ux0 = c.fdm_ux0;
+            f.uy0 = c.fdm_uy0;
+            f.onx = c.onx;
+            f.ony = c.ony;
+            f.nsub = int(subs[ci].size());
+            f.rowmap = reinterpret_cast<const int*>(size_t(in[6]));  // offsets, patched below
+            f.subs = reinterpret_cast<const int*>(size_t(off));
+            std::vector<double2> vx(c.Vx.size()), vy(c.Vy.size()), dv(c.Dinv.size());
+            for (size_t i = 0; i < vx.size(); ++i) vx[i] = make_double2(c.Vx[i].real(), c.Vx[i].imag());
+            for (size_t i = 0; i < vy.size(); ++i) vy[i] = make_double2(c.Vy[i].real(), c.Vy[i].imag());
+            for (size_t i = 0; i < dv.size(); ++i) dv[i] = make_double2(c.Dinv[i].real(), c.Dinv[i].imag());
+            auto put = [&](const std::vector<double2>& v) {
+                void* ptr = nullptr;
+                HTG_CUDA(cudaMalloc(&ptr, v.size() * sizeof(double2)));
+                allocs.push_back(ptr);
+                bytes += v.size() * sizeof(double2);
+                HTG_CUDA(cudaMemcpyAsync(ptr, v.data(), v.size() * sizeof(double2), cudaMemcpyHostToDevice, st));
+                HTG_CUDA(cudaStreamSynchronize(st));
+                return static_cast<const double2*>(ptr);
+            };
+            f.Vx = put(vx);
+            f.Vy = put(vy);
+            f.Dinv = put(dv);
+            fdm.push_back(f);
+            continue;
+        }
         for (int m0 = 0; m0 < c.nu; m0 += kTM)
             for (int n0 = 0; n0 < int(subs[ci].size()); n0 += kTN) tiles.push_back(make_int4(ci, m0, n0, off));
     }
@@ -347,6 +380,11 @@ DDDevice upload_dd_impl(const DDSetup& dd, const HostProblem& hp, std::vector<vo
     d.class_subs = up(class_subs);
     d.ntiles = int(tiles.size());
     d.nu_max = nu_max;
+    for (FdmClassDev& f : fdm) {  // patch offsets into device pointers
+        f.rowmap = d.rowmap + size_t(f.rowmap);
+        f.subs = d.class_subs + size_t(f.subs);
+        f.sub_o = d.sub_o;
+    }
     void* ys = nullptr;
     const size_t ysz = size_t(d.nsub) * nu_max * sizeof(double2);
     HTG_CUDA(cudaMalloc(&ys, std::max<size_t>(ysz, 16)));

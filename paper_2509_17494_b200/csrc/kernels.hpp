@@ -3,6 +3,8 @@
 
 #include <cuda_runtime.h>
 
+#include <vector>
+
 #include "common.hpp"
 
 namespace htg {
@@ -64,6 +66,24 @@ struct DDDevice {
     const int* class_subs;    // subdomains of each class, contiguous
 };
 void dd_gemm_launch(const FineGeom& g, const DDDevice& d, const double2* r, double2* ystage, cudaStream_t st);
+// separable classes: fast-diagonalisation subdomain solves (k_fdm.cu)
+struct FdmClassDev {
+    const double2 *Vx, *Vy, *Dinv;
+    int nx, ny, nux, nuy, ux0, uy0, onx, ony;
+    const int* rowmap;  // local Omega dof -> U row
+    const int* subs;    // subdomains of the class
+    const int* sub_o;   // Omega origin per subdomain
+    int nsub;
+    int first;          // offset of this class in the class-sorted subdomain list
+};
+struct FdmLaunch {
+    const FdmClassDev* classes;  // device copy of the class table
+    const int4* work;            // per CTA: class, first subdomain, count
+    int nwork;
+};
+void dd_fdm_launch(const FineGeom& g, const FdmLaunch& L, const double2* r, double2* ystage, int nu_max,
+                   cudaStream_t st);
+std::vector<int4> fdm_work_table(std::vector<FdmClassDev>& cls, int nsm);
 // out = u + sum_i y_i / L (u may be null -> 0); out may alias u
 void dd_combine_launch(const FineGeom& g, const DDDevice& d, const double2* ystage, const double2* u, double2* out,
                        cudaStream_t st);

@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <map>
 #include <thread>
 
@@ -447,6 +448,8 @@ DDSetup build_dd(const HostProblem& hp, const Basis1D& b, double alpha_s, int l_
             c.B.resize(size_t(c.nu) * n);
             for (int r = 0; r < c.nu; ++r)
                 for (int l = 0; l < n; ++l) c.B[size_t(r) * n + l] = X[size_t(l) * c.nu + r];
+            const char* fdm_env = std::getenv("HTG_FDM");
+            if (!(fdm_env && fdm_env[0] == '0')) c.fdm = build_fdm(hp, b, alpha_s, first[ci].ox, first[ci].oy, c);
         } catch (...) {
             errs[ci] = std::current_exception();
         }

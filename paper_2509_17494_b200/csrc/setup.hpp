@@ -59,7 +59,18 @@ struct DDClass {
     int nloc = 0, nu = 0;       // |Omega dofs|, |U dofs|
     std::vector<int> umem;      // local Omega index of each U row
     std::vector<cplx> B;        // nu x nloc, row-major
+    // fast diagonalisation (separable classes): A^-1 = (Vx (x) Vy) Dinv (Vx (x) Vy)^T
+    bool fdm = false;
+    int fdm_nx = 0, fdm_ny = 0;    // 1-D local index ranges of Omega
+    int fdm_ux0 = 0, fdm_uy0 = 0;  // first 1-D index of U
+    int fdm_nux = 0, fdm_nuy = 0;  // 1-D extent of U
+    std::vector<cplx> Vx, Vy;      // (nx x nx), (ny x ny) row-major, columns are eigenvectors
+    std::vector<cplx> Dinv;        // nx x ny
+    double fdm_err = 0.0;          // max |B_fdm - B| / max |B| over the class
 };
+// Build the FDM factors of a class whose first subdomain's Omega starts at
+// cell (ox, oy); false if the class is not separable or fails validation.
+bool build_fdm(const HostProblem& hp, const Basis1D& b, double alpha_s, int ox, int oy, DDClass& c);
 struct DDSetup {
     int l_dd = 4;
     int nbx = 0, nby = 0;  // blocks per direction
