@@ -80,8 +80,11 @@ int htg_destroy(htg_handle* h);
 
 /* out[0] ndof, [1] coarse ndof, [2] subdomains, [3] subdomain classes,
  * [4] device bytes held, [5] coarse factor bytes, [6] nx, [7] ny, [8] order,
- * [9] algorithmic flops of one batched subdomain sweep (8 |U_i| |Omega_i| summed),
- * [10] nested-dissection levels of the coarse solver. out must hold 11 entries. */
+ * [9] algorithmic flops of one sweep's subdomain solves on the path used
+ * (fast diagonalisation for separable classes, 8 |U_i| |Omega_i| otherwise),
+ * [10] nested-dissection levels of the coarse solver, [11] the dense-path
+ * flops 8 |U_i| |Omega_i| summed, [12] subdomains solved by fast
+ * diagonalisation. out must hold 13 entries. */
 int htg_info(const htg_handle* h, long long* out);
 int htg_set_stream(htg_handle* h, void* stream);
 

@@ -110,7 +110,9 @@ struct htg_handle {
     FdmLaunch fdm_launch{};
     double fdm_err = 0.0;
     int nclasses = 0;
-    double dd_flops = 0.0;  // algorithmic 8 |U| |Omega| per subdomain, summed
+    double dd_flops = 0.0;        // algorithmic flops of one sweep's subdomain solves (path used)
+    double dd_flops_dense = 0.0;  // 8 |U| |Omega| per subdomain, summed (dense path)
+    long long fdm_subs = 0;       // subdomains solved by fast diagonalisation
     // coarse solver
     std::unique_ptr<CoarseSolver> coarse;
     // pinned host scalars
@@ -205,7 +207,14 @@ void build_handle(htg_handle* H, const htg_problem& prob, const htg_config& cfg)
         H->nclasses = int(dd.classes.size());
         for (int sI = 0; sI < int(dd.sub_class.size()); ++sI) {
             const DDClass& c = dd.classes[dd.sub_class[sI]];
-            H->dd_flops += 8.0 * c.nu * c.nloc;
+            H->dd_flops_dense += 8.0 * c.nu * c.nloc;
+            if (c.fdm && c.fdm_nx <= 32 && c.fdm_ny <= 32 && hp.p <= 4) {
+                const double nx = c.fdm_nx, ny = c.fdm_ny, ux = c.fdm_nux, uy = c.fdm_nuy;
+                H->dd_flops += 8.0 * (nx * nx * ny + nx * ny * ny + ux * nx * ny + ux * ny * uy);
+                H->fdm_subs += 1;
+            } else {
+                H->dd_flops += 8.0 * c.nu * c.nloc;
+            }
         }
         H->dd = upload_dd_impl(dd, hp, M.ptrs, M.bytes, st, H->ystage, H->fdm);
         for (const DDClass& c : dd.classes)
@@ -553,6 +562,8 @@ int htg_info(const htg_handle* h, long long* out) {
         out[8] = h->hp.p;
         out[9] = (long long)h->dd_flops;
         out[10] = h->coarse ? h->coarse->levels() : 0;
+        out[11] = (long long)h->dd_flops_dense;
+        out[12] = h->fdm_subs;
     });
 }
 

@@ -197,12 +197,14 @@ class TwoGridOperators:
         st = C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
         check(L.htg_create(C.byref(cp), C.byref(cfg), st, C.byref(h)))
         self._h = h
-        info = (C.c_longlong * 11)()
+        info = (C.c_longlong * 13)()
         check(L.htg_info(h, info))
         (self.ndof, self.coarse_ndof, self.n_subdomains, self.n_classes, self.device_bytes,
          self.coarse_factor_bytes) = (int(v) for v in info[:6])
         self.dd_flops = int(info[9])
         self.coarse_levels = int(info[10])
+        self.dd_flops_dense = int(info[11])
+        self.fdm_subdomains = int(info[12])
 
     def close(self):
         if getattr(self, "_h", None):
