@@ -302,16 +302,19 @@ void factor_node(NDTree& t, int id, const std::vector<cplx>& A9, std::vector<int
 }
 
 // ------------------------------------------------------------------ GPU solve
-struct Task {
-    int node, r0, nr, pad;
-};
 struct NodeDev {
     int s, u;
     long long off_F, off_L, off_U, off_Z;  // into the factor buffer (row-major blocks)
     int off_var, off_ring;                 // into idx
     int off_front;                         // front scratch (s+u)
     int off_contrib;                       // contribution vector (u)
-    int child0, nchild;                    // into child list
+    int off_gsrc;                          // per front position: <= 2 child contribution indices
+    int pad;
+};
+// a launch's work item carries its front descriptor (no dependent load at start)
+struct Task {
+    NodeDev nd;
+    int r0, nr;
 };
 
 constexpr int kCT = 256;     // threads per CTA (8 warps)
@@ -327,11 +330,8 @@ __device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {
 }
 
 struct NDArgs {
-    const NodeDev* nodes;
     const int* idx;
-    const int* children;
-    const int* cmaps;
-    const long long* cmap_off;
+    const int2* gsrc;
     const double2* fac;
     const double2* rc;
     double2* contrib;
@@ -380,35 +380,37 @@ __device__ __forceinline__ void rows_dot(const double2* __restrict__ M, int len,
     }
 }
 
-// front vector v = [rc(vars); 0] + extend-add of the children's contribution
-// vectors, children summed in a fixed order
+// front vector v = [rc(vars); 0] + the children's contribution vectors (each
+// position has at most two, added in child order), one pass, no barrier inside
 template <int STRIDE, class Sync>
 __device__ void gather_front(const NDArgs& a, const NodeDev& nd, double2* sv, int t, Sync&& sync) {
     const int F = nd.s + nd.u;
-    for (int i = t; i < F; i += STRIDE) sv[i] = i < nd.s ? a.rc[a.idx[nd.off_var + i]] : make_double2(0.0, 0.0);
-    sync();
-    for (int c = 0; c < nd.nchild; ++c) {
-        const int ch = a.children[nd.child0 + c];
-        const NodeDev cn = a.nodes[ch];
-        const int* mp = a.cmaps + a.cmap_off[ch];
-        for (int k = t; k < cn.u; k += STRIDE) {
-            const double2 v = a.contrib[cn.off_contrib + k];
-            double2& d = sv[mp[k]];
-            d.x += v.x;
-            d.y += v.y;
+    for (int i = t; i < F; i += STRIDE) {
+        double2 v = i < nd.s ? a.rc[a.idx[nd.off_var + i]] : make_double2(0.0, 0.0);
+        const int2 src = a.gsrc[nd.off_gsrc + i];
+        if (src.x >= 0) {
+            const double2 c = a.contrib[src.x];
+            v.x += c.x;
+            v.y += c.y;
         }
-        sync();
+        if (src.y >= 0) {
+            const double2 c = a.contrib[src.y];
+            v.x += c.x;
+            v.y += c.y;
+        }
+        sv[i] = v;
     }
+    sync();
 }
 
 // forward: y1 = (L^-1 P) v1, c = v2 - L21 y1. Warp tier: one warp per front.
-__global__ void __launch_bounds__(kCT) k_nd_fwd_warp(const int* __restrict__ list, int n, NDArgs a) {
+__global__ void __launch_bounds__(kCT) k_nd_fwd_warp(const NodeDev* __restrict__ list, int n, NDArgs a) {
     __shared__ double2 sv[kCT / 32][kWarpFMax];
     __shared__ double2 sy[kCT / 32][kWarpFMax];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int id = blockIdx.x * (kCT / 32) + w;
     if (id >= n) return;
-    const NodeDev nd = a.nodes[list[id]];
+    const NodeDev nd = list[id];
     double2* v = sv[w];
     double2* y = sy[w];
     gather_front<32>(a, nd, v, lane, [] { __syncwarp(); });
@@ -424,9 +426,9 @@ __global__ void __launch_bounds__(kCT) k_nd_fwd_warp(const int* __restrict__ lis
 }
 
 // forward, CTA tier: one CTA per front, both phases
-__global__ void __launch_bounds__(kCT) k_nd_fwd_mid(const int* __restrict__ list, NDArgs a) {
+__global__ void __launch_bounds__(kCT) k_nd_fwd_mid(const NodeDev* __restrict__ list, NDArgs a) {
     extern __shared__ double2 smem[];
-    const NodeDev nd = a.nodes[list[blockIdx.x]];
+    const NodeDev nd = list[blockIdx.x];
     double2* v = smem;
     double2* y = smem + nd.s + nd.u;
     gather_front<kCT>(a, nd, v, threadIdx.x, [] { __syncthreads(); });
@@ -446,7 +448,7 @@ __global__ void __launch_bounds__(kCT) k_nd_fwd_mid(const int* __restrict__ list
 __global__ void __launch_bounds__(kCT) k_nd_fwd1(const Task* tasks, NDArgs a) {
     extern __shared__ double2 smem[];
     const Task tk = tasks[blockIdx.x];
-    const NodeDev nd = a.nodes[tk.node];
+    const NodeDev nd = tk.nd;
     gather_front<kCT>(a, nd, smem, threadIdx.x, [] { __syncthreads(); });
     if (tk.r0 == 0)
         for (int i = nd.s + threadIdx.x; i < nd.s + nd.u; i += kCT) a.front[nd.off_front + i] = smem[i];
@@ -459,7 +461,7 @@ __global__ void __launch_bounds__(kCT) k_nd_fwd1(const Task* tasks, NDArgs a) {
 __global__ void __launch_bounds__(kCT) k_nd_fwd2(const Task* tasks, NDArgs a) {
     extern __shared__ double2 smem[];
     const Task tk = tasks[blockIdx.x];
-    const NodeDev nd = a.nodes[tk.node];
+    const NodeDev nd = tk.nd;
     for (int i = threadIdx.x; i < nd.s; i += kCT) smem[i] = a.Y[a.idx[nd.off_var + i]];
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -488,13 +490,13 @@ __device__ __forceinline__ void bwd_rows(const NDArgs& a, const NodeDev& nd, con
 __device__ void sync_warp_fn() { __syncwarp(); }
 __device__ void sync_cta_fn() { __syncthreads(); }
 
-__global__ void __launch_bounds__(kCT) k_nd_bwd_warp(const int* __restrict__ list, int n, NDArgs a) {
+__global__ void __launch_bounds__(kCT) k_nd_bwd_warp(const NodeDev* __restrict__ list, int n, NDArgs a) {
     __shared__ double2 sv[kCT / 32][kWarpFMax];
     __shared__ double2 sz[kCT / 32][kWarpFMax];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int id = blockIdx.x * (kCT / 32) + w;
     if (id >= n) return;
-    const NodeDev nd = a.nodes[list[id]];
+    const NodeDev nd = list[id];
     double2* v = sv[w];
     for (int i = lane; i < nd.s; i += 32) v[i] = a.Y[a.idx[nd.off_var + i]];
     for (int i = lane; i < nd.u; i += 32) v[nd.s + i] = a.X[a.idx[nd.off_ring + i]];
@@ -506,7 +508,7 @@ __global__ void __launch_bounds__(kCT) k_nd_bwd_warp(const int* __restrict__ lis
 __global__ void __launch_bounds__(kCT) k_nd_bwd(const Task* tasks, NDArgs a) {
     extern __shared__ double2 smem[];
     const Task tk = tasks[blockIdx.x];
-    const NodeDev nd = a.nodes[tk.node];
+    const NodeDev nd = tk.nd;
     double2* y1 = smem;
     double2* x2 = smem + nd.s;
     double2* sz = smem + nd.s + nd.u;
@@ -601,7 +603,7 @@ class NDSolver : public CoarseSolver {
 
   private:
     struct Level {
-        const int *warp = nullptr, *mid = nullptr;
+        const NodeDev *warp = nullptr, *mid = nullptr;
         const Task *f1 = nullptr, *f2 = nullptr, *b = nullptr;
         int nwarp = 0, nmid = 0, nf1 = 0, nf2 = 0, nb = 0;
         size_t smem_mid = 0, smem_big = 0, smem_b = 0;
@@ -626,10 +628,9 @@ class NDSolver : public CoarseSolver {
     void upload(NDTree& t, cudaStream_t st) {
         const int nn = int(t.nodes.size());
         std::vector<NodeDev> nd(nn);
-        std::vector<int> idx, children, cmaps;
-        std::vector<long long> cmap_off(nn, 0);
+        std::vector<int> idx;
         long long fac_total = 0;
-        int front_total = 0, contrib_total = 0;
+        int front_total = 0, contrib_total = 0, gsrc_total = 0;
         for (int i = 0; i < nn; ++i) {
             const NDNode& n = t.nodes[i];
             NodeDev& d = nd[i];
@@ -651,11 +652,22 @@ class NDSolver : public CoarseSolver {
             front_total += d.s + d.u;
             d.off_contrib = contrib_total;
             contrib_total += d.u;
-            d.child0 = int(children.size());
-            d.nchild = int(n.children.size());
-            children.insert(children.end(), n.children.begin(), n.children.end());
-            cmap_off[i] = (long long)cmaps.size();
-            cmaps.insert(cmaps.end(), n.cmap.begin(), n.cmap.end());
+            d.off_gsrc = gsrc_total;
+            gsrc_total += d.s + d.u;
+        }
+        // gather plan: front position <- contribution entries of the children (child order)
+        std::vector<int2> gsrc(std::max(gsrc_total, 1), make_int2(-1, -1));
+        for (int i = 0; i < nn; ++i) {
+            for (int c : t.nodes[i].children) {
+                const NDNode& ch = t.nodes[c];
+                for (int k = 0; k < int(ch.cmap.size()); ++k) {
+                    int2& e = gsrc[nd[i].off_gsrc + ch.cmap[k]];
+                    const int src = nd[c].off_contrib + k;
+                    if (e.x < 0) e.x = src;
+                    else if (e.y < 0) e.y = src;
+                    else throw RuntimeError("coarse solve: more than two contributions to a front position");
+                }
+            }
         }
         void* facp = nullptr;
         HTG_CUDA(cudaMalloc(&facp, std::max<long long>(1, fac_total) * sizeof(double2)));
@@ -676,18 +688,15 @@ class NDSolver : public CoarseSolver {
             put(n.Z, d.off_Z);
         }
         args_.fac = static_cast<const double2*>(facp);
-        args_.nodes = up(nd, st);
         args_.idx = up(idx, st);
-        args_.children = up(children, st);
-        args_.cmaps = up(cmaps, st);
-        args_.cmap_off = up(cmap_off, st);
+        args_.gsrc = up(gsrc, st);
         args_.contrib = up(std::vector<double2>(std::max(contrib_total, 1)), st);
         args_.front = up(std::vector<double2>(std::max(front_total, 1)), st);
         args_.Y = up(std::vector<double2>(nv_), st);
         // per depth: warp tier, CTA tier, large tier (8 rows per CTA task)
         const int D = t.max_depth + 1;
         levels_.resize(D);
-        std::vector<std::vector<int>> wp(D), md(D);
+        std::vector<std::vector<NodeDev>> wp(D), md(D);
         std::vector<std::vector<Task>> f1(D), f2(D), bw(D);
         size_t max_smem = 0;
         const int warpF = std::min(kWarpFMax, env_int("HTG_ND_WARPF", 64));
@@ -698,19 +707,19 @@ class NDSolver : public CoarseSolver {
             Level& lv = levels_[dep];
             const int F = d.s + d.u;
             if (F <= warpF) {
-                wp[dep].push_back(i);
+                wp[dep].push_back(d);
             } else if ((long long)d.s * F <= midData) {
-                md[dep].push_back(i);
-                bw[dep].push_back({i, 0, d.s, 0});
+                md[dep].push_back(d);
+                bw[dep].push_back({d, 0, d.s});
                 lv.smem_mid = std::max(lv.smem_mid, size_t(F + d.s) * sizeof(double2));
                 lv.smem_b = std::max(lv.smem_b, size_t(F + d.s) * sizeof(double2));
             } else {
                 const int rpt = env_int("HTG_ND_RPT", 8);
                 for (int r = 0; r < d.s; r += rpt) {
-                    f1[dep].push_back({i, r, std::min(rpt, d.s - r), 0});
-                    bw[dep].push_back({i, r, std::min(rpt, d.s - r), 0});
+                    f1[dep].push_back({d, r, std::min(rpt, d.s - r)});
+                    bw[dep].push_back({d, r, std::min(rpt, d.s - r)});
                 }
-                for (int r = 0; r < d.u; r += rpt) f2[dep].push_back({i, r, std::min(rpt, d.u - r), 0});
+                for (int r = 0; r < d.u; r += rpt) f2[dep].push_back({d, r, std::min(rpt, d.u - r)});
                 lv.smem_big = std::max(lv.smem_big, size_t(F) * sizeof(double2));
                 lv.smem_b = std::max(lv.smem_b, size_t(F + rpt) * sizeof(double2));
             }
