@@ -58,11 +58,13 @@ template <class Epi>
 __device__ __forceinline__ void stage(const double2 (*A)[kLDF], const double2 (*B)[kLDF], int MT, int NT, int KS,
                                       int q, int lane, Epi&& epi) {
     const int nt_all = MT * NT;
-    double cr[4][2], ci[4][2];
+    // Gauss / 3M complex product: t1 = ar br, t2 = ai bi, t3 = (ar + ai)(br + bi);
+    // re = t1 - t2, im = t3 - t1 - t2 -- three DMMAs per k-step and tile instead of four
+    double t1[4][2], t2[4][2], t3[4][2];
     int tm[4], tn[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-        cr[j][0] = cr[j][1] = ci[j][0] = ci[j][1] = 0.0;
+        t1[j][0] = t1[j][1] = t2[j][0] = t2[j][1] = t3[j][0] = t3[j][1] = 0.0;
         const int t = q + 4 * j;
         tm[j] = t < nt_all ? t / NT : -1;
         tn[j] = t < nt_all ? t % NT : 0;
@@ -78,25 +80,23 @@ __device__ __forceinline__ void stage(const double2 (*A)[kLDF], const double2 (*
             a[j] = A[m * 8 + r][k];
             b[j] = B[n * 8 + r][k];
         }
-        // two passes: dependent DMMAs into one accumulator are 2*ntile apart
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-            if (j < ntile) {
-                dmma(cr[j][0], cr[j][1], a[j].x, b[j].x);
-                dmma(ci[j][0], ci[j][1], a[j].x, b[j].y);
-            }
+            if (j < ntile) dmma(t1[j][0], t1[j][1], a[j].x, b[j].x);
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-            if (j < ntile) {
-                dmma(cr[j][0], cr[j][1], -a[j].y, b[j].y);
-                dmma(ci[j][0], ci[j][1], a[j].y, b[j].x);
-            }
+            if (j < ntile) dmma(t2[j][0], t2[j][1], a[j].y, b[j].y);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (j < ntile) dmma(t3[j][0], t3[j][1], a[j].x + a[j].y, b[j].x + b[j].y);
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         if (tm[j] < 0) break;
 #pragma unroll
-        for (int i = 0; i < 2; ++i) epi(tm[j] * 8 + r, tn[j] * 8 + 2 * kq + i, make_double2(cr[j][i], ci[j][i]));
+        for (int i = 0; i < 2; ++i)
+            epi(tm[j] * 8 + r, tn[j] * 8 + 2 * kq + i,
+                make_double2(t1[j][i] - t2[j][i], t3[j][i] - t1[j][i] - t2[j][i]));
     }
 }
 
