@@ -101,6 +101,16 @@ __device__ __forceinline__ int lidx(int xc, int a) {
     return a == 0 ? xc * P : (a == 1 ? (xc + 1) * P : xc * P + a - 1);
 }
 
+// Structural nonzeros of the 1-D hierarchical factors (integrated Legendre
+// bubbles): S couples the two vertices and each bubble with itself; M couples
+// vertices, vertices with the degree-2/3 bubbles, and bubbles with |d - e| in
+// {0, 2}. Entries outside these patterns are zero up to quadrature round-off.
+__host__ __device__ constexpr bool nzS(int i, int j) { return (i < 2 && j < 2) || (i >= 2 && i == j); }
+__host__ __device__ constexpr bool nzM(int i, int j) {
+    return (i < 2 && j < 2) || (i < 2 && (j == 2 || j == 3)) || (j < 2 && (i == 2 || i == 3)) ||
+           (i >= 2 && j >= 2 && (i == j || i - j == 2 || j - i == 2));
+}
+
 // ---------------------------------------------------------------- K1
 // Data movement: per lattice row the strip's unit cells are one contiguous
 // byte range of u / f / r (the reference layout keeps each unit cell's p^2
@@ -243,8 +253,23 @@ __global__ void __launch_bounds__(kK1Threads) k1_residual(K1Args a) {
         issue_f(yout0);
         if (yout0 + 1 <= ylast) issue_f(yout0 + 1);
     }
-    auto uval = [&](int yy, int gy) -> double2 {
-        return valid ? sm.U[(yy - ystart) % 3][dofp<P>(nx, ny, gx, gy) - seg_lo(yy)] : zero;
+    // offsets of this thread's dofs inside a staged row segment (row-invariant):
+    // rows below the top: unit cell (x - xa) p^2 + layout position; top row: (x - xa) p + jx
+    int off_mid[P];
+#pragma unroll
+    for (int jy = 0; jy < P; ++jy) {
+        int pos;
+        if (x == nx) pos = jy;
+        else if (j == 0 && jy == 0) pos = 0;
+        else if (jy == 0) pos = j;
+        else if (j == 0) pos = P + jy - 1;
+        else pos = 2 * P - 1 + (j - 1) * (P - 1) + (jy - 1);
+        off_mid[jy] = (x - xa) * P * P + pos;
+    }
+    const int off_top = (x - xa) * P + j;
+    const int rshift = (x0 - xa);  // R segments start at x0
+    auto uval = [&](int yy, int jy) -> double2 {
+        return valid ? sm.U[(yy - ystart) % 3][yy < ny ? off_mid[jy] : off_top] : zero;
     };
     auto wait_u = [&](int yy) { mbar_wait(&sm.barU[(yy - ystart) % 3], unsigned(((yy - ystart) / 3) & 1)); };
     auto wait_f = [&](int yy) { mbar_wait(&sm.barF[(yy - yout0) & 1], unsigned(((yy - yout0) >> 1) & 1)); };
@@ -261,17 +286,18 @@ __global__ void __launch_bounds__(kK1Threads) k1_residual(K1Args a) {
     auto emit_row = [&](int yy, int nj, const double2* Au, const double2* ur, double2* rr) {
         wait_f(yy);
         const double2* Fs = sm.F[(yy - yout0) & 1];
+        const bool topr = yy == ny;
         for (int jy = 0; jy < nj; ++jy) {
             const int gy = yy * P + jy;
-            const long long d = dofp<P>(nx, ny, gx, gy);
             double2 A = Au[jy];
             if (g.has_dirichlet && fine_dir<P>(g, gx, gy)) A = ur[jy];
-            const double2 fv = Fs[d - seg_lo(yy)];
+            const double2 fv = Fs[topr ? off_top : off_mid[jy]];
             rr[jy] = csub(fv, A);
         }
         if (MODE == kK1Write && owned) {
             double2* Rs = sm.R[(yy - yout0) & 1];
-            for (int jy = 0; jy < nj; ++jy) Rs[dofp<P>(nx, ny, gx, yy * P + jy) - rseg_lo(yy)] = rr[jy];
+            for (int jy = 0; jy < nj; ++jy)
+                Rs[topr ? off_top - rshift * P : off_mid[jy] - rshift * P * P] = rr[jy];
         }
     };
     auto store_row = [&](int yy) {
@@ -334,10 +360,10 @@ __global__ void __launch_bounds__(kK1Threads) k1_residual(K1Args a) {
         wait_u(y);
         wait_u(y + 1);
         double2 zr[B], z[B];
-        zr[0] = uval(y, y * P);
-        zr[1] = uval(y + 1, (y + 1) * P);
+        zr[0] = uval(y, 0);
+        zr[1] = uval(y + 1, 0);
 #pragma unroll
-        for (int jy = 1; jy < P; ++jy) zr[jy + 1] = uval(y, y * P + jy);
+        for (int jy = 1; jy < P; ++jy) zr[jy + 1] = uval(y, jy);
 #pragma unroll
         for (int b = 0; b < B; ++b) {
             z[b] = zr[b];
@@ -353,8 +379,8 @@ __global__ void __launch_bounds__(kK1Threads) k1_residual(K1Args a) {
             double2 t = zero, v = zero;
 #pragma unroll
             for (int b = 0; b < B; ++b) {
-                t = rfma(sm.M[bp][b], z[b], t);
-                v = rfma(sm.S[bp][b], z[b], v);
+                if (nzM(bp, b)) t = rfma(sm.M[bp][b], z[b], t);
+                if (nzS(bp, b)) v = rfma(sm.S[bp][b], z[b], v);
             }
             T[bp] = t;
             if (valid) {
@@ -459,7 +485,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_residual(K1Args a) {
         if (MODE == kK1Write && ny - 2 >= yout0 && tid == 0) bulk_wait_read<1>();
         if (MODE == kK1Write) __syncthreads();
         if (emit) {
-            double2 Au[1] = {carryO}, ur[1] = {uval(ny, ny * P)};
+            double2 Au[1] = {carryO}, ur[1] = {uval(ny, 0)};
             emit_row(ny, 1, Au, ur, rr);
             if (MODE == kK1Norm && owned) acc += rr[0].x * rr[0].x + rr[0].y * rr[0].y;
         }
