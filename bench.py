@@ -126,6 +126,22 @@ def dist_env():
     return ws, rank, local
 
 
+def max_over_ranks(t_ms: float, dist, device) -> float:
+    """Timed-region length of the slowest rank (replicas: no data-path collective)."""
+    if dist is None:
+        return t_ms
+    import torch
+    t = torch.tensor([t_ms], device=device, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.barrier()
+    return float(t.item())
+
+
+def whole_job_value(world: int, ndof: int, steps: int, t_ms: float) -> float:
+    """DoF/s over all replicas: every rank sweeps its own ndof-dof problem `steps` times."""
+    return world * ndof * steps / (t_ms * 1e-3)
+
+
 def seeded_rhs(ndof: int, seed: int) -> np.ndarray:
     g = np.random.default_rng(seed)
     re = g.standard_normal(ndof)
@@ -244,12 +260,8 @@ def run_ours(args):
     T_ms = timed(lambda: ops.csdd_smoother(u, f), args.steps)
     launches = hb.launch_count()
     torch.cuda.synchronize()
-    if dist:
-        t = torch.tensor([T_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        T_ms = float(t.item())
-        dist.barrier()
-    value = ws * n * args.steps / (T_ms * 1e-3)
+    T_ms = max_over_ranks(T_ms, dist, dev)
+    value = whole_job_value(ws, n, args.steps, T_ms)
 
     # seconds per two-grid iteration (coarse solve included), same flush protocol
     k2 = max(3, min(args.steps, 20))

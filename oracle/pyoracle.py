@@ -146,7 +146,7 @@ class Session:
          self.nnz_A, self.nnz_Ac, self.nnz_IP) = (int(v) for v in info)
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and lib is not None:
             lib().orc_session_free(self._h)
             self._h = None
 

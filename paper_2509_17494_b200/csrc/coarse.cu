@@ -1,5 +1,5 @@
-// coarse.cu -- QSFEM coarse matrix, nested-dissection multifrontal LU (host)
-// and the level-batched GPU triangular solves.
+// coarse.cu -- level-batched GPU solves with the nested-dissection multifrontal
+// factors of the QSFEM coarse matrix (factored on the host in coarse_nd.cpp).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -14,302 +14,17 @@
 
 namespace htg {
 
-// ------------------------------------------------------------------ QSFEM
-QsfemWeights qsfem_weights(double eta) {
-    if (!(eta > 0.0) || !(eta < M_PI))
-        throw InvalidArgument("qsfem: eta = k*h_c must lie in (0, pi) (at least two coarse points per wavelength)");
-    // zero set of the symbol interpolated in the directions pi/16 and 3pi/16
-    const double a1 = std::cos(eta * std::cos(M_PI / 16.0)), b1 = std::cos(eta * std::sin(M_PI / 16.0));
-    const double a2 = std::cos(eta * std::cos(3.0 * M_PI / 16.0)), b2 = std::cos(eta * std::sin(3.0 * M_PI / 16.0));
-    const double den = a2 * b2 * (a1 + b1) - a1 * b1 * (a2 + b2);
-    if (std::fabs(den) < 1e-14) throw RuntimeError("qsfem: degenerate stencil (denominator ~ 0)");
-    QsfemWeights w;
-    w.eta = eta;
-    w.P0 = 4.0;
-    w.P1 = 2.0 * (a1 * b1 - a2 * b2) / den;
-    w.P2 = (a2 + b2 - a1 - b1) / den;
-    const double sigma0 = w.P0 + 4.0 * w.P1 + 4.0 * w.P2;  // symbol at the origin
-    if (sigma0 == 0.0) throw RuntimeError("qsfem: sigma_P(0) = 0, scaling undefined");
-    w.N = -eta * eta / sigma0;
-    w.q0 = w.N * w.P0 / 4.0;
-    w.q1 = w.N * w.P1 / 2.0;
-    w.q2 = w.N * w.P2;
-    return w;
-}
-
-std::vector<cplx> coarse_stencil(const HostProblem& hp) {
-    const int m = hp.p / 2, CX = hp.nx * m, CY = hp.ny * m;
-    const double hc = 2.0 * hp.h / hp.p;
-    const size_t nv = size_t(CX + 1) * (CY + 1);
-    std::vector<cplx> A9(nv * 9, cplx(0.0));
-    std::vector<QsfemWeights> qw(hp.cls_k.size());
-    for (size_t c = 0; c < qw.size(); ++c) qw[c] = qsfem_weights(hc * hp.cls_k[c]);
-    auto cellcls = [&](int cx, int cy) { return hp.cls[size_t(cy / m) * hp.nx + cx / m]; };
-    auto cdir = [&](int X, int Y) {
-        if (!hp.has_dirichlet) return false;
-        bool d = false;
-        if (X == 0 || X == CX) {
-            const auto& tg = X == 0 ? hp.tl : hp.tr;
-            d |= (Y > 0 && tg[(Y - 1) / m] == kDirichlet) || (Y < CY && tg[Y / m] == kDirichlet);
-        }
-        if (Y == 0 || Y == CY) {
-            const auto& tg = Y == 0 ? hp.tb : hp.tt;
-            d |= (X > 0 && tg[(X - 1) / m] == kDirichlet) || (X < CX && tg[X / m] == kDirichlet);
-        }
-        return d;
-    };
-    for (int Y = 0; Y <= CY; ++Y)
-        for (int X = 0; X <= CX; ++X) {
-            cplx* row = &A9[(size_t(Y) * (CX + 1) + X) * 9];
-            if (cdir(X, Y)) {
-                row[4] = 1.0;
-                continue;
-            }
-            for (int dy = -1; dy <= 1; ++dy)
-                for (int dx = -1; dx <= 1; ++dx) {
-                    const int WX = X + dx, WY = Y + dy;
-                    if (WX < 0 || WX > CX || WY < 0 || WY > CY || cdir(WX, WY)) continue;
-                    cplx s = 0.0;
-                    for (int cy = std::max(std::max(Y, WY) - 1, 0); cy <= std::min(std::min(Y, WY), CY - 1); ++cy)
-                        for (int cx = std::max(std::max(X, WX) - 1, 0); cx <= std::min(std::min(X, WX), CX - 1); ++cx) {
-                            const int c = cellcls(cx, cy);
-                            const QsfemWeights& q = qw[c];
-                            const int md = std::abs(dx) + std::abs(dy);
-                            const double qv = md == 0 ? q.q0 : (md == 1 ? q.q1 : q.q2);
-                            const double mass = double((dx == 0 ? 2 : 1) * (dy == 0 ? 2 : 1)) / 36.0;
-                            s += cplx(qv, -hp.cls_eps[c] * hc * hc * mass);
-                        }
-                    // absorbing coarse boundary edges containing both vertices
-                    auto robin = [&](const std::vector<double>& kh, int e) {
-                        const double khc = kh[e / m] / m;
-                        s += cplx(0.0, -khc * ((dx == 0 && dy == 0) ? 1.0 / 3.0 : 1.0 / 6.0));
-                    };
-                    if (dy == 0 && (Y == 0 || Y == CY)) {
-                        const auto& kh = Y == 0 ? hp.khb : hp.kht;
-                        if (dx <= 0 && X > 0) robin(kh, X - 1);
-                        if (dx >= 0 && X < CX) robin(kh, X);
-                    }
-                    if (dx == 0 && (X == 0 || X == CX)) {
-                        const auto& kh = X == 0 ? hp.khl : hp.khr;
-                        if (dy <= 0 && Y > 0) robin(kh, Y - 1);
-                        if (dy >= 0 && Y < CY) robin(kh, Y);
-                    }
-                    row[(dy + 1) * 3 + (dx + 1)] = s;
-                }
-        }
-    return A9;
-}
-
-// ------------------------------------------------------------------ nested dissection
 namespace {
-
-struct NDNode {
-    int x0, x1, y0, y1;  // box of the subtree (inclusive vertex coordinates)
-    int depth = 0;
-    bool leaf = false;
-    std::vector<int> vars, ring, children;
-    // factor blocks (host, freed after upload)
-    std::vector<cplx> Finv, L21, Uinv, Z, S;
-    std::vector<int> cmap;  // this node's ring -> parent's front positions
-};
-
-struct NDTree {
-    int CX, CY;
-    std::vector<NDNode> nodes;  // postorder: children before parents, root last
-    int max_depth = 0;
-};
-
-int build_nd(NDTree& t, int x0, int x1, int y0, int y1, int depth, int leaf_max) {
-    NDNode n;
-    n.x0 = x0;
-    n.x1 = x1;
-    n.y0 = y0;
-    n.y1 = y1;
-    n.depth = depth;
-    const int w = x1 - x0 + 1, h = y1 - y0 + 1;
-    std::vector<int> kids;
-    if (w * h <= leaf_max || std::max(w, h) < 3) {
-        n.leaf = true;
-        for (int y = y0; y <= y1; ++y)
-            for (int x = x0; x <= x1; ++x) n.vars.push_back(y * (t.CX + 1) + x);
-    } else if (w >= h) {
-        const int xm = (x0 + x1) / 2;
-        kids.push_back(build_nd(t, x0, xm - 1, y0, y1, depth + 1, leaf_max));
-        kids.push_back(build_nd(t, xm + 1, x1, y0, y1, depth + 1, leaf_max));
-        for (int y = y0; y <= y1; ++y) n.vars.push_back(y * (t.CX + 1) + xm);
-    } else {
-        const int ym = (y0 + y1) / 2;
-        kids.push_back(build_nd(t, x0, x1, y0, ym - 1, depth + 1, leaf_max));
-        kids.push_back(build_nd(t, x0, x1, ym + 1, y1, depth + 1, leaf_max));
-        for (int x = x0; x <= x1; ++x) n.vars.push_back(ym * (t.CX + 1) + x);
-    }
-    for (int y = y0 - 1; y <= y1 + 1; ++y)
-        for (int x = x0 - 1; x <= x1 + 1; ++x) {
-            if (x < 0 || y < 0 || x > t.CX || y > t.CY) continue;
-            if (x >= x0 && x <= x1 && y >= y0 && y <= y1) continue;
-            n.ring.push_back(y * (t.CX + 1) + x);
-        }
-    n.children = kids;
-    t.max_depth = std::max(t.max_depth, depth);
-    t.nodes.push_back(std::move(n));
-    return int(t.nodes.size()) - 1;
-}
-
-// C[rows i0..i1) -= A (m x k) * B (k x n), row-major, parallel over rows
-void gemm_sub(int m, int n, int k, const cplx* A, const cplx* B, cplx* C, int nthreads) {
-    auto body = [&](int i0, int i1) {
-        for (int i = i0; i < i1; ++i) {
-            cplx* ci = C + size_t(i) * n;
-            const cplx* ai = A + size_t(i) * k;
-            for (int kk = 0; kk < k; ++kk) {
-                const cplx a = ai[kk];
-                if (a == cplx(0.0)) continue;
-                const cplx* bk = B + size_t(kk) * n;
-                for (int j = 0; j < n; ++j) ci[j] -= a * bk[j];
-            }
-        }
-    };
-    if (nthreads <= 1 || size_t(m) * n * k < 2000000) {
-        body(0, m);
-        return;
-    }
-    std::vector<std::thread> th;
-    for (int t = 0; t < nthreads; ++t) th.emplace_back(body, m * t / nthreads, m * (t + 1) / nthreads);
-    for (auto& x : th) x.join();
-}
-
-void parallel_rows(int m, int nthreads, const std::function<void(int, int)>& body, size_t work) {
-    if (nthreads <= 1 || work < 2000000) {
-        body(0, m);
-        return;
-    }
-    std::vector<std::thread> th;
-    for (int t = 0; t < nthreads; ++t) th.emplace_back(body, m * t / nthreads, m * (t + 1) / nthreads);
-    for (auto& x : th) x.join();
-}
-
-// Factor one front (children already factored). pos: scratch global->front map.
-void factor_node(NDTree& t, int id, const std::vector<cplx>& A9, std::vector<int>& pos, int nthreads) {
-    NDNode& n = t.nodes[id];
-    const int s = int(n.vars.size()), u = int(n.ring.size()), F = s + u;
-    for (int i = 0; i < s; ++i) pos[n.vars[i]] = i;
-    for (int i = 0; i < u; ++i) pos[n.ring[i]] = s + i;
-    std::vector<cplx> Fm(size_t(F) * F, cplx(0.0));
-    const int W = t.CX + 1;
-    for (int i = 0; i < s; ++i) {
-        const int v = n.vars[i], X = v % W, Y = v / W;
-        for (int dy = -1; dy <= 1; ++dy)
-            for (int dx = -1; dx <= 1; ++dx) {
-                const int WX = X + dx, WY = Y + dy;
-                if (WX < 0 || WX > t.CX || WY < 0 || WY > t.CY) continue;
-                const int w = WY * W + WX, pw = pos[w];
-                if (pw < 0) continue;
-                Fm[size_t(i) * F + pw] += A9[size_t(v) * 9 + (dy + 1) * 3 + (dx + 1)];
-                if (pw >= s) Fm[size_t(pw) * F + i] += A9[size_t(w) * 9 + (1 - dy) * 3 + (1 - dx)];
-            }
-    }
-    for (int c : n.children) {
-        NDNode& ch = t.nodes[c];
-        const int uc = int(ch.ring.size());
-        ch.cmap.resize(uc);
-        for (int a = 0; a < uc; ++a) ch.cmap[a] = pos[ch.ring[a]];
-        for (int a = 0; a < uc; ++a) {
-            const int pa = ch.cmap[a];
-            for (int b = 0; b < uc; ++b) Fm[size_t(pa) * F + ch.cmap[b]] += ch.S[size_t(a) * uc + b];
-        }
-        std::vector<cplx>().swap(ch.S);
-    }
-    for (int i = 0; i < s; ++i) pos[n.vars[i]] = -1;
-    for (int i = 0; i < u; ++i) pos[n.ring[i]] = -1;
-
-    // LU of F11 with partial pivoting restricted to the front's pivot rows;
-    // row swaps applied to the whole front row (F11 and F12 parts)
-    std::vector<int> perm(s);
-    for (int i = 0; i < s; ++i) perm[i] = i;
-    for (int k = 0; k < s; ++k) {
-        int p = k;
-        double best = std::abs(Fm[size_t(k) * F + k]);
-        for (int i = k + 1; i < s; ++i) {
-            const double a = std::abs(Fm[size_t(i) * F + k]);
-            if (a > best) {
-                best = a;
-                p = i;
-            }
-        }
-        if (best == 0.0) throw RuntimeError("coarse LU: singular front (zero pivot)");
-        if (p != k) {
-            std::swap_ranges(Fm.begin() + size_t(k) * F, Fm.begin() + size_t(k) * F + F, Fm.begin() + size_t(p) * F);
-            std::swap(perm[k], perm[p]);
-        }
-        const cplx inv = 1.0 / Fm[size_t(k) * F + k];
-        const cplx* rk = &Fm[size_t(k) * F];
-        // eliminate below in the pivot block and in the F21 block (rows s..F-1 are
-        // the L21 computation: L21 = F21 U^-1 falls out of the same elimination)
-        auto elim = [&](int i0, int i1) {
-            for (int i = i0; i < i1; ++i) {
-                const int row = i < s - k - 1 ? k + 1 + i : s + (i - (s - k - 1));
-                cplx* ri = &Fm[size_t(row) * F];
-                if (ri[k] == cplx(0.0)) continue;
-                const cplx l = ri[k] * inv;
-                ri[k] = l;
-                for (int j = k + 1; j < F; ++j) ri[j] -= l * rk[j];
-            }
-        };
-        const int nrows = (s - k - 1) + u;
-        parallel_rows(nrows, nthreads, elim, size_t(nrows) * (F - k));
-    }
-    // Now: rows 0..s-1: L (unit, strict lower of cols < s), U (upper of cols < s), U12 (cols >= s)
-    //      rows s..F-1: L21 (cols < s), S (cols >= s) -- the Schur complement
-    n.S.assign(size_t(u) * u, cplx(0.0));
-    for (int i = 0; i < u; ++i)
-        for (int j = 0; j < u; ++j) n.S[size_t(i) * u + j] = Fm[size_t(s + i) * F + s + j];
-    n.L21.assign(size_t(u) * s, cplx(0.0));
-    for (int i = 0; i < u; ++i)
-        for (int j = 0; j < s; ++j) n.L21[size_t(i) * s + j] = Fm[size_t(s + i) * F + j];
-    // Finv = L^-1 P : column perm[k] of Finv is column k of L^-1
-    std::vector<cplx> Linv(size_t(s) * s, cplx(0.0));
-    for (int c = 0; c < s; ++c) {
-        Linv[size_t(c) * s + c] = 1.0;
-        for (int i = c + 1; i < s; ++i) {
-            cplx acc = 0.0;
-            for (int k2 = c; k2 < i; ++k2) acc += Fm[size_t(i) * F + k2] * Linv[size_t(k2) * s + c];
-            Linv[size_t(i) * s + c] = -acc;
-        }
-    }
-    n.Finv.assign(size_t(s) * s, cplx(0.0));
-    for (int i = 0; i < s; ++i)
-        for (int k2 = 0; k2 < s; ++k2) n.Finv[size_t(i) * s + perm[k2]] = Linv[size_t(i) * s + k2];
-    // Uinv (upper triangular inverse)
-    n.Uinv.assign(size_t(s) * s, cplx(0.0));
-    for (int c = s - 1; c >= 0; --c) {
-        n.Uinv[size_t(c) * s + c] = 1.0 / Fm[size_t(c) * F + c];
-        for (int i = c - 1; i >= 0; --i) {
-            cplx acc = 0.0;
-            for (int k2 = i + 1; k2 <= c; ++k2) acc += Fm[size_t(i) * F + k2] * n.Uinv[size_t(k2) * s + c];
-            n.Uinv[size_t(i) * s + c] = -acc / Fm[size_t(i) * F + i];
-        }
-    }
-    // Z = Uinv U12
-    n.Z.assign(size_t(s) * u, cplx(0.0));
-    if (u > 0) {
-        std::vector<cplx> U12(size_t(s) * u);
-        for (int i = 0; i < s; ++i)
-            for (int j = 0; j < u; ++j) U12[size_t(i) * u + j] = Fm[size_t(i) * F + s + j];
-        std::vector<cplx> negZ(size_t(s) * u, cplx(0.0));
-        gemm_sub(s, u, s, n.Uinv.data(), U12.data(), negZ.data(), nthreads);
-        for (size_t i = 0; i < negZ.size(); ++i) n.Z[i] = -negZ[i];
-    }
-}
 
 // ------------------------------------------------------------------ GPU solve
 struct NodeDev {
-    int s, u;
+    int s, u;                              // eliminated here / contribution rows (delayed + ring)
     long long off_F, off_L, off_U, off_Z;  // into the factor buffer (row-major blocks)
-    int off_var, off_ring;                 // into idx
+    int off_var, off_ring;                 // into idx: eliminated / remaining column labels
     int off_front;                         // front scratch (s+u)
     int off_contrib;                       // contribution vector (u)
-    int off_gsrc;                          // per front position: <= 2 child contribution indices
-    int pad;
+    int off_gsrc;                          // per front position: <= 4 child contribution indices
+    int off_rc;                            // into idx: per front row, rhs entry injected here or -1
 };
 // a launch's work item carries its front descriptor (no dependent load at start)
 struct Task {
@@ -331,7 +46,7 @@ __device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {
 
 struct NDArgs {
     const int* idx;
-    const int2* gsrc;
+    const int4* gsrc;
     const double2* fac;
     const double2* rc;
     double2* contrib;
@@ -386,15 +101,14 @@ template <int STRIDE, class Sync>
 __device__ void gather_front(const NDArgs& a, const NodeDev& nd, double2* sv, int t, Sync&& sync) {
     const int F = nd.s + nd.u;
     for (int i = t; i < F; i += STRIDE) {
-        double2 v = i < nd.s ? a.rc[a.idx[nd.off_var + i]] : make_double2(0.0, 0.0);
-        const int2 src = a.gsrc[nd.off_gsrc + i];
-        if (src.x >= 0) {
-            const double2 c = a.contrib[src.x];
-            v.x += c.x;
-            v.y += c.y;
-        }
-        if (src.y >= 0) {
-            const double2 c = a.contrib[src.y];
+        const int ri = a.idx[nd.off_rc + i];
+        double2 v = ri >= 0 ? a.rc[ri] : make_double2(0.0, 0.0);
+        const int4 src = a.gsrc[nd.off_gsrc + i];
+        const int sx[4] = {src.x, src.y, src.z, src.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (sx[q] < 0) break;
+            const double2 c = a.contrib[sx[q]];
             v.x += c.x;
             v.y += c.y;
         }
@@ -521,41 +235,11 @@ __global__ void __launch_bounds__(kCT) k_nd_bwd(const Task* tasks, NDArgs a) {
 class NDSolver : public CoarseSolver {
   public:
     NDSolver(const HostProblem& hp, cudaStream_t st) {
-        const int m = hp.p / 2;
         NDTree t;
-        t.CX = hp.nx * m;
-        t.CY = hp.ny * m;
-        const int nv = (t.CX + 1) * (t.CY + 1);
-        nv_ = nv;
-        build_nd(t, 0, t.CX, 0, t.CY, 0, env_int("HTG_ND_LEAF", 16));
-        const std::vector<cplx> A9 = coarse_stencil(hp);
-        // factor bottom-up by depth; nodes of one depth in parallel
-        const int nthr = std::max(1, int(std::thread::hardware_concurrency()));
-        std::vector<std::vector<int>> bydepth(t.max_depth + 1);
-        for (int i = 0; i < int(t.nodes.size()); ++i) bydepth[t.nodes[i].depth].push_back(i);
-        for (int d = t.max_depth; d >= 0; --d) {
-            const auto& ids = bydepth[d];
-            if (int(ids.size()) >= nthr) {
-                std::vector<std::thread> th;
-                std::vector<std::exception_ptr> errs(nthr);
-                std::atomic<int> next{0};
-                for (int w = 0; w < nthr; ++w)
-                    th.emplace_back([&, w] {
-                        try {
-                            std::vector<int> pos(nv, -1);
-                            for (int i; (i = next++) < int(ids.size());) factor_node(t, ids[i], A9, pos, 1);
-                        } catch (...) {
-                            errs[w] = std::current_exception();
-                        }
-                    });
-                for (auto& x : th) x.join();
-                for (auto& e : errs)
-                    if (e) std::rethrow_exception(e);
-            } else {
-                std::vector<int> pos(nv, -1);
-                for (int id : ids) factor_node(t, id, A9, pos, nthr);
-            }
-        }
+        const char* pt = std::getenv("HTG_ND_PIVTOL");
+        nd_factor(hp, t, env_int("HTG_ND_LEAF", 16), pt ? std::atof(pt) : 0.3);
+        nv_ = (t.CX + 1) * (t.CY + 1);
+        delayed_ = t.delayed;
         upload(t, st);
     }
     ~NDSolver() override {
@@ -612,6 +296,7 @@ class NDSolver : public CoarseSolver {
     std::vector<void*> allocs_;
     size_t bytes_ = 0;
     int nv_ = 0;
+    long long delayed_ = 0;
     NDArgs args_{};
 
     template <class T>
@@ -634,8 +319,8 @@ class NDSolver : public CoarseSolver {
         for (int i = 0; i < nn; ++i) {
             const NDNode& n = t.nodes[i];
             NodeDev& d = nd[i];
-            d.s = int(n.vars.size());
-            d.u = int(n.ring.size());
+            d.s = n.ke;
+            d.u = n.F - n.ke;
             d.off_F = fac_total;
             fac_total += (long long)d.s * d.s;
             d.off_L = fac_total;
@@ -645,9 +330,11 @@ class NDSolver : public CoarseSolver {
             d.off_Z = fac_total;
             fac_total += (long long)d.s * d.u;
             d.off_var = int(idx.size());
-            idx.insert(idx.end(), n.vars.begin(), n.vars.end());
+            idx.insert(idx.end(), n.cols.begin(), n.cols.begin() + n.ke);
             d.off_ring = int(idx.size());
-            idx.insert(idx.end(), n.ring.begin(), n.ring.end());
+            idx.insert(idx.end(), n.cols.begin() + n.ke, n.cols.end());
+            d.off_rc = int(idx.size());
+            idx.insert(idx.end(), n.rc.begin(), n.rc.end());
             d.off_front = front_total;
             front_total += d.s + d.u;
             d.off_contrib = contrib_total;
@@ -656,18 +343,24 @@ class NDSolver : public CoarseSolver {
             gsrc_total += d.s + d.u;
         }
         // gather plan: front position <- contribution entries of the children (child order)
-        std::vector<int2> gsrc(std::max(gsrc_total, 1), make_int2(-1, -1));
+        std::vector<int4> gsrc(std::max(gsrc_total, 1), make_int4(-1, -1, -1, -1));
+        std::vector<int> rpos(nv_, -1);
         for (int i = 0; i < nn; ++i) {
-            for (int c : t.nodes[i].children) {
+            const NDNode& n = t.nodes[i];
+            for (int k = 0; k < n.F; ++k) rpos[n.rows[k]] = k;
+            for (int c : n.children) {
                 const NDNode& ch = t.nodes[c];
-                for (int k = 0; k < int(ch.cmap.size()); ++k) {
-                    int2& e = gsrc[nd[i].off_gsrc + ch.cmap[k]];
+                for (int k = 0; k < ch.F - ch.ke; ++k) {
+                    int4& e = gsrc[nd[i].off_gsrc + rpos[ch.rows[ch.ke + k]]];
                     const int src = nd[c].off_contrib + k;
                     if (e.x < 0) e.x = src;
                     else if (e.y < 0) e.y = src;
-                    else throw RuntimeError("coarse solve: more than two contributions to a front position");
+                    else if (e.z < 0) e.z = src;
+                    else if (e.w < 0) e.w = src;
+                    else throw RuntimeError("coarse solve: more than four contributions to a front position");
                 }
             }
+            for (int k = 0; k < n.F; ++k) rpos[n.rows[k]] = -1;
         }
         void* facp = nullptr;
         HTG_CUDA(cudaMalloc(&facp, std::max<long long>(1, fac_total) * sizeof(double2)));

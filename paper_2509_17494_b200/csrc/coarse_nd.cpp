@@ -1,0 +1,377 @@
+// coarse_nd.cpp -- QSFEM coarse matrix and its nested-dissection multifrontal
+// LU, factored once on the host at setup (coarse.cu uploads the factors and
+// runs the level-batched solves on the GPU).
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <exception>
+#include <functional>
+#include <thread>
+
+#include "coarse.hpp"
+
+namespace htg {
+
+// ------------------------------------------------------------------ QSFEM
+QsfemWeights qsfem_weights(double eta) {
+    if (!(eta > 0.0) || !(eta < M_PI))
+        throw InvalidArgument("qsfem: eta = k*h_c must lie in (0, pi) (at least two coarse points per wavelength)");
+    // zero set of the symbol interpolated in the directions pi/16 and 3pi/16
+    const double a1 = std::cos(eta * std::cos(M_PI / 16.0)), b1 = std::cos(eta * std::sin(M_PI / 16.0));
+    const double a2 = std::cos(eta * std::cos(3.0 * M_PI / 16.0)), b2 = std::cos(eta * std::sin(3.0 * M_PI / 16.0));
+    const double den = a2 * b2 * (a1 + b1) - a1 * b1 * (a2 + b2);
+    if (std::fabs(den) < 1e-14) throw RuntimeError("qsfem: degenerate stencil (denominator ~ 0)");
+    QsfemWeights w;
+    w.eta = eta;
+    w.P0 = 4.0;
+    w.P1 = 2.0 * (a1 * b1 - a2 * b2) / den;
+    w.P2 = (a2 + b2 - a1 - b1) / den;
+    const double sigma0 = w.P0 + 4.0 * w.P1 + 4.0 * w.P2;  // symbol at the origin
+    if (sigma0 == 0.0) throw RuntimeError("qsfem: sigma_P(0) = 0, scaling undefined");
+    w.N = -eta * eta / sigma0;
+    w.q0 = w.N * w.P0 / 4.0;
+    w.q1 = w.N * w.P1 / 2.0;
+    w.q2 = w.N * w.P2;
+    return w;
+}
+
+std::vector<cplx> coarse_stencil(const HostProblem& hp) {
+    const int m = hp.p / 2, CX = hp.nx * m, CY = hp.ny * m;
+    const double hc = 2.0 * hp.h / hp.p;
+    const size_t nv = size_t(CX + 1) * (CY + 1);
+    std::vector<cplx> A9(nv * 9, cplx(0.0));
+    std::vector<QsfemWeights> qw(hp.cls_k.size());
+    for (size_t c = 0; c < qw.size(); ++c) qw[c] = qsfem_weights(hc * hp.cls_k[c]);
+    auto cellcls = [&](int cx, int cy) { return hp.cls[size_t(cy / m) * hp.nx + cx / m]; };
+    auto cdir = [&](int X, int Y) {
+        if (!hp.has_dirichlet) return false;
+        bool d = false;
+        if (X == 0 || X == CX) {
+            const auto& tg = X == 0 ? hp.tl : hp.tr;
+            d |= (Y > 0 && tg[(Y - 1) / m] == kDirichlet) || (Y < CY && tg[Y / m] == kDirichlet);
+        }
+        if (Y == 0 || Y == CY) {
+            const auto& tg = Y == 0 ? hp.tb : hp.tt;
+            d |= (X > 0 && tg[(X - 1) / m] == kDirichlet) || (X < CX && tg[X / m] == kDirichlet);
+        }
+        return d;
+    };
+    for (int Y = 0; Y <= CY; ++Y)
+        for (int X = 0; X <= CX; ++X) {
+            cplx* row = &A9[(size_t(Y) * (CX + 1) + X) * 9];
+            if (cdir(X, Y)) {
+                row[4] = 1.0;
+                continue;
+            }
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                    const int WX = X + dx, WY = Y + dy;
+                    if (WX < 0 || WX > CX || WY < 0 || WY > CY || cdir(WX, WY)) continue;
+                    cplx s = 0.0;
+                    for (int cy = std::max(std::max(Y, WY) - 1, 0); cy <= std::min(std::min(Y, WY), CY - 1); ++cy)
+                        for (int cx = std::max(std::max(X, WX) - 1, 0); cx <= std::min(std::min(X, WX), CX - 1); ++cx) {
+                            const int c = cellcls(cx, cy);
+                            const QsfemWeights& q = qw[c];
+                            const int md = std::abs(dx) + std::abs(dy);
+                            const double qv = md == 0 ? q.q0 : (md == 1 ? q.q1 : q.q2);
+                            const double mass = double((dx == 0 ? 2 : 1) * (dy == 0 ? 2 : 1)) / 36.0;
+                            s += cplx(qv, -hp.cls_eps[c] * hc * hc * mass);
+                        }
+                    // absorbing coarse boundary edges containing both vertices
+                    auto robin = [&](const std::vector<double>& kh, int e) {
+                        const double khc = kh[e / m] / m;
+                        s += cplx(0.0, -khc * ((dx == 0 && dy == 0) ? 1.0 / 3.0 : 1.0 / 6.0));
+                    };
+                    if (dy == 0 && (Y == 0 || Y == CY)) {
+                        const auto& kh = Y == 0 ? hp.khb : hp.kht;
+                        if (dx <= 0 && X > 0) robin(kh, X - 1);
+                        if (dx >= 0 && X < CX) robin(kh, X);
+                    }
+                    if (dx == 0 && (X == 0 || X == CX)) {
+                        const auto& kh = X == 0 ? hp.khl : hp.khr;
+                        if (dy <= 0 && Y > 0) robin(kh, Y - 1);
+                        if (dy >= 0 && Y < CY) robin(kh, Y);
+                    }
+                    row[(dy + 1) * 3 + (dx + 1)] = s;
+                }
+        }
+    return A9;
+}
+
+// ------------------------------------------------------------------ nested dissection
+namespace {
+
+int build_nd(NDTree& t, int x0, int x1, int y0, int y1, int depth, int leaf_max) {
+    NDNode n;
+    n.x0 = x0;
+    n.x1 = x1;
+    n.y0 = y0;
+    n.y1 = y1;
+    n.depth = depth;
+    const int w = x1 - x0 + 1, h = y1 - y0 + 1;
+    std::vector<int> kids;
+    if (w * h <= leaf_max || std::max(w, h) < 3) {
+        n.leaf = true;
+        for (int y = y0; y <= y1; ++y)
+            for (int x = x0; x <= x1; ++x) n.vars.push_back(y * (t.CX + 1) + x);
+    } else if (w >= h) {
+        const int xm = (x0 + x1) / 2;
+        kids.push_back(build_nd(t, x0, xm - 1, y0, y1, depth + 1, leaf_max));
+        kids.push_back(build_nd(t, xm + 1, x1, y0, y1, depth + 1, leaf_max));
+        for (int y = y0; y <= y1; ++y) n.vars.push_back(y * (t.CX + 1) + xm);
+    } else {
+        const int ym = (y0 + y1) / 2;
+        kids.push_back(build_nd(t, x0, x1, y0, ym - 1, depth + 1, leaf_max));
+        kids.push_back(build_nd(t, x0, x1, ym + 1, y1, depth + 1, leaf_max));
+        for (int x = x0; x <= x1; ++x) n.vars.push_back(ym * (t.CX + 1) + x);
+    }
+    for (int y = y0 - 1; y <= y1 + 1; ++y)
+        for (int x = x0 - 1; x <= x1 + 1; ++x) {
+            if (x < 0 || y < 0 || x > t.CX || y > t.CY) continue;
+            if (x >= x0 && x <= x1 && y >= y0 && y <= y1) continue;
+            n.ring.push_back(y * (t.CX + 1) + x);
+        }
+    n.children = kids;
+    t.max_depth = std::max(t.max_depth, depth);
+    t.nodes.push_back(std::move(n));
+    const int id = int(t.nodes.size()) - 1;
+    for (int k : kids) t.nodes[k].parent = id;
+    return id;
+}
+
+// C[rows i0..i1) -= A (m x k) * B (k x n), row-major, parallel over rows
+void gemm_sub(int m, int n, int k, const cplx* A, const cplx* B, cplx* C, int nthreads) {
+    auto body = [&](int i0, int i1) {
+        for (int i = i0; i < i1; ++i) {
+            cplx* ci = C + size_t(i) * n;
+            const cplx* ai = A + size_t(i) * k;
+            for (int kk = 0; kk < k; ++kk) {
+                const cplx a = ai[kk];
+                if (a == cplx(0.0)) continue;
+                const cplx* bk = B + size_t(kk) * n;
+                for (int j = 0; j < n; ++j) ci[j] -= a * bk[j];
+            }
+        }
+    };
+    if (nthreads <= 1 || size_t(m) * n * k < 2000000) {
+        body(0, m);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (int t = 0; t < nthreads; ++t) th.emplace_back(body, m * t / nthreads, m * (t + 1) / nthreads);
+    for (auto& x : th) x.join();
+}
+
+void parallel_rows(int m, int nthreads, const std::function<void(int, int)>& body, size_t work) {
+    if (nthreads <= 1 || work < 2000000) {
+        body(0, m);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (int t = 0; t < nthreads; ++t) th.emplace_back(body, m * t / nthreads, m * (t + 1) / nthreads);
+    for (auto& x : th) x.join();
+}
+
+// Factor one front (children already factored). rpos/cpos: scratch
+// global -> front row / column maps (all -1 on entry and exit).
+//
+// Front rows are [own separator vars | rows delayed by the children | ring],
+// columns [own vars | columns delayed by the children | ring]. LU with
+// threshold partial pivoting over the pivot block (the first sN rows and
+// columns): column k is eliminated only if its best pivot candidate is at
+// least pivtol times the largest entry of that column in the ring rows, which
+// bounds the multipliers L21 by 1/pivtol. A column that fails is delayed: it
+// is swapped to the end of the pivot block and, with the same number of
+// unpivoted rows, handed to the parent as part of the contribution block.
+// Pivoting restricted to one front cannot otherwise cope with the nearly
+// singular pivot blocks of boxes close to a Dirichlet resonance (Helmholtz),
+// and the growth it lets through costs ~cond * eps in backward error.
+void factor_node(NDTree& t, int id, const std::vector<cplx>& A9, std::vector<int>& rpos, std::vector<int>& cpos,
+                 double pivtol, int nthreads) {
+    NDNode& n = t.nodes[id];
+    std::vector<int> rows = n.vars, cols = n.vars;
+    for (int c : n.children) {
+        const NDNode& ch = t.nodes[c];
+        rows.insert(rows.end(), ch.rows.begin() + ch.ke, ch.rows.begin() + ch.sN);
+        cols.insert(cols.end(), ch.cols.begin() + ch.ke, ch.cols.begin() + ch.sN);
+    }
+    const int nown = int(n.vars.size()), sN = int(rows.size()), u = int(n.ring.size()), F = sN + u;
+    rows.insert(rows.end(), n.ring.begin(), n.ring.end());
+    cols.insert(cols.end(), n.ring.begin(), n.ring.end());
+    for (int i = 0; i < F; ++i) {
+        rpos[rows[i]] = i;
+        cpos[cols[i]] = i;
+    }
+    std::vector<cplx> Fm(size_t(F) * F, cplx(0.0));
+    const int W = t.CX + 1;
+    // original entries not assembled below: own-var rows against own and ring
+    // columns, and ring rows against own columns (a delayed variable's
+    // couplings already sit in the child's contribution block)
+    auto fresh = [&](int p) { return p >= 0 && (p < nown || p >= sN); };
+    for (int i = 0; i < nown; ++i) {
+        const int v = n.vars[i], X = v % W, Y = v / W;
+        for (int dy = -1; dy <= 1; ++dy)
+            for (int dx = -1; dx <= 1; ++dx) {
+                const int WX = X + dx, WY = Y + dy;
+                if (WX < 0 || WX > t.CX || WY < 0 || WY > t.CY) continue;
+                const int w = WY * W + WX, pw = cpos[w];
+                if (!fresh(pw)) continue;
+                Fm[size_t(i) * F + pw] += A9[size_t(v) * 9 + (dy + 1) * 3 + (dx + 1)];
+                if (pw >= sN) Fm[size_t(rpos[w]) * F + i] += A9[size_t(w) * 9 + (1 - dy) * 3 + (1 - dx)];
+            }
+    }
+    for (int c : n.children) {
+        NDNode& ch = t.nodes[c];
+        const int uc = ch.F - ch.ke;
+        std::vector<int> rm(uc), cm(uc);
+        for (int a = 0; a < uc; ++a) {
+            rm[a] = rpos[ch.rows[ch.ke + a]];
+            cm[a] = cpos[ch.cols[ch.ke + a]];
+        }
+        for (int a = 0; a < uc; ++a)
+            for (int b = 0; b < uc; ++b) Fm[size_t(rm[a]) * F + cm[b]] += ch.S[size_t(a) * uc + b];
+    }
+    for (int i = 0; i < F; ++i) {
+        rpos[rows[i]] = -1;
+        cpos[cols[i]] = -1;
+    }
+
+    int k = 0, last = sN;  // columns [k, last) are still candidates
+    while (k < last) {
+        int p = k;
+        double best = std::abs(Fm[size_t(k) * F + k]);
+        for (int i = k + 1; i < sN; ++i) {
+            const double a = std::abs(Fm[size_t(i) * F + k]);
+            if (a > best) {
+                best = a;
+                p = i;
+            }
+        }
+        double ringmax = 0.0;
+        for (int i = sN; i < F; ++i) ringmax = std::max(ringmax, std::abs(Fm[size_t(i) * F + k]));
+        if (best == 0.0 || best < pivtol * ringmax) {
+            if (u == 0) throw RuntimeError("coarse LU: singular root front (zero pivot)");
+            --last;  // delay column k
+            for (int i = 0; i < F; ++i) std::swap(Fm[size_t(i) * F + k], Fm[size_t(i) * F + last]);
+            std::swap(cols[k], cols[last]);
+            continue;
+        }
+        if (p != k) {
+            std::swap_ranges(Fm.begin() + size_t(k) * F, Fm.begin() + size_t(k) * F + F, Fm.begin() + size_t(p) * F);
+            std::swap(rows[k], rows[p]);
+        }
+        const cplx inv = 1.0 / Fm[size_t(k) * F + k];
+        const cplx* rk = &Fm[size_t(k) * F];
+        auto elim = [&](int i0, int i1) {
+            for (int i = k + 1 + i0; i < k + 1 + i1; ++i) {
+                cplx* ri = &Fm[size_t(i) * F];
+                if (ri[k] == cplx(0.0)) continue;
+                const cplx l = ri[k] * inv;
+                ri[k] = l;
+                for (int j = k + 1; j < F; ++j) ri[j] -= l * rk[j];
+            }
+        };
+        const int nrows = F - k - 1;
+        parallel_rows(nrows, nthreads, elim, size_t(nrows) * (F - k));
+        ++k;
+    }
+    const int ke = k, r = F - ke;  // eliminated here / handed to the parent
+    n.sN = sN;
+    n.F = F;
+    n.ke = ke;
+    n.rc.assign(F, -1);  // right-hand side entries injected at this front: own-var rows
+    {
+        std::vector<char> own(size_t(t.CX + 1) * (t.CY + 1), 0);
+        for (int v : n.vars) own[v] = 1;
+        for (int i = 0; i < F; ++i)
+            if (own[rows[i]]) n.rc[i] = rows[i];
+    }
+    // Now rows [0, ke): unit L11 (cols < ke), U11 (cols >= row, < ke), U12 (cols >= ke);
+    //     rows [ke, F): L21 (cols < ke), S (cols >= ke) -- the contribution block.
+    n.S.assign(size_t(r) * r, cplx(0.0));
+    for (int i = 0; i < r; ++i)
+        for (int j = 0; j < r; ++j) n.S[size_t(i) * r + j] = Fm[size_t(ke + i) * F + ke + j];
+    n.L21.assign(size_t(r) * ke, cplx(0.0));
+    for (int i = 0; i < r; ++i)
+        for (int j = 0; j < ke; ++j) n.L21[size_t(i) * ke + j] = Fm[size_t(ke + i) * F + j];
+    // Finv = L11^-1 (the row permutation is folded into the front's row order)
+    n.Finv.assign(size_t(ke) * ke, cplx(0.0));
+    for (int c = 0; c < ke; ++c) {
+        n.Finv[size_t(c) * ke + c] = 1.0;
+        for (int i = c + 1; i < ke; ++i) {
+            cplx acc = 0.0;
+            for (int k2 = c; k2 < i; ++k2) acc += Fm[size_t(i) * F + k2] * n.Finv[size_t(k2) * ke + c];
+            n.Finv[size_t(i) * ke + c] = -acc;
+        }
+    }
+    n.Uinv.assign(size_t(ke) * ke, cplx(0.0));
+    for (int c = ke - 1; c >= 0; --c) {
+        n.Uinv[size_t(c) * ke + c] = 1.0 / Fm[size_t(c) * F + c];
+        for (int i = c - 1; i >= 0; --i) {
+            cplx acc = 0.0;
+            for (int k2 = i + 1; k2 <= c; ++k2) acc += Fm[size_t(i) * F + k2] * n.Uinv[size_t(k2) * ke + c];
+            n.Uinv[size_t(i) * ke + c] = -acc / Fm[size_t(i) * F + i];
+        }
+    }
+    // Z = Uinv U12
+    n.Z.assign(size_t(ke) * r, cplx(0.0));
+    if (r > 0 && ke > 0) {
+        std::vector<cplx> U12(size_t(ke) * r);
+        for (int i = 0; i < ke; ++i)
+            for (int j = 0; j < r; ++j) U12[size_t(i) * r + j] = Fm[size_t(i) * F + ke + j];
+        std::vector<cplx> negZ(size_t(ke) * r, cplx(0.0));
+        gemm_sub(ke, r, ke, n.Uinv.data(), U12.data(), negZ.data(), nthreads);
+        for (size_t i = 0; i < negZ.size(); ++i) n.Z[i] = -negZ[i];
+    }
+    n.rows.swap(rows);
+    n.cols.swap(cols);
+}
+
+}  // namespace
+
+void nd_factor(const HostProblem& hp, NDTree& t, int leaf_max, double pivtol) {
+    const int m = hp.p / 2;
+    t.CX = hp.nx * m;
+    t.CY = hp.ny * m;
+    const int nv = (t.CX + 1) * (t.CY + 1);
+    build_nd(t, 0, t.CX, 0, t.CY, 0, leaf_max);
+    const std::vector<cplx> A9 = coarse_stencil(hp);
+    // factor bottom-up by depth; nodes of one depth in parallel
+    const int nthr = std::max(1, int(std::thread::hardware_concurrency()));
+    std::vector<std::vector<int>> bydepth(t.max_depth + 1);
+    for (int i = 0; i < int(t.nodes.size()); ++i) bydepth[t.nodes[i].depth].push_back(i);
+    for (int d = t.max_depth; d >= 0; --d) {
+        const auto& ids = bydepth[d];
+        if (int(ids.size()) >= nthr) {
+            std::vector<std::thread> th;
+            std::vector<std::exception_ptr> errs(nthr);
+            std::atomic<int> next{0};
+            for (int w = 0; w < nthr; ++w)
+                th.emplace_back([&, w] {
+                    try {
+                        std::vector<int> rpos(nv, -1), cpos(nv, -1);
+                        for (int i; (i = next++) < int(ids.size());)
+                            factor_node(t, ids[i], A9, rpos, cpos, pivtol, 1);
+                    } catch (...) {
+                        errs[w] = std::current_exception();
+                    }
+                });
+            for (auto& x : th) x.join();
+            for (auto& e : errs)
+                if (e) std::rethrow_exception(e);
+        } else {
+            std::vector<int> rpos(nv, -1), cpos(nv, -1);
+            for (int id : ids) factor_node(t, id, A9, rpos, cpos, pivtol, nthr);
+        }
+        for (int id : ids) {
+            const NDNode& n = t.nodes[id];
+            t.delayed += n.sN - n.ke;
+            t.max_front = std::max(t.max_front, n.F);
+            for (int c : n.children) std::vector<cplx>().swap(t.nodes[c].S);
+        }
+    }
+}
+
+}  // namespace htg

@@ -154,3 +154,28 @@ def test_readme_krylov_iters_7(W):
     ops = hb.setup_two_grid(prob, hb.SolverConfig(outer=hb.KRYLOV))
     res = ops.solve(torch.from_numpy(prob.rhs).cuda())
     assert ops.ndof == 40401 and res.converged and res.iterations == 7
+
+
+def test_cfg2_substitute_layer():
+    """BASELINE cfg2 (Q3) is rejected by the reference (fespace.cpp:11-16); its
+    substitute is Q4 at the same dof count: 40 wavelengths, 12 ppw (120x120
+    cells), sin^2 layer on left+bottom with Neumann behind, point source plus
+    1e-3 seeded noise. Mixed separable / non-separable
+    subdomain classes, full solve and one step against the oracle."""
+    import paper_2509_17494_b200 as hb
+    torch = _torch()
+    kw = dict(order=4, wavelengths=40, ppw=12, side_tags=(N_, A_, N_, A_), layer_sides=(po.LEFT, po.BOTTOM))
+    oses = po.Session(po.ProblemSpec(**kw), po.SolverConfig())
+    prob = hb.build_problem(hb.ProblemSpec(**kw))
+    ops = hb.setup_two_grid(prob, hb.SolverConfig())
+    assert ops.ndof == 231361 and 0 < ops.fdm_subdomains < ops.n_subdomains
+    g = np.random.default_rng(1002)
+    f = prob.rhs + 1e-3 * (g.standard_normal(ops.ndof) + 1j * g.standard_normal(ops.ndof))
+    u0 = po.random_vector(ops.ndof, 9)
+    ud = dev(u0)
+    ops.two_grid_step(ud, dev(f))
+    assert rel(host(ud), oses.two_grid_step(u0, f)) <= TOL
+    ro = oses.solve(f)
+    rg = ops.solve(dev(f))
+    assert rg.converged and ro.converged and abs(rg.iterations - ro.iterations) <= 1
+    assert rel(host(rg.u), ro.u) <= 1e-8
