@@ -129,8 +129,7 @@ template <int P>
 struct K1Smem {
     using C = K1Cfg<P>;
     double2 U[3][C::SEG];  // u rows y, y+1, y+2 (ring)
-    double2 F[2][C::SEG];  // f rows (ring)
-    double2 R[2][C::SEG];  // r rows staged for the bulk store (ring)
+    double2 F[2][C::SEG];  // f rows (ring); r overwrites f in place and is bulk-stored from here
     double2 T[kK1Threads][C::B];
     double2 V[kK1Threads][C::B];
     double2 Z[kK1Threads][2];
@@ -204,24 +203,26 @@ __global__ void __launch_bounds__(kK1Threads) k1_residual(K1Args a) {
         sm.E[i / (MM + 1)][i % (MM + 1)] = c_E[P / 2 - 1][i / (MM + 1)][i % (MM + 1)];
 
     const int nx = g.nx, ny = g.ny, NG = nx * P + 1;
-    const int x0 = blockIdx.x * W;
+    // balanced strips / row blocks (at most W cells per strip)
+    const int x0 = int((long long)blockIdx.x * g.nx / gridDim.x);
+    const int xe = int((long long)(blockIdx.x + 1) * g.nx / gridDim.x);
     const int G0 = max(x0 * P - P, 0);
     const int gx = G0 + tid;
-    const int gend = min((x0 + W) * P + 1, NG);
+    const int gend = min(xe * P + 1, NG);
     const bool valid = gx < gend;
-    const int own_lo = x0 * P, own_hi = (x0 + W >= nx) ? NG : (x0 + W) * P;
+    const int own_lo = x0 * P, own_hi = (xe >= nx) ? NG : xe * P;
     const bool owned = valid && gx >= own_lo && gx < own_hi;
     const int x = gx / P, j = gx - x * P;
     const bool halo_bubble = valid && !owned && j > 0 && x == x0 - 1;
     const bool emit = owned || (MODE == kK1Restrict && halo_bubble);
-    const int ys = blockIdx.y * a.rows, ye = min(ys + a.rows, ny);
+    const int ys = int((long long)blockIdx.y * ny / gridDim.y), ye = int((long long)(blockIdx.y + 1) * ny / gridDim.y);
     const int nhalo = MODE == kK1Restrict ? 2 : 1;
     const int ystart = max(ys - nhalo, 0);
     const double2* mt = a.shifted ? g.mtabS : g.mtab0;
     auto coef = [&](int xc, int y) -> double2 { return mt[g.cls ? g.cls[(size_t)y * nx + xc] : 0]; };
     const double2 zero = make_double2(0.0, 0.0);
-    const int xa = max(x0 - 1, 0), xb = min(x0 + W, nx);                  // staged unit cells (u, f)
-    const int xo = (x0 + W >= nx) ? nx : x0 + W - 1;                      // last owned unit cell
+    const int xa = max(x0 - 1, 0), xb = xe;                               // staged unit cells (u, f)
+    const int xo = (xe >= nx) ? nx : xe - 1;                              // last owned unit cell
     auto seg_lo = [&](int yy) { return unit_off<P>(nx, ny, xa, yy); };
     auto seg_bytes = [&](int yy) {
         return unsigned((unit_off<P>(nx, ny, xb, yy) + unit_size<P>(nx, ny, xb, yy) - seg_lo(yy)) * 16);
@@ -285,7 +286,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_residual(K1Args a) {
     // r rows: lattice row yy -> R slot; write into smem, bulk store by thread 0
     auto emit_row = [&](int yy, int nj, const double2* Au, const double2* ur, double2* rr) {
         wait_f(yy);
-        const double2* Fs = sm.F[(yy - yout0) & 1];
+        double2* Fs = sm.F[(yy - yout0) & 1];
         const bool topr = yy == ny;
         for (int jy = 0; jy < nj; ++jy) {
             const int gy = yy * P + jy;
@@ -294,18 +295,15 @@ __global__ void __launch_bounds__(kK1Threads) k1_residual(K1Args a) {
             const double2 fv = Fs[topr ? off_top : off_mid[jy]];
             rr[jy] = csub(fv, A);
         }
-        if (MODE == kK1Write && owned) {
-            double2* Rs = sm.R[(yy - yout0) & 1];
-            for (int jy = 0; jy < nj; ++jy)
-                Rs[topr ? off_top - rshift * P : off_mid[jy] - rshift * P * P] = rr[jy];
-        }
+        if (MODE == kK1Write && owned)  // in place: each position is read and written by its own thread
+            for (int jy = 0; jy < nj; ++jy) Fs[topr ? off_top : off_mid[jy]] = rr[jy];
     };
     auto store_row = [&](int yy) {
         // all threads: make smem writes visible to the async proxy, then one thread stores
         fence_async_smem();
         __syncthreads();
         if (tid == 0) {
-            tma_store_1d(a.r + rseg_lo(yy), sm.R[(yy - yout0) & 1], rseg_bytes(yy));
+            tma_store_1d(a.r + rseg_lo(yy), sm.F[(yy - yout0) & 1] + rshift * (yy < ny ? P * P : P), rseg_bytes(yy));
             bulk_commit();
         }
     };
@@ -335,7 +333,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_residual(K1Args a) {
 #pragma unroll
         for (int i = 0; i < MM; ++i) sm.Rt[tid][i] = t[i];
         __syncthreads();
-        const int cX0 = x0 * MM, cXend = (x0 + W >= nx) ? nx * MM + 1 : (x0 + W) * MM;
+        const int cX0 = x0 * MM, cXend = (xe >= nx) ? nx * MM + 1 : xe * MM;
         const int ncx = cXend - cX0;
         const int nrow = (nj == 1 && y == ny) ? 1 : MM;
         for (int w = tid; w < ncx * nrow; w += kK1Threads) {
@@ -455,8 +453,6 @@ __global__ void __launch_bounds__(kK1Threads) k1_residual(K1Args a) {
 #pragma unroll
         for (int jy = 0; jy < P; ++jy) rr[jy] = zero;
         if (out_row) {
-            if (MODE == kK1Write && y - 2 >= yout0 && tid == 0) bulk_wait_read<1>();  // R slot reuse
-            if (MODE == kK1Write) __syncthreads();
             if (emit) {
                 double2 Au[P], ur[P];
                 Au[0] = cadd(O[0], carryO);
@@ -477,13 +473,14 @@ __global__ void __launch_bounds__(kK1Threads) k1_residual(K1Args a) {
         }
         carryO = O[1];
         __syncthreads();  // F slot of row y and U slot of row y are free after this
-        if (tid == 0 && out_row && y + 2 <= ylast) issue_f(y + 2);
+        if (tid == 0 && out_row && y + 2 <= ylast) {
+            if (MODE == kK1Write) bulk_wait_read<0>();  // the slot's r row has been read by its store
+            issue_f(y + 2);
+        }
     }
     // top lattice row (vertex / h-edge dofs only): the carried b = 1 contributions
     if (top) {
         double2 rr[1] = {zero};
-        if (MODE == kK1Write && ny - 2 >= yout0 && tid == 0) bulk_wait_read<1>();
-        if (MODE == kK1Write) __syncthreads();
         if (emit) {
             double2 Au[1] = {carryO}, ur[1] = {uval(ny, 0)};
             emit_row(ny, 1, Au, ur, rr);
@@ -501,6 +498,374 @@ __global__ void __launch_bounds__(kK1Threads) k1_residual(K1Args a) {
             double s = 0.0;
             for (int w = 0; w < kK1Threads / 32; ++w) s += sm.red[w];
             a.partial[blockIdx.y * gridDim.x + blockIdx.x] = s;
+        }
+    }
+}
+
+
+// ---------------------------------------------------------------- K1, one thread per cell (p <= 4)
+// Each thread owns one unit cell (its p^2 dofs: bottom-left vertex, bottom and
+// left edge bubbles, interior) and keeps the whole element contraction in
+// registers: per local column cl the y contraction T = M z, V = S z, W = V - m T,
+// then O[al][.] += S[al][cl] T + M[al][cl] W. Shared nodes are completed by
+// (a) handing the right column O[1][.] to the right neighbour (shared memory
+// exchange) and (b) carrying the top row O[.][1] in registers to the next cell
+// row of the same thread. u / f row segments are staged with cp.async into a
+// shared-memory layout padded to an odd unit stride (p^2 + 1 entries), so the
+// per-thread unit reads are bank-conflict free while the global loads and the
+// r stores stay fully coalesced.
+constexpr int kKCThreads = 120;
+
+template <int P>
+struct KCCfg {
+    static constexpr int B = P + 1, MM = P / 2, UD = P * P, SU = P * P + 1;
+    static constexpr int H = 2;                     // halo cells on the left (restrict mode needs 2)
+    static constexpr int C = kKCThreads - H - 1;    // owned cells per strip (one thread left for x = nx)
+    static constexpr int NU = kKCThreads + 1;       // staged units per row: threads + right neighbour
+    static constexpr int NF = 3;                    // f slots (a slot is re-filled two rows after its r store)
+};
+
+template <int P>
+struct KCSmem {
+    using C = KCCfg<P>;
+    double2 U[3][C::NU * C::SU];
+    double2 F[C::NF][C::NU * C::SU];
+    double2 X[2][kKCThreads][C::B];     // right-column exchange, double-buffered by row parity
+    double2 XP[kKCThreads][C::MM + 1];  // restriction partials exchange
+    double red[kKCThreads];
+};
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// position of local node (a, b) of unit cell row y < ny inside its unit (a, b != 1)
+template <int P>
+__device__ __forceinline__ constexpr int upos(int a, int b) {
+    return a == 0 ? (b == 0 ? 0 : P + b - 2) : (b == 0 ? a - 1 : 2 * P - 1 + (a - 2) * (P - 1) + (b - 2));
+}
+
+template <int P, int MODE>
+__global__ void __launch_bounds__(kKCThreads, 1) k1_cells(K1Args a) {
+    using Cf = KCCfg<P>;
+    constexpr int B = Cf::B, MM = Cf::MM, SU = Cf::SU, NT = kKCThreads;
+    constexpr int SL = P / 2 - 1;  // basis table slot
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    KCSmem<P>& sm = *reinterpret_cast<KCSmem<P>*>(smem_raw);
+    const FineGeom& g = a.g;
+    const int tid = threadIdx.x, nx = g.nx, ny = g.ny;
+    const double2 zero = make_double2(0.0, 0.0);
+
+    const int x0 = int((long long)blockIdx.x * nx / gridDim.x);
+    const int xe = int((long long)(blockIdx.x + 1) * nx / gridDim.x);
+    const int H = MODE == kK1Restrict ? 2 : 1;
+    const int xa = max(x0 - H, 0);
+    const int xlast = xe == nx ? nx : xe - 1;  // last unit with outputs (x = nx: right boundary column)
+    const int xb = xe;                          // last staged unit (right neighbour of the last cell)
+    const int ux = xa + tid;
+    const bool active = ux <= xlast;
+    const bool cell = active && ux < nx;
+    const bool owned = active && ux >= x0;
+    const bool resid = owned || (MODE == kK1Restrict && active && ux == x0 - 1);
+    const int ys = int((long long)blockIdx.y * ny / gridDim.y), ye = int((long long)(blockIdx.y + 1) * ny / gridDim.y);
+    const int nhalo = MODE == kK1Restrict ? 2 : 1;
+    const int ystart = max(ys - nhalo, 0);
+    const int yres0 = MODE == kK1Restrict ? max(ys - 1, 0) : ys;  // first row whose residual is needed
+    const bool top = ye == ny;
+    const double2* mt = a.shifted ? g.mtabS : g.mtab0;
+
+    // Row staging: coalesced 16-byte cp.async chunks into the padded unit layout.
+    auto stage = [&](double2* dst, const double2* src, int yy) {
+        const long long lo = unit_off<P>(nx, ny, xa, yy);
+        const int n = int(unit_off<P>(nx, ny, xb, yy) + unit_size<P>(nx, ny, xb, yy) - lo);
+        const int usz = yy < ny ? P * P : P;
+        for (int e = tid; e < n; e += NT) {
+            const int uu = e / usz;
+            cp_async16(dst + uu * SU + (e - uu * usz), src + lo + e);
+        }
+    };
+    auto uslot = [&](int yy) { return sm.U[(yy - ystart) % 3]; };
+    auto fslot = [&](int yy) { return sm.F[(yy - yres0) % Cf::NF]; };
+    // prologue: u rows ystart, ystart + 1 and f row ystart
+    stage(uslot(ystart), a.u, ystart);
+    if (ystart + 1 <= ye) stage(uslot(ystart + 1), a.u, ystart + 1);
+    if (ystart >= yres0) stage(fslot(ystart), a.f, ystart);
+    cp_commit();
+
+    double2 carry[B];  // O[al][1] of the previous cell row (al != 1)
+#pragma unroll
+    for (int i = 0; i < B; ++i) carry[i] = zero;
+    double2 pcarry[MM + 1];  // restriction partials of the previous row, coarse row y*m
+#pragma unroll
+    for (int i = 0; i <= MM; ++i) pcarry[i] = zero;
+    double acc = 0.0;
+
+    // copy the owned range of r row yy (written in place into its f slot) to global, coalesced
+    auto store_row = [&](int yy) {
+        const double2* src = fslot(yy);
+        const long long lo = unit_off<P>(nx, ny, x0, yy);
+        const int n = int(unit_off<P>(nx, ny, xlast, yy) + unit_size<P>(nx, ny, xlast, yy) - lo);
+        const int usz = yy < ny ? P * P : P;
+        const int ush = x0 - xa;
+        for (int e = tid; e < n; e += NT) {
+            const int uu = e / usz;
+            a.r[lo + e] = src[(uu + ush) * SU + (e - uu * usz)];
+        }
+    };
+    // coarse restriction weights: wgt(d, j) for local node index d (0: vertex at j = 0)
+    auto wgt = [&](int d, int j) -> double { return d == 0 ? (j == 0 ? 1.0 : 0.0) : c_E[SL][d][j]; };
+    const int CXn = nx * MM + 1;
+    auto write_rc = [&](int X, int Y, double2 v) {
+        if (g.has_dirichlet && coarse_dir(g, MM, X, Y)) v = zero;
+        a.rc[(size_t)Y * CXn + X] = v;
+    };
+
+    for (int y = ystart; y < ye; ++y) {
+        // Prefetch u(y + 2) into the slot of u(y - 1) and f(y + 1) into the slot of
+        // f(y - 2). Every read of u(y - 1) precedes the last barrier of row y - 1
+        // (compute: exchange barrier; Dirichlet reads: store / partials barrier, or
+        // the extra barrier below), and every read of f(y - 2) precedes the staging
+        // barrier of row y - 1.
+        if (y + 2 <= ye) stage(uslot(y + 2), a.u, y + 2);
+        if (y + 1 >= yres0 && (y + 1 < ye || (top && y + 1 == ny))) stage(fslot(y + 1), a.f, y + 1);
+        cp_commit();
+        cp_wait<1>();
+        __syncthreads();
+        const double2* Uy = uslot(y);
+        const double2* Uy1 = uslot(y + 1);
+        const double2* own = Uy + tid * SU;
+        const double2* rn = Uy + (tid + 1) * SU;
+        const double2* tp = Uy1 + tid * SU;
+        const double2* tpr = Uy1 + (tid + 1) * SU;
+        const bool rn_edge = ux + 1 == nx;  // right neighbour is the x = nx column unit (p dofs)
+        auto zval = [&](int cl, int b) -> double2 {
+            double2 v;
+            if (cl == 1) v = b == 0 ? rn[0] : (b == 1 ? tpr[0] : rn[rn_edge ? b - 1 : P + b - 2]);
+            else if (b == 1) v = tp[cl == 0 ? 0 : cl - 1];
+            else v = own[upos<P>(cl, b)];
+            if (g.has_dirichlet && fine_dir<P>(g, lidx<P>(ux, cl), lidx<P>(y, b))) v = zero;
+            return v;
+        };
+        double2 O[B][B];
+#pragma unroll
+        for (int i = 0; i < B; ++i)
+#pragma unroll
+            for (int j = 0; j < B; ++j) O[i][j] = zero;
+        if (cell) {
+            const double2 m = mt[g.cls ? g.cls[(size_t)y * nx + ux] : 0];
+#pragma unroll
+            for (int cl = 0; cl < B; ++cl) {
+                double2 zc[B];
+#pragma unroll
+                for (int b = 0; b < B; ++b) zc[b] = zval(cl, b);
+                double2 T[B], Wv[B];
+#pragma unroll
+                for (int bp = 0; bp < B; ++bp) {
+                    double2 t = zero, v = zero;
+#pragma unroll
+                    for (int b = 0; b < B; ++b) {
+                        if (nzM(bp, b)) t = rfma(c_M[SL][bp][b], zc[b], t);
+                        if (nzS(bp, b)) v = rfma(c_S[SL][bp][b], zc[b], v);
+                    }
+                    T[bp] = t;
+                    Wv[bp] = csub(v, cmul(m, t));
+                }
+                if (cl == 0 && ux == 0) {
+                    const double kh = g.kh_l[y];
+#pragma unroll
+                    for (int bp = 0; bp < B; ++bp) O[0][bp] = cadd(O[0][bp], mik(kh, T[bp]));
+                }
+                if (cl == 1 && ux == nx - 1) {
+                    const double kh = g.kh_r[y];
+#pragma unroll
+                    for (int bp = 0; bp < B; ++bp) O[1][bp] = cadd(O[1][bp], mik(kh, T[bp]));
+                }
+#pragma unroll
+                for (int al = 0; al < B; ++al) {
+                    if (nzS(al, cl)) {
+#pragma unroll
+                        for (int bp = 0; bp < B; ++bp) O[al][bp] = rfma(c_S[SL][al][cl], T[bp], O[al][bp]);
+                    }
+                    if (nzM(al, cl)) {
+#pragma unroll
+                        for (int bp = 0; bp < B; ++bp) O[al][bp] = rfma(c_M[SL][al][cl], Wv[bp], O[al][bp]);
+                    }
+                }
+            }
+            // horizontal Robin edges: 1-D mass along x of the bottom / top node rows
+            if (y == 0 || y == ny - 1) {
+#pragma unroll
+                for (int side = 0; side < 2; ++side) {
+                    if (side == 0 ? y != 0 : y != ny - 1) continue;
+                    const double kh = side == 0 ? g.kh_b[ux] : g.kh_t[ux];
+                    double2 zr[B];
+#pragma unroll
+                    for (int cl = 0; cl < B; ++cl) zr[cl] = zval(cl, side);
+#pragma unroll
+                    for (int al = 0; al < B; ++al) {
+                        double2 s = zero;
+#pragma unroll
+                        for (int cl = 0; cl < B; ++cl)
+                            if (nzM(al, cl)) s = rfma(c_M[SL][al][cl], zr[cl], s);
+                        O[al][side] = cadd(O[al][side], mik(kh, s));
+                    }
+                }
+            }
+        }
+        // carried top row of the cell row below (al != 1: the right column went to the neighbour)
+#pragma unroll
+        for (int al = 0; al < B; ++al)
+            if (al != 1) O[al][0] = cadd(O[al][0], carry[al]);
+        // right column -> right neighbour
+        double2 (*Xb)[B] = sm.X[(y - ystart) & 1];
+        if (active)
+#pragma unroll
+            for (int bp = 0; bp < B; ++bp) Xb[tid][bp] = O[1][bp];
+        __syncthreads();
+        if (active && tid > 0)
+#pragma unroll
+            for (int bp = 0; bp < B; ++bp) O[0][bp] = cadd(O[0][bp], Xb[tid - 1][bp]);
+#pragma unroll
+        for (int al = 0; al < B; ++al) carry[al] = al == 1 ? zero : O[al][1];
+
+        if (y >= yres0) {
+            double2* Fs = fslot(y);
+            // residual at own nodes (a, b != 1) overwrites O; Dirichlet rows: r = f - u, restricted as 0
+            if (resid) {
+#pragma unroll
+                for (int al = 0; al < B; ++al) {
+                    if (al == 1 || (!cell && al != 0)) continue;
+#pragma unroll
+                    for (int bp = 0; bp < B; ++bp) {
+                        if (bp == 1) continue;
+                        const int pos = cell ? upos<P>(al, bp) : (bp == 0 ? 0 : bp - 1);
+                        double2 Av = O[al][bp];
+                        const bool dir = g.has_dirichlet && fine_dir<P>(g, lidx<P>(ux, al), lidx<P>(y, bp));
+                        if (dir) Av = Uy[tid * SU + pos];
+                        const double2 rv = csub(Fs[tid * SU + pos], Av);
+                        if (MODE == kK1Write) Fs[tid * SU + pos] = rv;
+                        if (MODE == kK1Norm && y >= ys && owned) acc += rv.x * rv.x + rv.y * rv.y;
+                        O[al][bp] = dir ? zero : rv;
+                    }
+                }
+            }
+            if (MODE == kK1Write) {
+                __syncthreads();
+                if (y >= ys) store_row(y);
+            }
+            if (MODE == kK1Norm && g.has_dirichlet) __syncthreads();  // Dirichlet reads of u(y) vs its re-fill
+            if (MODE == kK1Restrict) {
+                double2 pt[MM + 1][MM + 1];  // partials at coarse nodes (jx, jy) of this cell
+#pragma unroll
+                for (int jx = 0; jx <= MM; ++jx)
+#pragma unroll
+                    for (int jy = 0; jy <= MM; ++jy) pt[jx][jy] = zero;
+                if (resid) {
+#pragma unroll
+                    for (int al = 0; al < B; ++al) {
+                        if (al == 1 || (!cell && al != 0)) continue;
+                        double2 q[MM + 1];
+#pragma unroll
+                        for (int jy = 0; jy <= MM; ++jy) {
+                            q[jy] = zero;
+#pragma unroll
+                            for (int bp = 0; bp < B; ++bp)
+                                if (bp == 0 || (bp >= 2 && bp <= MM)) q[jy] = rfma(wgt(bp, jy), O[al][bp], q[jy]);
+                        }
+#pragma unroll
+                        for (int jx = 0; jx <= MM; ++jx) {
+                            if (al != 0 && al > MM) continue;
+                            const double w = wgt(al, jx);
+#pragma unroll
+                            for (int jy = 0; jy <= MM; ++jy) pt[jx][jy] = rfma(w, q[jy], pt[jx][jy]);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int jx = 0; jx < MM; ++jx) pt[jx][0] = cadd(pt[jx][0], pcarry[jx]);
+                // XP reads of row y - 1 precede this row's exchange barrier
+                double2 (*Xp)[MM + 1] = sm.XP;
+                if (active)
+#pragma unroll
+                    for (int jy = 0; jy <= MM; ++jy) Xp[tid][jy] = pt[MM][jy];
+                __syncthreads();
+                if (active && tid > 0)
+#pragma unroll
+                    for (int jy = 0; jy <= MM; ++jy) pt[0][jy] = cadd(pt[0][jy], Xp[tid - 1][jy]);
+#pragma unroll
+                for (int jx = 0; jx <= MM; ++jx) pcarry[jx] = jx == MM ? zero : pt[jx][MM];
+                if (owned && y >= ys) {
+#pragma unroll
+                    for (int jx = 0; jx < MM; ++jx) {
+                        if (!cell && jx > 0) continue;
+#pragma unroll
+                        for (int jy = 0; jy < MM; ++jy) write_rc(ux * MM + jx, y * MM + jy, pt[jx][jy]);
+                    }
+                }
+            }
+        }
+    }
+
+    // top lattice row: vertex / horizontal-edge dofs of the units (x, ny), carried in `carry`
+    if (top) {
+        cp_wait<0>();
+        __syncthreads();
+        double2* Fs = fslot(ny);
+        const double2* Ut = uslot(ny);
+        double2 Rt[B];
+#pragma unroll
+        for (int al = 0; al < B; ++al) Rt[al] = zero;
+        if (resid) {
+#pragma unroll
+            for (int al = 0; al < B; ++al) {
+                if (al == 1 || (!cell && al != 0)) continue;
+                const int pos = al == 0 ? 0 : al - 1;
+                double2 Av = carry[al];
+                const bool dir = g.has_dirichlet && fine_dir<P>(g, lidx<P>(ux, al), ny * P);
+                if (dir) Av = Ut[tid * SU + pos];
+                const double2 rv = csub(Fs[tid * SU + pos], Av);
+                if (MODE == kK1Write) Fs[tid * SU + pos] = rv;
+                if (MODE == kK1Norm && owned) acc += rv.x * rv.x + rv.y * rv.y;
+                Rt[al] = dir ? zero : rv;
+            }
+        }
+        if (MODE == kK1Write) {
+            __syncthreads();
+            store_row(ny);
+        }
+        if (MODE == kK1Restrict) {
+            double2 pt[MM + 1];
+#pragma unroll
+            for (int jx = 0; jx <= MM; ++jx) {
+                pt[jx] = jx < MM ? pcarry[jx] : zero;
+#pragma unroll
+                for (int al = 0; al < B; ++al) {
+                    if (al == 1 || (al != 0 && al > MM)) continue;
+                    pt[jx] = rfma(wgt(al, jx), Rt[al], pt[jx]);
+                }
+            }
+            __syncthreads();  // both exchange buffers may still be read by a neighbour
+            if (active) sm.X[0][tid][0] = pt[MM];
+            __syncthreads();
+            if (active && tid > 0) pt[0] = cadd(pt[0], sm.X[0][tid - 1][0]);
+            if (owned)
+#pragma unroll
+                for (int jx = 0; jx < MM; ++jx)
+                    if (cell || jx == 0) write_rc(ux * MM + jx, ny * MM, pt[jx]);
+        }
+    }
+    if (MODE == kK1Norm) {  // fixed-order block sum (the last warp is partial)
+        sm.red[tid] = acc;
+        __syncthreads();
+        if (tid == 0) {
+            double sacc = 0.0;
+            for (int w = 0; w < NT; ++w) sacc += sm.red[w];
+            a.partial[blockIdx.y * gridDim.x + blockIdx.x] = sacc;
         }
     }
 }
@@ -529,22 +894,51 @@ static int k1_gx(const FineGeom& g) {
     }
 }
 
-static int k1_rows(const FineGeom& g, int rows) {
-    if (rows > 0) return rows;
-    const long long strips = k1_gx(g);
-    long long r = (g.ny * strips + 295) / 296;  // about two CTAs per SM
-    return int(std::max<long long>(4, std::min<long long>(r, g.ny)));
+// row blocks per strip: fill one wave of resident CTAs (kK1CtasPerSM per SM),
+// at least 4 lattice rows per block (a block re-reads one halo row of u)
+constexpr int kK1CtasPerSM = 3;
+static int k1_row_blocks(const FineGeom& g, int rows) {
+    if (rows > 0) return (g.ny + rows - 1) / rows;
+    static int nsm = 0;
+    if (!nsm) HTG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
+    const int strips = k1_gx(g);
+    const int nb = std::max(1, nsm * kK1CtasPerSM / strips);
+    return std::max(1, std::min(nb, g.ny / 4));
+}
+
+// cell-per-thread kernel (p <= 4): one CTA per SM, strips of at most KCCfg::C cells
+template <int P>
+static int kc_strips(int nx) { return (nx + KCCfg<P>::C - 1) / KCCfg<P>::C; }
+static int kc_gx(const FineGeom& g) { return g.p == 2 ? kc_strips<2>(g.nx) : kc_strips<4>(g.nx); }
+static int kc_row_blocks(const FineGeom& g, int rows) {
+    if (rows > 0) return (g.ny + rows - 1) / rows;
+    static int nsm = 0;
+    if (!nsm) HTG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
+    return std::max(1, std::min(nsm / kc_gx(g), g.ny / 2));
 }
 
 int k1_partials(const FineGeom& g, int rows) {
-    const int r = k1_rows(g, rows);
-    return k1_gx(g) * ((g.ny + r - 1) / r);
+    if (g.p <= 4) return kc_gx(g) * kc_row_blocks(g, rows);
+    return k1_gx(g) * k1_row_blocks(g, rows);
+}
+
+template <int P, int MODE>
+static void kc_launch_t(K1Args a, cudaStream_t st) {
+    dim3 grid(kc_strips<P>(a.g.nx), kc_row_blocks(a.g, a.rows));
+    const size_t smem = sizeof(KCSmem<P>);
+    static bool attr = false;
+    if (!attr) {
+        HTG_CUDA(cudaFuncSetAttribute(k1_cells<P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        attr = true;
+    }
+    k1_cells<P, MODE><<<grid, kKCThreads, smem, st>>>(a);
+    HTG_CUDA(cudaGetLastError());
+    count_launch();
 }
 
 template <int P, int MODE>
 static void k1_launch_t(K1Args a, cudaStream_t st) {
-    a.rows = k1_rows(a.g, a.rows);
-    dim3 grid(k1_grid_x<P>(a.g.nx), (a.g.ny + a.rows - 1) / a.rows);
+    dim3 grid(k1_grid_x<P>(a.g.nx), k1_row_blocks(a.g, a.rows));
     const size_t smem = sizeof(K1Smem<P>);
     static bool attr = false;
     if (!attr) {
@@ -558,9 +952,15 @@ static void k1_launch_t(K1Args a, cudaStream_t st) {
 
 template <int P>
 static void k1_mode(int mode, const K1Args& a, cudaStream_t st) {
-    if (mode == kK1Write) k1_launch_t<P, kK1Write>(a, st);
-    else if (mode == kK1Norm) k1_launch_t<P, kK1Norm>(a, st);
-    else k1_launch_t<P, kK1Restrict>(a, st);
+    if constexpr (P <= 4) {
+        if (mode == kK1Write) kc_launch_t<P, kK1Write>(a, st);
+        else if (mode == kK1Norm) kc_launch_t<P, kK1Norm>(a, st);
+        else kc_launch_t<P, kK1Restrict>(a, st);
+    } else {
+        if (mode == kK1Write) k1_launch_t<P, kK1Write>(a, st);
+        else if (mode == kK1Norm) k1_launch_t<P, kK1Norm>(a, st);
+        else k1_launch_t<P, kK1Restrict>(a, st);
+    }
 }
 
 int k1_launch(int mode, const K1Args& a, cudaStream_t st) {
