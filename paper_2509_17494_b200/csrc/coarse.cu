@@ -95,6 +95,33 @@ __device__ __forceinline__ void rows_dot(const double2* __restrict__ M, int len,
     }
 }
 
+// Warp tier (small fronts): blocks are stored column-major, one lane group per
+// row: lanes (i, part) with i = lane % R accumulate the k = part (mod S) terms
+// of row i, S = 32 / R parts combined with S - 1 shuffles. Column reads are
+// coalesced and there is no per-row reduction tree (short rows).
+template <class Out>
+__device__ __forceinline__ void cols_dot(const double2* __restrict__ M, int rows, int len, const double2* v, int lane,
+                                         Out&& out) {
+    int R = 32;
+    if (rows <= 4) R = 4;
+    else if (rows <= 8) R = 8;
+    else if (rows <= 16) R = 16;
+    const int S = 32 / R, i0 = lane % R, part = lane / R;
+    for (int rb = 0; rb < rows; rb += R) {
+        const int i = rb + i0;
+        double2 acc = make_double2(0.0, 0.0);
+        if (i < rows) {
+#pragma unroll 4
+            for (int k = part; k < len; k += S) acc = cfma(M[(size_t)k * rows + i], v[k], acc);
+        }
+        for (int o = R; o < 32; o <<= 1) {
+            acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+            acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+        }
+        if (part == 0 && i < rows) out(i, acc);
+    }
+}
+
 // front vector v = [rc(vars); 0] + the children's contribution vectors (each
 // position has at most two, added in child order), one pass, no barrier inside
 template <int STRIDE, class Sync>
@@ -128,12 +155,12 @@ __global__ void __launch_bounds__(kCT) k_nd_fwd_warp(const NodeDev* __restrict__
     double2* v = sv[w];
     double2* y = sy[w];
     gather_front<32>(a, nd, v, lane, [] { __syncwarp(); });
-    rows_dot(a.fac + nd.off_F, nd.s, v, 0, nd.s, 0, 1, lane, [&](int r, double2 acc) {
+    cols_dot(a.fac + nd.off_F, nd.s, nd.s, v, lane, [&](int r, double2 acc) {
         y[r] = acc;
         a.Y[a.idx[nd.off_var + r]] = acc;
     });
     __syncwarp();
-    rows_dot(a.fac + nd.off_L, nd.s, y, 0, nd.u, 0, 1, lane, [&](int r, double2 acc) {
+    cols_dot(a.fac + nd.off_L, nd.u, nd.s, y, lane, [&](int r, double2 acc) {
         const double2 v2 = v[nd.s + r];
         a.contrib[nd.off_contrib + r] = make_double2(v2.x - acc.x, v2.y - acc.y);
     });
@@ -215,7 +242,19 @@ __global__ void __launch_bounds__(kCT) k_nd_bwd_warp(const NodeDev* __restrict__
     for (int i = lane; i < nd.s; i += 32) v[i] = a.Y[a.idx[nd.off_var + i]];
     for (int i = lane; i < nd.u; i += 32) v[nd.s + i] = a.X[a.idx[nd.off_ring + i]];
     __syncwarp();
-    bwd_rows(a, nd, v, v + nd.s, sz[w], 0, nd.s, 0, 1, lane, sync_warp_fn);
+    // x1 = U^-1 y1 - Z x2 (column-major blocks)
+    double2* z = sz[w];
+    if (nd.u > 0) {
+        cols_dot(a.fac + nd.off_Z, nd.s, nd.u, v + nd.s, lane, [&](int r, double2 acc) { z[r] = acc; });
+        __syncwarp();
+    }
+    cols_dot(a.fac + nd.off_U, nd.s, nd.s, v, lane, [&](int r, double2 acc) {
+        if (nd.u > 0) {
+            acc.x -= z[r].x;
+            acc.y -= z[r].y;
+        }
+        a.X[a.idx[nd.off_var + r]] = acc;
+    });
 }
 
 // backward, CTA tasks (whole front for the CTA tier, row blocks for the large tier)
@@ -362,6 +401,7 @@ class NDSolver : public CoarseSolver {
             }
             for (int k = 0; k < n.F; ++k) rpos[n.rows[k]] = -1;
         }
+        const int warpF = std::min(kWarpFMax, env_int("HTG_ND_WARPF", 64));
         void* facp = nullptr;
         HTG_CUDA(cudaMalloc(&facp, std::max<long long>(1, fac_total) * sizeof(double2)));
         allocs_.push_back(facp);
@@ -375,6 +415,18 @@ class NDSolver : public CoarseSolver {
                                     cudaMemcpyHostToDevice));
                 std::vector<cplx>().swap(v);
             };
+            if (d.s + d.u <= warpF) {  // warp tier: column-major blocks (cols_dot)
+                auto tr = [](std::vector<cplx>& M, int rows, int cols) {
+                    std::vector<cplx> T(M.size());
+                    for (int i = 0; i < rows; ++i)
+                        for (int k = 0; k < cols; ++k) T[size_t(k) * rows + i] = M[size_t(i) * cols + k];
+                    M.swap(T);
+                };
+                tr(n.Finv, d.s, d.s);
+                tr(n.L21, d.u, d.s);
+                tr(n.Uinv, d.s, d.s);
+                tr(n.Z, d.s, d.u);
+            }
             put(n.Finv, d.off_F);
             put(n.L21, d.off_L);
             put(n.Uinv, d.off_U);
@@ -392,7 +444,6 @@ class NDSolver : public CoarseSolver {
         std::vector<std::vector<NodeDev>> wp(D), md(D);
         std::vector<std::vector<Task>> f1(D), f2(D), bw(D);
         size_t max_smem = 0;
-        const int warpF = std::min(kWarpFMax, env_int("HTG_ND_WARPF", 64));
         const long long midData = env_int("HTG_ND_MIDDATA", 16384);
         for (int i = 0; i < nn; ++i) {
             const int dep = t.nodes[i].depth;

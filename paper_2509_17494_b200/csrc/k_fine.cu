@@ -10,10 +10,13 @@
 // A CTA owns a strip of cells in x and marches upward over cell rows; the
 // top-edge (b = 1) contributions of a cell row are carried in registers into
 // the next lattice row, so every u and f value is read once from HBM.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <atomic>
+#include <string>
 
 #include "common.hpp"
 #include "kernels.hpp"
@@ -504,59 +507,87 @@ __global__ void __launch_bounds__(kK1Threads) k1_residual(K1Args a) {
 
 
 // ---------------------------------------------------------------- K1, one thread per cell (p <= 4)
-// Each thread owns one unit cell (its p^2 dofs: bottom-left vertex, bottom and
-// left edge bubbles, interior) and keeps the whole element contraction in
-// registers: per local column cl the y contraction T = M z, V = S z, W = V - m T,
-// then O[al][.] += S[al][cl] T + M[al][cl] W. Shared nodes are completed by
-// (a) handing the right column O[1][.] to the right neighbour (shared memory
-// exchange) and (b) carrying the top row O[.][1] in registers to the next cell
-// row of the same thread. u / f row segments are staged with cp.async into a
-// shared-memory layout padded to an odd unit stride (p^2 + 1 entries), so the
-// per-thread unit reads are bank-conflict free while the global loads and the
-// r stores stay fully coalesced.
-constexpr int kKCThreads = 120;
+// Each cell of a strip is owned by one lane in each of two warp groups; the
+// element contraction is kept in registers: per local column cl the y
+// contraction T = M z, V = S z, W = V - m T, then O[al][.] += S[al][cl] T +
+// M[al][cl] W. Group 0 computes the output node rows bp in {0, 1} of the cell,
+// group 1 the rows 2..p (warp-uniform split, no divergence, two resident warps
+// per scheduler). Shared nodes are completed by (a) handing the right column
+// O[1][.] to the right neighbour (shared-memory exchange) and (b) carrying the
+// top row O[.][1] in group-0 registers to the next cell row.
+//
+// Data movement: a lattice row's unit cells are one contiguous byte range in
+// the reference layout, and row starts are 16-byte aligned, so u / f rows are
+// TMA tensor loads of a 3-D map [row][sub-row][16-byte chunk] (sub-rows of 128
+// bytes for p = 4, 64 bytes for p = 2) with the matching shared-memory
+// swizzle: one instruction per row, and the per-lane unit reads hit distinct
+// banks (p = 2) or two-way (p = 4). The x = nx column unit (p dofs) and the top
+// lattice row (p dofs per unit) are 1-D bulk copies; r is written back from
+// shared memory with coalesced stores.
+constexpr int kKCCells = 120;                        // cell slots per CTA (lanes per warp group)
+constexpr int kKCGroupWarps = (kKCCells + 31) / 32;  // warps per group
+constexpr int kKCThreads = 2 * 32 * kKCGroupWarps;   // two warp groups
 
 template <int P>
 struct KCCfg {
-    static constexpr int B = P + 1, MM = P / 2, UD = P * P, SU = P * P + 1;
-    static constexpr int H = 2;                     // halo cells on the left (restrict mode needs 2)
-    static constexpr int C = kKCThreads - H - 1;    // owned cells per strip (one thread left for x = nx)
-    static constexpr int NU = kKCThreads + 1;       // staged units per row: threads + right neighbour
-    static constexpr int NF = 3;                    // f slots (a slot is re-filled two rows after its r store)
+    static constexpr int B = P + 1, MM = P / 2;
+    static constexpr int H = 2;                  // halo cells on the left (restrict mode needs 2)
+    static constexpr int C = kKCCells - H - 1;   // owned cells per strip (one slot left for x = nx)
+    static constexpr int NU = kKCCells + 1;      // staged units per row: cells + right neighbour
+    static constexpr int NR = B - 2 > 2 ? B - 2 : 2;  // most node rows of one group
+    static constexpr int UB = P * P * 16;             // unit bytes
+    static constexpr int RB = UB < 128 ? UB : 128;    // tensor-map sub-row bytes (= swizzle span)
+    static constexpr int RPU = UB / RB;               // sub-rows per unit
+    static constexpr int CPR = RB / 16;               // 16-byte chunks per sub-row
+    static constexpr int BOX = NU * UB;               // bytes of one row box
+    static constexpr int SLOT = (BOX + P * 16 + 1023) / 1024 * 1024;  // box + the x = nx unit, 1 KB aligned
 };
 
 template <int P>
-struct KCSmem {
+struct __align__(1024) KCSmem {
     using C = KCCfg<P>;
-    double2 U[3][C::NU * C::SU];
-    double2 F[C::NF][C::NU * C::SU];
-    double2 X[2][kKCThreads][C::B];     // right-column exchange, double-buffered by row parity
-    double2 XP[kKCThreads][C::MM + 1];  // restriction partials exchange
+    double2 U[3][C::SLOT / 16];
+    double2 F[3][C::SLOT / 16];
+    double2 X[2][2][kKCCells][C::NR];    // right-column exchange [row parity][group]
+    double2 XP[kKCCells][C::MM + 1];     // restriction partials exchange
     double red[kKCThreads];
+    unsigned long long barU[3], barF[3];
 };
 
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+// double2 index of element k of staged unit u (rows below the top): the
+// tensor-map box layout with its 16-byte-chunk swizzle (128B: chunk ^= sub-row
+// & 7; 64B: chunk ^= (sub-row >> 1) & 3)
+template <int P>
+__device__ __forceinline__ int kc_idx(int u, int k) {
+    using C = KCCfg<P>;
+    const int r = u * C::RPU + k / C::CPR, c = k % C::CPR;
+    const int sw = C::RB == 128 ? (r & 7) : ((r >> 1) & 3);
+    return r * C::CPR + (c ^ sw);
 }
 
-// position of local node (a, b) of unit cell row y < ny inside its unit (a, b != 1)
+// position of local node (a, b) of a unit cell of row y < ny inside its unit (a, b != 1)
 template <int P>
 __device__ __forceinline__ constexpr int upos(int a, int b) {
     return a == 0 ? (b == 0 ? 0 : P + b - 2) : (b == 0 ? a - 1 : 2 * P - 1 + (a - 2) * (P - 1) + (b - 2));
 }
 
-template <int P, int MODE>
-__global__ void __launch_bounds__(kKCThreads, 1) k1_cells(K1Args a) {
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];\n" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <int P, int MODE, int GRP, bool DIR>
+__device__ __forceinline__ void k1c_body(const K1Args& a, const CUtensorMap* tmu, const CUtensorMap* tmf,
+                                         KCSmem<P>& sm, int ct) {
     using Cf = KCCfg<P>;
-    constexpr int B = Cf::B, MM = Cf::MM, SU = Cf::SU, NT = kKCThreads;
+    constexpr int B = Cf::B, MM = Cf::MM, NT = kKCThreads;
+    constexpr int R0 = GRP == 0 ? 0 : 2, R1 = GRP == 0 ? 2 : B, NRG = R1 - R0;  // node rows of this group
     constexpr int SL = P / 2 - 1;  // basis table slot
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    KCSmem<P>& sm = *reinterpret_cast<KCSmem<P>*>(smem_raw);
+    constexpr int EDGE = Cf::BOX / 16;  // double2 offset of the x = nx unit inside a slot
     const FineGeom& g = a.g;
     const int tid = threadIdx.x, nx = g.nx, ny = g.ny;
     const double2 zero = make_double2(0.0, 0.0);
@@ -567,9 +598,10 @@ __global__ void __launch_bounds__(kKCThreads, 1) k1_cells(K1Args a) {
     const int xa = max(x0 - H, 0);
     const int xlast = xe == nx ? nx : xe - 1;  // last unit with outputs (x = nx: right boundary column)
     const int xb = xe;                          // last staged unit (right neighbour of the last cell)
-    const int ux = xa + tid;
+    const int ux = xa + ct;
     const bool active = ux <= xlast;
     const bool cell = active && ux < nx;
+    const bool edge = active && ux == nx;      // the x = nx column unit (p dofs, staged apart)
     const bool owned = active && ux >= x0;
     const bool resid = owned || (MODE == kK1Restrict && active && ux == x0 - 1);
     const int ys = int((long long)blockIdx.y * ny / gridDim.y), ye = int((long long)(blockIdx.y + 1) * ny / gridDim.y);
@@ -579,83 +611,114 @@ __global__ void __launch_bounds__(kKCThreads, 1) k1_cells(K1Args a) {
     const bool top = ye == ny;
     const double2* mt = a.shifted ? g.mtabS : g.mtab0;
 
-    // Row staging: coalesced 16-byte cp.async chunks into the padded unit layout.
-    auto stage = [&](double2* dst, const double2* src, int yy) {
-        const long long lo = unit_off<P>(nx, ny, xa, yy);
-        const int n = int(unit_off<P>(nx, ny, xb, yy) + unit_size<P>(nx, ny, xb, yy) - lo);
-        const int usz = yy < ny ? P * P : P;
-        for (int e = tid; e < n; e += NT) {
-            const int uu = e / usz;
-            cp_async16(dst + uu * SU + (e - uu * usz), src + lo + e);
+    auto uslot = [&](int yy) { return sm.U[(yy - ystart) % 3]; };
+    auto fslot = [&](int yy) { return sm.F[(yy - yres0) % 3]; };
+    auto ubar = [&](int yy) { return &sm.barU[(yy - ystart) % 3]; };
+    auto fbar = [&](int yy) { return &sm.barF[(yy - yres0) % 3]; };
+    // the k-th use of a slot completes its barrier's phase k
+    auto wait_u = [&](int yy) { mbar_wait(ubar(yy), unsigned(((yy - ystart) / 3) & 1)); };
+    auto wait_f = [&](int yy) { mbar_wait(fbar(yy), unsigned(((yy - yres0) / 3) & 1)); };
+    // thread 0: stage row yy of u or f (rows < ny: tensor box + the x = nx unit; top row: linear)
+    auto stage = [&](double2* dst, const double2* src, const CUtensorMap* map, int yy, unsigned long long* bar) {
+        fence_async_smem();  // generic accesses to the slot precede the async-proxy writes
+        if (yy < ny) {
+            const bool with_edge = xb == nx;
+            mbar_expect_tx(bar, unsigned(Cf::BOX + (with_edge ? P * 16 : 0)));
+            tma_load_3d(dst, map, 0, xa * Cf::RPU, yy, bar);
+            if (with_edge) tma_load_1d(dst + EDGE, src + unit_off<P>(nx, ny, nx, yy), P * 16, bar);
+        } else {
+            const long long lo = unit_off<P>(nx, ny, xa, ny);
+            const unsigned bytes = unsigned((unit_off<P>(nx, ny, xb, ny) + unit_size<P>(nx, ny, xb, ny) - lo) * 16);
+            mbar_expect_tx(bar, bytes);
+            tma_load_1d(dst, src + lo, bytes, bar);
         }
     };
-    auto uslot = [&](int yy) { return sm.U[(yy - ystart) % 3]; };
-    auto fslot = [&](int yy) { return sm.F[(yy - yres0) % Cf::NF]; };
-    // prologue: u rows ystart, ystart + 1 and f row ystart
-    stage(uslot(ystart), a.u, ystart);
-    if (ystart + 1 <= ye) stage(uslot(ystart + 1), a.u, ystart + 1);
-    if (ystart >= yres0) stage(fslot(ystart), a.f, ystart);
-    cp_commit();
+    if (tid == 0) {
+        for (int i = 0; i < 3; ++i) {
+            mbar_init(&sm.barU[i], 1);
+            mbar_init(&sm.barF[i], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {
+        stage(uslot(ystart), a.u, tmu, ystart, ubar(ystart));
+        if (ystart + 1 <= ye) stage(uslot(ystart + 1), a.u, tmu, ystart + 1, ubar(ystart + 1));
+        if (ystart >= yres0) stage(fslot(ystart), a.f, tmf, ystart, fbar(ystart));
+    }
 
-    double2 carry[B];  // O[al][1] of the previous cell row (al != 1)
+    double2 carry[B];  // group 0: O[al][1] of the previous cell row (al != 1)
 #pragma unroll
     for (int i = 0; i < B; ++i) carry[i] = zero;
-    double2 pcarry[MM + 1];  // restriction partials of the previous row, coarse row y*m
+    double2 pcarry[MM + 1];  // group 0: restriction partials of the previous row, coarse row y*m
 #pragma unroll
     for (int i = 0; i <= MM; ++i) pcarry[i] = zero;
     double acc = 0.0;
 
-    // copy the owned range of r row yy (written in place into its f slot) to global, coalesced
+    // copy the owned range of r row yy < ny (written in place into its f slot) to global, coalesced
     auto store_row = [&](int yy) {
         const double2* src = fslot(yy);
+        const int xl = min(xlast, nx - 1);
         const long long lo = unit_off<P>(nx, ny, x0, yy);
-        const int n = int(unit_off<P>(nx, ny, xlast, yy) + unit_size<P>(nx, ny, xlast, yy) - lo);
-        const int usz = yy < ny ? P * P : P;
+        const int n = (xl - x0 + 1) * P * P;
+        double2* dst = a.r + lo;
         const int ush = x0 - xa;
-        for (int e = tid; e < n; e += NT) {
-            const int uu = e / usz;
-            a.r[lo + e] = src[(uu + ush) * SU + (e - uu * usz)];
-        }
+        for (int e = tid; e < n; e += NT) dst[e] = src[kc_idx<P>(e / (P * P) + ush, e % (P * P))];
+        if (xlast == nx && tid < P) dst[n + tid] = src[EDGE + tid];
+    };
+    auto store_top = [&]() {
+        const double2* src = fslot(ny);
+        const long long lo = unit_off<P>(nx, ny, x0, ny);
+        const int n = int(unit_off<P>(nx, ny, xlast, ny) + unit_size<P>(nx, ny, xlast, ny) - lo);
+        const int sh = (x0 - xa) * P;
+        for (int e = tid; e < n; e += NT) a.r[lo + e] = src[sh + e];
     };
     // coarse restriction weights: wgt(d, j) for local node index d (0: vertex at j = 0)
     auto wgt = [&](int d, int j) -> double { return d == 0 ? (j == 0 ? 1.0 : 0.0) : c_E[SL][d][j]; };
     const int CXn = nx * MM + 1;
     auto write_rc = [&](int X, int Y, double2 v) {
-        if (g.has_dirichlet && coarse_dir(g, MM, X, Y)) v = zero;
+        if (DIR && coarse_dir(g, MM, X, Y)) v = zero;
         a.rc[(size_t)Y * CXn + X] = v;
     };
+    // element index of own node (al, bp) in a row < ny slot (the x = nx unit: its edge copy)
+    auto own_idx = [&](int al, int bp) { return edge ? EDGE + (bp == 0 ? 0 : bp - 1) : kc_idx<P>(ct, upos<P>(al, bp)); };
 
     for (int y = ystart; y < ye; ++y) {
-        // Prefetch u(y + 2) into the slot of u(y - 1) and f(y + 1) into the slot of
-        // f(y - 2). Every read of u(y - 1) precedes the last barrier of row y - 1
-        // (compute: exchange barrier; Dirichlet reads: store / partials barrier, or
-        // the extra barrier below), and every read of f(y - 2) precedes the staging
-        // barrier of row y - 1.
-        if (y + 2 <= ye) stage(uslot(y + 2), a.u, y + 2);
-        if (y + 1 >= yres0 && (y + 1 < ye || (top && y + 1 == ny))) stage(fslot(y + 1), a.f, y + 1);
-        cp_commit();
-        cp_wait<1>();
-        __syncthreads();
+        // Thread 0 prefetches u(y + 2) into the slot of u(y - 1) and f(y + 1) into
+        // the slot of f(y - 2). Every read of u(y - 1) precedes the last barrier of
+        // row y - 1 (compute: exchange barrier; Dirichlet reads: store / partials
+        // barrier, or the extra barrier below), and every read of f(y - 2) precedes
+        // the exchange barrier of row y - 1.
+        if (tid == 0) {
+            if (y + 2 <= ye) stage(uslot(y + 2), a.u, tmu, y + 2, ubar(y + 2));
+            if (y + 1 >= yres0 && (y + 1 < ye || (top && y + 1 == ny))) stage(fslot(y + 1), a.f, tmf, y + 1, fbar(y + 1));
+        }
+        wait_u(y);
+        wait_u(y + 1);
+        if (y >= yres0) wait_f(y);
         const double2* Uy = uslot(y);
         const double2* Uy1 = uslot(y + 1);
-        const double2* own = Uy + tid * SU;
-        const double2* rn = Uy + (tid + 1) * SU;
-        const double2* tp = Uy1 + tid * SU;
-        const double2* tpr = Uy1 + (tid + 1) * SU;
-        const bool rn_edge = ux + 1 == nx;  // right neighbour is the x = nx column unit (p dofs)
+        const bool toprow = y + 1 == ny;      // the row above is the linear top row
+        const bool rn_edge = ux + 1 == nx;    // right neighbour is the x = nx column unit
         auto zval = [&](int cl, int b) -> double2 {
             double2 v;
-            if (cl == 1) v = b == 0 ? rn[0] : (b == 1 ? tpr[0] : rn[rn_edge ? b - 1 : P + b - 2]);
-            else if (b == 1) v = tp[cl == 0 ? 0 : cl - 1];
-            else v = own[upos<P>(cl, b)];
-            if (g.has_dirichlet && fine_dir<P>(g, lidx<P>(ux, cl), lidx<P>(y, b))) v = zero;
+            if (b == 1) {
+                const int k = cl == 0 ? 0 : (cl == 1 ? P : cl - 1);  // top-row index relative to the unit
+                v = toprow ? Uy1[ct * P + k] : (cl == 1 ? (rn_edge ? Uy1[EDGE] : Uy1[kc_idx<P>(ct + 1, 0)])
+                                                        : Uy1[kc_idx<P>(ct, k)]);
+            } else if (cl == 1) {
+                v = rn_edge ? Uy[EDGE + (b == 0 ? 0 : b - 1)] : Uy[kc_idx<P>(ct + 1, upos<P>(0, b))];
+            } else {
+                v = Uy[kc_idx<P>(ct, upos<P>(cl, b))];
+            }
+            if (DIR && fine_dir<P>(g, lidx<P>(ux, cl), lidx<P>(y, b))) v = zero;
             return v;
         };
-        double2 O[B][B];
+        double2 O[B][NRG];  // output node rows R0..R1-1
 #pragma unroll
         for (int i = 0; i < B; ++i)
 #pragma unroll
-            for (int j = 0; j < B; ++j) O[i][j] = zero;
+            for (int j = 0; j < NRG; ++j) O[i][j] = zero;
         if (cell) {
             const double2 m = mt[g.cls ? g.cls[(size_t)y * nx + ux] : 0];
 #pragma unroll
@@ -663,42 +726,43 @@ __global__ void __launch_bounds__(kKCThreads, 1) k1_cells(K1Args a) {
                 double2 zc[B];
 #pragma unroll
                 for (int b = 0; b < B; ++b) zc[b] = zval(cl, b);
-                double2 T[B], Wv[B];
+                double2 T[NRG], Wv[NRG];
 #pragma unroll
-                for (int bp = 0; bp < B; ++bp) {
+                for (int j = 0; j < NRG; ++j) {
+                    const int bp = R0 + j;
                     double2 t = zero, v = zero;
 #pragma unroll
                     for (int b = 0; b < B; ++b) {
                         if (nzM(bp, b)) t = rfma(c_M[SL][bp][b], zc[b], t);
                         if (nzS(bp, b)) v = rfma(c_S[SL][bp][b], zc[b], v);
                     }
-                    T[bp] = t;
-                    Wv[bp] = csub(v, cmul(m, t));
+                    T[j] = t;
+                    Wv[j] = make_double2(fma(-m.x, t.x, fma(m.y, t.y, v.x)), fma(-m.x, t.y, fma(-m.y, t.x, v.y)));
                 }
                 if (cl == 0 && ux == 0) {
                     const double kh = g.kh_l[y];
 #pragma unroll
-                    for (int bp = 0; bp < B; ++bp) O[0][bp] = cadd(O[0][bp], mik(kh, T[bp]));
+                    for (int j = 0; j < NRG; ++j) O[0][j] = cadd(O[0][j], mik(kh, T[j]));
                 }
                 if (cl == 1 && ux == nx - 1) {
                     const double kh = g.kh_r[y];
 #pragma unroll
-                    for (int bp = 0; bp < B; ++bp) O[1][bp] = cadd(O[1][bp], mik(kh, T[bp]));
+                    for (int j = 0; j < NRG; ++j) O[1][j] = cadd(O[1][j], mik(kh, T[j]));
                 }
 #pragma unroll
                 for (int al = 0; al < B; ++al) {
                     if (nzS(al, cl)) {
 #pragma unroll
-                        for (int bp = 0; bp < B; ++bp) O[al][bp] = rfma(c_S[SL][al][cl], T[bp], O[al][bp]);
+                        for (int j = 0; j < NRG; ++j) O[al][j] = rfma(c_S[SL][al][cl], T[j], O[al][j]);
                     }
                     if (nzM(al, cl)) {
 #pragma unroll
-                        for (int bp = 0; bp < B; ++bp) O[al][bp] = rfma(c_M[SL][al][cl], Wv[bp], O[al][bp]);
+                        for (int j = 0; j < NRG; ++j) O[al][j] = rfma(c_M[SL][al][cl], Wv[j], O[al][j]);
                     }
                 }
             }
-            // horizontal Robin edges: 1-D mass along x of the bottom / top node rows
-            if (y == 0 || y == ny - 1) {
+            // horizontal Robin edges (node rows 0 and 1: group 0): 1-D mass along x
+            if (GRP == 0 && (y == 0 || y == ny - 1)) {
 #pragma unroll
                 for (int side = 0; side < 2; ++side) {
                     if (side == 0 ? y != 0 : y != ny - 1) continue;
@@ -708,49 +772,53 @@ __global__ void __launch_bounds__(kKCThreads, 1) k1_cells(K1Args a) {
                     for (int cl = 0; cl < B; ++cl) zr[cl] = zval(cl, side);
 #pragma unroll
                     for (int al = 0; al < B; ++al) {
-                        double2 s = zero;
+                        double2 sv = zero;
 #pragma unroll
                         for (int cl = 0; cl < B; ++cl)
-                            if (nzM(al, cl)) s = rfma(c_M[SL][al][cl], zr[cl], s);
-                        O[al][side] = cadd(O[al][side], mik(kh, s));
+                            if (nzM(al, cl)) sv = rfma(c_M[SL][al][cl], zr[cl], sv);
+                        O[al][side] = cadd(O[al][side], mik(kh, sv));
                     }
                 }
             }
         }
-        // carried top row of the cell row below (al != 1: the right column went to the neighbour)
+        if (GRP == 0) {  // carried top row of the cell row below (al != 1: that column went right)
 #pragma unroll
-        for (int al = 0; al < B; ++al)
-            if (al != 1) O[al][0] = cadd(O[al][0], carry[al]);
+            for (int al = 0; al < B; ++al)
+                if (al != 1) O[al][0] = cadd(O[al][0], carry[al]);
+        }
         // right column -> right neighbour
-        double2 (*Xb)[B] = sm.X[(y - ystart) & 1];
+        double2 (*Xb)[Cf::NR] = sm.X[(y - ystart) & 1][GRP];
         if (active)
 #pragma unroll
-            for (int bp = 0; bp < B; ++bp) Xb[tid][bp] = O[1][bp];
+            for (int j = 0; j < NRG; ++j) Xb[ct][j] = O[1][j];
         __syncthreads();
-        if (active && tid > 0)
+        if (active && ct > 0)
 #pragma unroll
-            for (int bp = 0; bp < B; ++bp) O[0][bp] = cadd(O[0][bp], Xb[tid - 1][bp]);
+            for (int j = 0; j < NRG; ++j) O[0][j] = cadd(O[0][j], Xb[ct - 1][j]);
+        if (GRP == 0) {
 #pragma unroll
-        for (int al = 0; al < B; ++al) carry[al] = al == 1 ? zero : O[al][1];
+            for (int al = 0; al < B; ++al) carry[al] = al == 1 ? zero : O[al][1];
+        }
 
         if (y >= yres0) {
             double2* Fs = fslot(y);
-            // residual at own nodes (a, b != 1) overwrites O; Dirichlet rows: r = f - u, restricted as 0
+            // residual at own nodes (rows != 1) overwrites O; Dirichlet rows: r = f - u, restricted as 0
             if (resid) {
 #pragma unroll
                 for (int al = 0; al < B; ++al) {
                     if (al == 1 || (!cell && al != 0)) continue;
 #pragma unroll
-                    for (int bp = 0; bp < B; ++bp) {
+                    for (int j = 0; j < NRG; ++j) {
+                        const int bp = R0 + j;
                         if (bp == 1) continue;
-                        const int pos = cell ? upos<P>(al, bp) : (bp == 0 ? 0 : bp - 1);
-                        double2 Av = O[al][bp];
-                        const bool dir = g.has_dirichlet && fine_dir<P>(g, lidx<P>(ux, al), lidx<P>(y, bp));
-                        if (dir) Av = Uy[tid * SU + pos];
-                        const double2 rv = csub(Fs[tid * SU + pos], Av);
-                        if (MODE == kK1Write) Fs[tid * SU + pos] = rv;
+                        const int pos = own_idx(al, bp);
+                        double2 Av = O[al][j];
+                        const bool dir = DIR && fine_dir<P>(g, lidx<P>(ux, al), lidx<P>(y, bp));
+                        if (dir) Av = Uy[pos];
+                        const double2 rv = csub(Fs[pos], Av);
+                        if (MODE == kK1Write) Fs[pos] = rv;
                         if (MODE == kK1Norm && y >= ys && owned) acc += rv.x * rv.x + rv.y * rv.y;
-                        O[al][bp] = dir ? zero : rv;
+                        O[al][j] = dir ? zero : rv;
                     }
                 }
             }
@@ -758,85 +826,100 @@ __global__ void __launch_bounds__(kKCThreads, 1) k1_cells(K1Args a) {
                 __syncthreads();
                 if (y >= ys) store_row(y);
             }
-            if (MODE == kK1Norm && g.has_dirichlet) __syncthreads();  // Dirichlet reads of u(y) vs its re-fill
+            if (MODE == kK1Norm && DIR) __syncthreads();  // Dirichlet reads of u(y) vs its re-fill
             if (MODE == kK1Restrict) {
+                // node rows 2..m of group 1 -> group 0 through the idle exchange buffer
+                constexpr int NH = MM >= 2 ? MM - 1 : 1;
+                double2* XR = &sm.X[(y - ystart + 1) & 1][0][0][0];
+                if (GRP == 1 && resid && MM >= 2) {
+#pragma unroll
+                    for (int al = 0; al < B; ++al) {
+                        if (al == 1 || (!cell && al != 0)) continue;
+#pragma unroll
+                        for (int h = 0; h < NH; ++h) XR[(ct * B + al) * NH + h] = O[al][h];
+                    }
+                }
+                __syncthreads();
                 double2 pt[MM + 1][MM + 1];  // partials at coarse nodes (jx, jy) of this cell
 #pragma unroll
                 for (int jx = 0; jx <= MM; ++jx)
 #pragma unroll
                     for (int jy = 0; jy <= MM; ++jy) pt[jx][jy] = zero;
-                if (resid) {
+                if (GRP == 0) {
+                    if (resid) {
 #pragma unroll
-                    for (int al = 0; al < B; ++al) {
-                        if (al == 1 || (!cell && al != 0)) continue;
-                        double2 q[MM + 1];
-#pragma unroll
-                        for (int jy = 0; jy <= MM; ++jy) {
-                            q[jy] = zero;
-#pragma unroll
-                            for (int bp = 0; bp < B; ++bp)
-                                if (bp == 0 || (bp >= 2 && bp <= MM)) q[jy] = rfma(wgt(bp, jy), O[al][bp], q[jy]);
-                        }
-#pragma unroll
-                        for (int jx = 0; jx <= MM; ++jx) {
+                        for (int al = 0; al < B; ++al) {
+                            if (al == 1 || (!cell && al != 0)) continue;
                             if (al != 0 && al > MM) continue;
-                            const double w = wgt(al, jx);
+                            double2 q[MM + 1];
 #pragma unroll
-                            for (int jy = 0; jy <= MM; ++jy) pt[jx][jy] = rfma(w, q[jy], pt[jx][jy]);
+                            for (int jy = 0; jy <= MM; ++jy) {
+                                q[jy] = rfma(wgt(0, jy), O[al][0], zero);
+                                if (MM >= 2)
+#pragma unroll
+                                    for (int h = 0; h < NH; ++h)
+                                        q[jy] = rfma(wgt(2 + h, jy), XR[(ct * B + al) * NH + h], q[jy]);
+                            }
+#pragma unroll
+                            for (int jx = 0; jx <= MM; ++jx) {
+                                const double w = wgt(al, jx);
+#pragma unroll
+                                for (int jy = 0; jy <= MM; ++jy) pt[jx][jy] = rfma(w, q[jy], pt[jx][jy]);
+                            }
                         }
                     }
+#pragma unroll
+                    for (int jx = 0; jx < MM; ++jx) pt[jx][0] = cadd(pt[jx][0], pcarry[jx]);
+                    if (active)
+#pragma unroll
+                        for (int jy = 0; jy <= MM; ++jy) sm.XP[ct][jy] = pt[MM][jy];
                 }
-#pragma unroll
-                for (int jx = 0; jx < MM; ++jx) pt[jx][0] = cadd(pt[jx][0], pcarry[jx]);
-                // XP reads of row y - 1 precede this row's exchange barrier
-                double2 (*Xp)[MM + 1] = sm.XP;
-                if (active)
-#pragma unroll
-                    for (int jy = 0; jy <= MM; ++jy) Xp[tid][jy] = pt[MM][jy];
                 __syncthreads();
-                if (active && tid > 0)
+                if (GRP == 0) {
+                    if (active && ct > 0)
 #pragma unroll
-                    for (int jy = 0; jy <= MM; ++jy) pt[0][jy] = cadd(pt[0][jy], Xp[tid - 1][jy]);
+                        for (int jy = 0; jy <= MM; ++jy) pt[0][jy] = cadd(pt[0][jy], sm.XP[ct - 1][jy]);
 #pragma unroll
-                for (int jx = 0; jx <= MM; ++jx) pcarry[jx] = jx == MM ? zero : pt[jx][MM];
-                if (owned && y >= ys) {
+                    for (int jx = 0; jx <= MM; ++jx) pcarry[jx] = jx == MM ? zero : pt[jx][MM];
+                    if (owned && y >= ys) {
 #pragma unroll
-                    for (int jx = 0; jx < MM; ++jx) {
-                        if (!cell && jx > 0) continue;
+                        for (int jx = 0; jx < MM; ++jx) {
+                            if (!cell && jx > 0) continue;
 #pragma unroll
-                        for (int jy = 0; jy < MM; ++jy) write_rc(ux * MM + jx, y * MM + jy, pt[jx][jy]);
+                            for (int jy = 0; jy < MM; ++jy) write_rc(ux * MM + jx, y * MM + jy, pt[jx][jy]);
+                        }
                     }
                 }
             }
         }
     }
 
-    // top lattice row: vertex / horizontal-edge dofs of the units (x, ny), carried in `carry`
+    // top lattice row: vertex / horizontal-edge dofs of the units (x, ny), carried by group 0
     if (top) {
-        cp_wait<0>();
-        __syncthreads();
+        wait_u(ny);
+        wait_f(ny);
         double2* Fs = fslot(ny);
         const double2* Ut = uslot(ny);
         double2 Rt[B];
 #pragma unroll
         for (int al = 0; al < B; ++al) Rt[al] = zero;
-        if (resid) {
+        if (GRP == 0 && resid) {
 #pragma unroll
             for (int al = 0; al < B; ++al) {
                 if (al == 1 || (!cell && al != 0)) continue;
-                const int pos = al == 0 ? 0 : al - 1;
+                const int pos = ct * P + (al == 0 ? 0 : al - 1);
                 double2 Av = carry[al];
-                const bool dir = g.has_dirichlet && fine_dir<P>(g, lidx<P>(ux, al), ny * P);
-                if (dir) Av = Ut[tid * SU + pos];
-                const double2 rv = csub(Fs[tid * SU + pos], Av);
-                if (MODE == kK1Write) Fs[tid * SU + pos] = rv;
+                const bool dir = DIR && fine_dir<P>(g, lidx<P>(ux, al), ny * P);
+                if (dir) Av = Ut[pos];
+                const double2 rv = csub(Fs[pos], Av);
+                if (MODE == kK1Write) Fs[pos] = rv;
                 if (MODE == kK1Norm && owned) acc += rv.x * rv.x + rv.y * rv.y;
                 Rt[al] = dir ? zero : rv;
             }
         }
         if (MODE == kK1Write) {
             __syncthreads();
-            store_row(ny);
+            store_top();
         }
         if (MODE == kK1Restrict) {
             double2 pt[MM + 1];
@@ -849,17 +932,19 @@ __global__ void __launch_bounds__(kKCThreads, 1) k1_cells(K1Args a) {
                     pt[jx] = rfma(wgt(al, jx), Rt[al], pt[jx]);
                 }
             }
-            __syncthreads();  // both exchange buffers may still be read by a neighbour
-            if (active) sm.X[0][tid][0] = pt[MM];
+            __syncthreads();  // exchange buffers may still be read by a neighbour
+            if (GRP == 0 && active) sm.XP[ct][0] = pt[MM];
             __syncthreads();
-            if (active && tid > 0) pt[0] = cadd(pt[0], sm.X[0][tid - 1][0]);
-            if (owned)
+            if (GRP == 0) {
+                if (active && ct > 0) pt[0] = cadd(pt[0], sm.XP[ct - 1][0]);
+                if (owned)
 #pragma unroll
-                for (int jx = 0; jx < MM; ++jx)
-                    if (cell || jx == 0) write_rc(ux * MM + jx, ny * MM, pt[jx]);
+                    for (int jx = 0; jx < MM; ++jx)
+                        if (cell || jx == 0) write_rc(ux * MM + jx, ny * MM, pt[jx]);
+            }
         }
     }
-    if (MODE == kK1Norm) {  // fixed-order block sum (the last warp is partial)
+    if (MODE == kK1Norm) {  // fixed-order block sum
         sm.red[tid] = acc;
         __syncthreads();
         if (tid == 0) {
@@ -868,6 +953,22 @@ __global__ void __launch_bounds__(kKCThreads, 1) k1_cells(K1Args a) {
             a.partial[blockIdx.y * gridDim.x + blockIdx.x] = sacc;
         }
     }
+}
+
+template <int P, int MODE, bool DIR>
+__global__ void __launch_bounds__(kKCThreads, 1)
+    k1_cells(const __grid_constant__ K1Args a, const __grid_constant__ CUtensorMap tmu,
+             const __grid_constant__ CUtensorMap tmf) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    // the swizzled TMA boxes need 1 KB aligned slots: align inside the allocation
+    KCSmem<P>& sm = *reinterpret_cast<KCSmem<P>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // even warps: group 0, odd warps: group 1. Warps are assigned to the SM's
+    // four schedulers by warp index mod 4, so each scheduler runs one group's
+    // code only (the two unrolled bodies would otherwise thrash its icache).
+    const int w = threadIdx.x >> 5;
+    const int ct = (w >> 1) * 32 + (threadIdx.x & 31);
+    if ((w & 1) == 0) k1c_body<P, MODE, 0, DIR>(a, &tmu, &tmf, sm, ct);
+    else k1c_body<P, MODE, 1, DIR>(a, &tmu, &tmf, sm, ct);
 }
 
 }  // namespace htg
@@ -922,16 +1023,47 @@ int k1_partials(const FineGeom& g, int rows) {
     return k1_gx(g) * k1_row_blocks(g, rows);
 }
 
-template <int P, int MODE>
-static void kc_launch_t(K1Args a, cudaStream_t st) {
+// 3-D tensor map over a fine vector for the K1 row boxes: [row][sub-row][chunk]
+template <int P>
+static CUtensorMap kc_tensor_map(const FineGeom& g, const double2* base) {
+    using C = KCCfg<P>;
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        HTG_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode),
+                                         cudaEnableDefault, &q));
+        if (!encode || q != cudaDriverEntryPointSuccess) throw RuntimeError("cuTensorMapEncodeTiled unavailable");
+    }
+    CUtensorMap m;
+    const cuuint64_t dims[3] = {cuuint64_t(C::RB / 8), cuuint64_t(g.nx) * C::RPU, cuuint64_t(g.ny)};
+    const cuuint64_t strides[2] = {cuuint64_t(C::RB), cuuint64_t(g.nx * P * P + P) * 16};
+    const cuuint32_t box[3] = {cuuint32_t(C::RB / 8), cuuint32_t(C::NU * C::RPU), 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double2*>(base), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              C::RB == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw RuntimeError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+    return m;
+}
+
+template <int P, int MODE, bool DIR>
+static void kc_launch_dir(const K1Args& a, cudaStream_t st) {
     dim3 grid(kc_strips<P>(a.g.nx), kc_row_blocks(a.g, a.rows));
-    const size_t smem = sizeof(KCSmem<P>);
+    const size_t smem = sizeof(KCSmem<P>) + 1024;
     static bool attr = false;
     if (!attr) {
-        HTG_CUDA(cudaFuncSetAttribute(k1_cells<P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        HTG_CUDA(cudaFuncSetAttribute(k1_cells<P, MODE, DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         attr = true;
     }
-    k1_cells<P, MODE><<<grid, kKCThreads, smem, st>>>(a);
+    const CUtensorMap tmu = kc_tensor_map<P>(a.g, a.u), tmf = kc_tensor_map<P>(a.g, a.f);
+    k1_cells<P, MODE, DIR><<<grid, kKCThreads, smem, st>>>(a, tmu, tmf);
+}
+
+template <int P, int MODE>
+static void kc_launch_t(K1Args a, cudaStream_t st) {
+    if (a.g.has_dirichlet) kc_launch_dir<P, MODE, true>(a, st);
+    else kc_launch_dir<P, MODE, false>(a, st);
     HTG_CUDA(cudaGetLastError());
     count_launch();
 }

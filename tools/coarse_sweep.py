@@ -5,9 +5,12 @@ import subprocess
 import sys
 
 settings = []
-for leaf in (9, 16, 36, 64):
-    for warpf in (64, 96, 128):
-        for mid in (8192, 16384, 65536):
+LEAFS = [int(v) for v in os.environ.get("SWEEP_LEAF", "9,16,36,64").split(",")]
+WARPFS = [int(v) for v in os.environ.get("SWEEP_WARPF", "64,96,128").split(",")]
+MIDS = [int(v) for v in os.environ.get("SWEEP_MID", "8192,16384,65536").split(",")]
+for leaf in LEAFS:
+    for warpf in WARPFS:
+        for mid in MIDS:
             settings.append(dict(HTG_ND_LEAF=leaf, HTG_ND_WARPF=warpf, HTG_ND_MIDDATA=mid))
 code = r'''
 import numpy as np, torch, sys
