@@ -162,76 +162,29 @@ __global__ void __launch_bounds__(kThreads, 2) k_dd_gemm(FineGeom g, DDDevice d,
     }
 }
 
-// out = u + (sum over U-memberships of Y) / L, summed in subdomain order
-template <int P>
-__global__ void k_dd_combine(FineGeom g, DDDevice d, const double2* __restrict__ ystage, const double2* u,
+// out = u + (sum over U-memberships of Y) / L, summed in subdomain order; one
+// thread per fine dof in storage order (coalesced u / out / table), the staged
+// values are gathered (they were just written and sit in L2)
+__global__ void k_dd_combine(long long ndof, DDDevice d, const double2* __restrict__ ystage, const double2* u,
                              double2* out) {
-    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    const int pp = P * P;
-    const long long cellid = t / pp;
-    const int pos = int(t - cellid * pp);
-    const int x = int(cellid % (g.nx + 1)), y = int(cellid / (g.nx + 1));
-    if (y > g.ny) return;
-    int jx, jy;
-    const bool rx = x == g.nx, ty = y == g.ny;
-    if (rx && ty) {
-        if (pos) return;
-        jx = jy = 0;
-    } else if (rx) {  // vertex + v-edge
-        if (pos >= P) return;
-        jx = 0;
-        jy = pos;
-    } else if (ty) {  // vertex + h-edge
-        if (pos >= P) return;
-        jx = pos;
-        jy = 0;
-    } else if (pos == 0) {
-        jx = jy = 0;
-    } else if (pos < P) {
-        jx = pos;
-        jy = 0;
-    } else if (pos < 2 * P - 1) {
-        jx = 0;
-        jy = pos - P + 1;
+    const long long di = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (di >= ndof) return;
+    const int src = d.srcmap[di];
+    double2 acc;
+    double inv = 1.0;
+    if (src >= 0) {
+        acc = ystage[src];
     } else {
-        const int q = pos - (2 * P - 1);
-        jx = q / (P - 1) + 1;
-        jy = q % (P - 1) + 1;
-    }
-    const int gx = x * P + jx, gy = y * P + jy;
-    const int l = d.l_dd;
-    int bxs[2], bys[2], nbxs = 0, nbys = 0;
-    {
-        const int c0 = jx ? x : x - 1, c1 = min(x, g.nx - 1);
-        for (int cc = max(c0, 0); cc <= c1; ++cc) {
-            const int b = cc / l;
-            if (nbxs == 0 || bxs[nbxs - 1] != b) bxs[nbxs++] = b;
-        }
-    }
-    {
-        const int c0 = jy ? y : y - 1, c1 = min(y, g.ny - 1);
-        for (int cc = max(c0, 0); cc <= c1; ++cc) {
-            const int b = cc / l;
-            if (nbys == 0 || bys[nbys - 1] != b) bys[nbys++] = b;
-        }
-    }
-    double2 acc = make_double2(0.0, 0.0);
-    for (int iy = 0; iy < nbys; ++iy)
-        for (int ix = 0; ix < nbxs; ++ix) {
-            const int s = bys[iy] * d.nbx + bxs[ix];
-            const int c = d.sub_class[s];
-            const int* ci = d.cls_info + 8 * c;
-            const int so = d.sub_o[s];
-            const int lgx = gx - (so & 0xffff) * P, lgy = gy - (so >> 16) * P;
-            const int li = int(dof_index(ci[0], ci[1], P, lgx, lgy));
-            const int row = d.rowmap[ci[6] + li];
-            const double2 yv = ystage[(size_t)s * d.nu_max + row];
+        const int k = -1 - src, b0 = d.bptr[k], b1 = d.bptr[k + 1];
+        acc = make_double2(0.0, 0.0);
+        for (int b = b0; b < b1; ++b) {
+            const double2 yv = ystage[d.bsrc[b]];
             acc.x += yv.x;
             acc.y += yv.y;
         }
-    const double inv = 1.0 / double(nbxs * nbys);
-    const long long di = dof_index(g.nx, g.ny, P, gx, gy);
-    double2 base = u ? u[di] : make_double2(0.0, 0.0);
+        inv = 1.0 / double(b1 - b0);
+    }
+    const double2 base = u ? u[di] : make_double2(0.0, 0.0);
     out[di] = make_double2(base.x + acc.x * inv, base.y + acc.y * inv);
 }
 
@@ -260,14 +213,7 @@ void dd_gemm_launch(const FineGeom& g, const DDDevice& d, const double2* r, doub
 
 void dd_combine_launch(const FineGeom& g, const DDDevice& d, const double2* ystage, const double2* u, double2* out,
                        cudaStream_t st) {
-    const long long n = (long long)(g.nx + 1) * (g.ny + 1) * g.p * g.p;
-    const unsigned nb = unsigned((n + 255) / 256);
-    switch (g.p) {
-        case 2: k_dd_combine<2><<<nb, 256, 0, st>>>(g, d, ystage, u, out); break;
-        case 4: k_dd_combine<4><<<nb, 256, 0, st>>>(g, d, ystage, u, out); break;
-        case 6: k_dd_combine<6><<<nb, 256, 0, st>>>(g, d, ystage, u, out); break;
-        default: k_dd_combine<8><<<nb, 256, 0, st>>>(g, d, ystage, u, out); break;
-    }
+    k_dd_combine<<<unsigned((g.ndof + 255) / 256), 256, 0, st>>>(g.ndof, d, ystage, u, out);
     HTG_CUDA(cudaGetLastError());
     count_launch();
 }
@@ -355,6 +301,32 @@ DDDevice upload_dd_impl(const DDSetup& dd, const HostProblem& hp, std::vector<vo
         for (int m0 = 0; m0 < c.nu; m0 += kTM)
             for (int n0 = 0; n0 < int(subs[ci].size()); n0 += kTN) tiles.push_back(make_int4(ci, m0, n0, off));
     }
+    // partition-of-unity combine table: every fine dof's staged values in subdomain order
+    std::vector<int> srcmap(size_t(hp.ndof()), 0), bptr{0}, bsrc;
+    {
+        std::vector<std::vector<int>> lists(size_t(hp.ndof()));
+        for (int s = 0; s < d.nsub; ++s) {
+            const int ci = dd.sub_class[s];
+            const DDClass& c = dd.classes[ci];
+            const int lo = info[8 * ci + 6];
+            for (int rI = 0; rI < c.nu; ++rI) {
+                const int lxy = locg[lo + c.umem[rI]];
+                const int gx = dd.sub_ox[s] * p + (lxy & 0xffff), gy = dd.sub_oy[s] * p + (lxy >> 16);
+                lists[size_t(dof_index(hp.nx, hp.ny, p, gx, gy))].push_back(s * nu_max + rI);
+            }
+        }
+        for (size_t di = 0; di < lists.size(); ++di) {
+            const auto& li = lists[di];
+            if (li.empty()) throw RuntimeError("dd setup: fine dof outside every subdomain U");
+            if (li.size() == 1) {
+                srcmap[di] = li[0];
+            } else {
+                srcmap[di] = -int(bptr.size());
+                bsrc.insert(bsrc.end(), li.begin(), li.end());
+                bptr.push_back(int(bsrc.size()));
+            }
+        }
+    }
     // big classes first
     std::stable_sort(tiles.begin(), tiles.end(), [&](const int4& a, const int4& b) {
         return info[8 * a.x + 4] * 1.0 > info[8 * b.x + 4] * 1.0;
@@ -380,6 +352,9 @@ DDDevice upload_dd_impl(const DDSetup& dd, const HostProblem& hp, std::vector<vo
     d.class_subs = up(class_subs);
     d.ntiles = int(tiles.size());
     d.nu_max = nu_max;
+    d.srcmap = up(srcmap);
+    d.bptr = up(bptr);
+    d.bsrc = up(bsrc);
     for (FdmClassDev& f : fdm) {  // patch offsets into device pointers
         f.rowmap = d.rowmap + size_t(f.rowmap);
         f.subs = d.class_subs + size_t(f.subs);

@@ -64,6 +64,12 @@ struct DDDevice {
     // per tile: class, m0, n0, sub list offset
     const int4* tiles;
     const int* class_subs;    // subdomains of each class, contiguous
+    // partition-of-unity combine table per fine dof: >= 0: the only staged value
+    // (dof in one U), < 0: -(1 + k) for shared dof k, whose staged values are
+    // bsrc[bptr[k] .. bptr[k + 1]) in subdomain order
+    const int* srcmap;
+    const int* bptr;
+    const int* bsrc;
 };
 void dd_gemm_launch(const FineGeom& g, const DDDevice& d, const double2* r, double2* ystage, cudaStream_t st);
 // separable classes: fast-diagonalisation subdomain solves (k_fdm.cu)
@@ -84,7 +90,7 @@ struct FdmLaunch {
 void dd_fdm_launch(const FineGeom& g, const FdmLaunch& L, const double2* r, double2* ystage, int nu_max,
                    cudaStream_t st);
 std::vector<int4> fdm_work_table(std::vector<FdmClassDev>& cls, int nsm);
-// out = u + sum_i y_i / L (u may be null -> 0); out may alias u
+// out = u + sum_i y_i / L in subdomain order (u may be null -> 0); out may alias u
 void dd_combine_launch(const FineGeom& g, const DDDevice& d, const double2* ystage, const double2* u, double2* out,
                        cudaStream_t st);
 
