@@ -290,10 +290,12 @@ def run_ours(args):
     dd_tf = ops.dd_flops / (prof["dd_gemm"] * 1e-3) / 1e12
     hbm_peak, hbm_src = peaks()
     res_gbs = BYTES_PER_DOF_RESIDUAL * n / (prof["residual"] * 1e-3) / 1e9
-    traffic = None
+    traffic = res_traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh_:
-            traffic = json.load(fh_).get("dd_dram_bytes_per_launch")
+            tj = json.load(fh_)
+            traffic = tj.get("dd_dram_bytes_per_launch")
+            res_traffic = tj.get("residual_dram_bytes_per_launch")
     except Exception:
         pass
     # the general dense path (every class as one batched DMMA GEMM), measured on a
@@ -336,8 +338,10 @@ def run_ours(args):
                      "peak_source": "measured in this run: DMMA m8n8k4 f64 microbenchmark (no FP64 entry in "
                                     "MEASURED_PEAKS.json)",
                      "algorithmic_flops_per_launch": ops.dd_flops},
-        "roofline_residual": {"bound": "hbm", "kernel": "k1_residual", "achieved": res_gbs, "peak": hbm_peak,
+        "roofline_residual": {"bound": "hbm", "kernel": "k1_cells (r = f - A u, one thread per cell)",
+                              "achieved": res_gbs, "peak": hbm_peak,
                               "unit": "GB/s", "frac": res_gbs / hbm_peak, "peak_source": hbm_src,
+                              "traffic": res_traffic,
                               "algorithmic_bytes_per_launch": BYTES_PER_DOF_RESIDUAL * n},
         "e2e": e2e,
         "gpu_launches": launches,

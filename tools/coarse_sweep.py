@@ -8,10 +8,12 @@ settings = []
 LEAFS = [int(v) for v in os.environ.get("SWEEP_LEAF", "9,16,36,64").split(",")]
 WARPFS = [int(v) for v in os.environ.get("SWEEP_WARPF", "64,96,128").split(",")]
 MIDS = [int(v) for v in os.environ.get("SWEEP_MID", "8192,16384,65536").split(",")]
+RPTS = [int(v) for v in os.environ.get("SWEEP_RPT", "8").split(",")]
 for leaf in LEAFS:
     for warpf in WARPFS:
         for mid in MIDS:
-            settings.append(dict(HTG_ND_LEAF=leaf, HTG_ND_WARPF=warpf, HTG_ND_MIDDATA=mid))
+            for rpt in RPTS:
+                settings.append(dict(HTG_ND_LEAF=leaf, HTG_ND_WARPF=warpf, HTG_ND_MIDDATA=mid, HTG_ND_RPT=rpt))
 code = r'''
 import numpy as np, torch, sys
 sys.path.insert(0, ".")
