@@ -610,6 +610,7 @@ __device__ __forceinline__ void k1c_body(const K1Args& a, const CUtensorMap* tmu
     const int yres0 = MODE == kK1Restrict ? max(ys - 1, 0) : ys;  // first row whose residual is needed
     const bool top = ye == ny;
     const double2* mt = a.shifted ? g.mtabS : g.mtab0;
+    const double2 m_uniform = mt[0];  // one coefficient class: loaded once
 
     auto uslot = [&](int yy) { return sm.U[(yy - ystart) % 3]; };
     auto fslot = [&](int yy) { return sm.F[(yy - yres0) % 3]; };
@@ -720,7 +721,7 @@ __device__ __forceinline__ void k1c_body(const K1Args& a, const CUtensorMap* tmu
 #pragma unroll
             for (int j = 0; j < NRG; ++j) O[i][j] = zero;
         if (cell) {
-            const double2 m = mt[g.cls ? g.cls[(size_t)y * nx + ux] : 0];
+            const double2 m = g.cls ? mt[g.cls[(size_t)y * nx + ux]] : m_uniform;
 #pragma unroll
             for (int cl = 0; cl < B; ++cl) {
                 double2 zc[B];
@@ -961,7 +962,9 @@ __global__ void __launch_bounds__(kKCThreads, 1)
              const __grid_constant__ CUtensorMap tmf) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // the swizzled TMA boxes need 1 KB aligned slots: align inside the allocation
-    KCSmem<P>& sm = *reinterpret_cast<KCSmem<P>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // (offset arithmetic on the shared pointer keeps the accesses LDS/STS)
+    const unsigned pad = (1024u - (static_cast<unsigned>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u;
+    KCSmem<P>& sm = *reinterpret_cast<KCSmem<P>*>(smem_raw + pad);
     // even warps: group 0, odd warps: group 1. Warps are assigned to the SM's
     // four schedulers by warp index mod 4, so each scheduler runs one group's
     // code only (the two unrolled bodies would otherwise thrash its icache).
