@@ -10,7 +10,8 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhelmtg_b200.so")
+# HTG_LIB selects another build of the same library (kernel variants under exp/)
+LIB_PATH = os.environ.get("HTG_LIB") or os.path.join(HERE, "libhelmtg_b200.so")
 CSRC = os.path.join(HERE, "csrc")
 
 HTG_OK, HTG_ERR_RUNTIME, HTG_ERR_INVALID, HTG_NOT_CONVERGED = 0, 1, 2, 3

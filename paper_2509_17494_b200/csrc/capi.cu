@@ -208,7 +208,7 @@ void build_handle(htg_handle* H, const htg_problem& prob, const htg_config& cfg)
         for (int sI = 0; sI < int(dd.sub_class.size()); ++sI) {
             const DDClass& c = dd.classes[dd.sub_class[sI]];
             H->dd_flops_dense += 8.0 * c.nu * c.nloc;
-            if (c.fdm && c.fdm_nx <= 32 && c.fdm_ny <= 32 && hp.p <= 4) {
+            if (c.fdm && fdm_supported(hp.p, c.fdm_nx, c.fdm_ny)) {
                 const double nx = c.fdm_nx, ny = c.fdm_ny, ux = c.fdm_nux, uy = c.fdm_nuy;
                 H->dd_flops += 8.0 * (nx * nx * ny + nx * ny * ny + ux * nx * ny + ux * ny * uy);
                 H->fdm_subs += 1;
@@ -222,7 +222,7 @@ void build_handle(htg_handle* H, const htg_problem& prob, const htg_config& cfg)
         if (!H->fdm.empty()) {
             int nsm = 0;
             HTG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
-            const std::vector<int4> work = fdm_work_table(H->fdm, nsm);  // sets FdmClassDev::first
+            const std::vector<int4> work = fdm_plan(H->fdm, hp.p, nsm, H->fdm_launch);  // sets FdmClassDev::first
             H->fdm_launch.classes = M.upload(H->fdm, st);
             H->fdm_launch.work = M.upload(work, st);
             H->fdm_launch.nwork = int(work.size());

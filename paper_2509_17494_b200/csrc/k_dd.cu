@@ -266,7 +266,7 @@ DDDevice upload_dd_impl(const DDSetup& dd, const HostProblem& hp, std::vector<vo
         rowmap.insert(rowmap.end(), rm.begin(), rm.end());
         const int off = int(class_subs.size());
         class_subs.insert(class_subs.end(), subs[ci].begin(), subs[ci].end());
-        if (c.fdm && c.fdm_nx <= 32 && c.fdm_ny <= 32 && p <= 4) {
+        if (c.fdm && fdm_supported(p, c.fdm_nx, c.fdm_ny)) {
             FdmClassDev f{};
             f.nx = c.fdm_nx;
             f.ny = c.fdm_ny;

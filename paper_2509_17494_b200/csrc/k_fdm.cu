@@ -3,11 +3,19 @@
 // For a class with A_s^(Omega) = Kx (x) My + Mx (x) Ky (fdm.cpp) the U rows of
 // A^-1 g are, with the gathered residual as a tensor tile G[ix][iy],
 //   Y_U = Vx_U [ (Vx^T G Vy) o Dinv ] Vy_U^T,
-// four small complex products per subdomain (8 (2 nx^2 ny + nux nx ny + nux ny nuy)
+// four small complex products per subdomain (8 (nx^2 ny + nx ny^2 + nux nx ny + nux ny nuy)
 // flop, 3.7x fewer than the dense |U| x |Omega| product at p = 4).
-// A CTA runs kGroups groups of 4 warps; a group takes one subdomain at a time
-// (named barrier per group), the class factors sit in shared memory, every
-// stage is mma.sync.m8n8k4.f64 on tiles padded to 32 with k steps of 4.
+//
+// Batching: the four products share their class factor, so a group of 4 warps
+// solves S subdomains of one class at once, stacked along the data dimension
+// of every product (S = 2 at p = 4 with 4 groups: 50 data rows instead of
+// 2 x 25 padded to 2 x 32). Only the factor dimension is padded to the m8/n8
+// tile, and the contraction to the k4 step: 13% fewer DMMAs than one
+// subdomain per product. Four groups per CTA (one CTA per SM, 16 warps, the
+// whole 227 KB of shared memory) alternate batches of the CTA's range; measured
+// at cfg4: 2 groups x S=4 0.265 ms, 3 x S=2 0.259 ms, 4 x S=2 0.242 ms.
+// Every product is mma.sync.m8n8k4.f64 in the Gauss (3M) form: three real
+// DMMAs per complex k-step and tile.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -19,24 +27,17 @@ namespace htg {
 
 namespace {
 
-// rows padded to 32 (m8/n8 tiles), k to 28 (k4 steps); LD = 28 = 4 mod 8 keeps the
-// 128-bit fragment loads of 8 lanes (2 rows x 4 k) on distinct banks
-constexpr int kNP = 32, kLDF = 28;
 #ifndef HTG_FDM_GROUPS
 #define HTG_FDM_GROUPS 4
 #endif
-constexpr int kGroups = HTG_FDM_GROUPS, kFThreads = kGroups * 128;
-constexpr int kXBuf = kGroups <= 3 ? 2 : 1;  // prefetch the next tile when shared memory allows
+constexpr int kFGroups = HTG_FDM_GROUPS, kFThreads = kFGroups * 128;
+constexpr int kSmemMax = 232448;  // opt-in dynamic shared memory per block (227 KB)
 
-struct FdmSmem {
-    double2 V1T[kNP][kLDF];  // A of stage 1: [ix'][ix] = Vx[ix][ix']
-    double2 V2T[kNP][kLDF];  // B of stage 2: [iy'][iy] = Vy[iy][iy']
-    double2 V1U[kNP][kLDF];  // A of stage 3: [ixu][ix'] = Vx[ux0 + ixu][ix']
-    double2 V2U[kNP][kLDF];  // B of stage 4: [iyu][iy'] = Vy[uy0 + iyu][iy']
-    double2 D[kNP][kNP + 1]; // Dinv[ix'][iy']
-    double2 X[kGroups][kXBuf][kNP][kLDF];  // gathered tile (ping-pong when prefetching)
-    double2 W[kGroups][kNP][kLDF];
-};
+// Row pitch of every operand (double2): 4 mod 8 keeps the 128-bit fragment
+// loads of 8 lanes (2 rows x 4 k) on distinct banks; k steps cover [0, 4 KS).
+template <int P> struct FdmDims;
+template <> struct FdmDims<2> { static constexpr int LD = 20, KS = 4; };  // extents <= 16
+template <> struct FdmDims<4> { static constexpr int LD = 28, KS = 7; };  // extents <= 28
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -50,184 +51,366 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
+// exact floor(n / d) for 0 <= n < 2^16 and small d (margin 0.5 / n >> fp32 rounding)
+__device__ __forceinline__ int fdiv(int n, float inv) { return __float2int_rz((float(n) + 0.5f) * inv); }
 
-// C[m][n] = sum_k A[m][k] B[n][k] over MT x NT 8x8 tiles, KS k-steps of 4; the
-// group's warp q owns tiles q, q+4, q+8, q+12 (all in flight together).
-// epi(m, n, value) is called for every element of the warp's tiles.
-template <class Epi>
-__device__ __forceinline__ void stage(const double2 (*A)[kLDF], const double2 (*B)[kLDF], int MT, int NT, int KS,
-                                      int q, int lane, Epi&& epi) {
-    const int nt_all = MT * NT;
-    // Gauss / 3M complex product: t1 = ar br, t2 = ai bi, t3 = (ar + ai)(br + bi);
-    // re = t1 - t2, im = t3 - t1 - t2 -- three DMMAs per k-step and tile instead of four
-    double t1[4][2], t2[4][2], t3[4][2];
-    int tm[4], tn[4];
+// One stage C[m][n] = sum_k A[m][k] B[n][k], A rows [0, am), B rows [0, bn),
+// MT x NT tiles of 8 x 8, KS k steps of 4. Rows past am / bn are clamped (their
+// outputs are discarded); the k padding of one operand is zero, so the
+// padded k columns contribute exactly zero.
+//
+// Tile order per warp q of the group:
+//   MT % 4 == 0: A-stationary, the warp owns m-tiles q, q+4, .., its A
+//                fragments stay in registers over all n-tiles (1 load per tile-step);
+//   NT % 4 == 0: B-stationary, likewise;
+//   otherwise:   tiles q, q+4, q+8, .. of the flattened list, 4 in flight.
+// The tile count of a group of tiles is a template argument, so the DMMAs are
+// straight-line code without predicates.
+#ifndef HTG_FDM_KSPLIT
+#define HTG_FDM_KSPLIT 1
+#endif
+constexpr int kKP = HTG_FDM_KSPLIT;  // independent accumulator chains per product (k steps interleaved)
+
+template <int LD, int KS>
+struct Stage {
+    const double2* A;
+    const double2* B;
+    int am, bn, MT, NT, q, lane;
+
+    using Acc = double[kKP][4][2];
+    template <int NTL, class Epi>
+    __device__ __forceinline__ void finish(Acc& t1, Acc& t2, Acc& t3, const int* tm, const int* tn, Epi& epi) const {
+        const int r = lane >> 2, kq = lane & 3;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        t1[j][0] = t1[j][1] = t2[j][0] = t2[j][1] = t3[j][0] = t3[j][1] = 0.0;
-        const int t = q + 4 * j;
-        tm[j] = t < nt_all ? t / NT : -1;
-        tn[j] = t < nt_all ? t % NT : 0;
+        for (int j = 0; j < NTL; ++j)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                double a1 = t1[0][j][i], a2 = t2[0][j][i], a3 = t3[0][j][i];
+#pragma unroll
+                for (int h = 1; h < kKP; ++h) {
+                    a1 += t1[h][j][i];
+                    a2 += t2[h][j][i];
+                    a3 += t3[h][j][i];
+                }
+                epi(tm[j] * 8 + r, tn[j] * 8 + 2 * kq + i, make_double2(a1 - a2, a3 - a1 - a2));
+            }
     }
-    const int r = lane >> 2, kq = lane & 3;
-    const int ntile = max(0, min(4, (nt_all - q + 3) / 4));
-    for (int ks = 0; ks < KS; ++ks) {
-        const int k = ks * 4 + kq;
-        double2 a[4], b[4];
+    template <int NTL>
+    __device__ __forceinline__ static void zero(Acc& t1, Acc& t2, Acc& t3) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int m = j < ntile ? tm[j] : 0, n = j < ntile ? tn[j] : 0;
-            a[j] = A[m * 8 + r][k];
-            b[j] = B[n * 8 + r][k];
+        for (int h = 0; h < kKP; ++h)
+#pragma unroll
+            for (int j = 0; j < NTL; ++j)
+                t1[h][j][0] = t1[h][j][1] = t2[h][j][0] = t2[h][j][1] = t3[h][j][0] = t3[h][j][1] = 0.0;
+    }
+
+    // stationary fragments sf/ss (all k), moving operand rows mv + mrow[j]
+    template <int NTL, bool SA, class Epi>
+    __device__ __forceinline__ void run_stat(const double2 (&sf)[KS], const double (&ss)[KS], const double2* mv,
+                                             const int* mrow, const int* tm, const int* tn, Epi& epi) const {
+        Acc t1, t2, t3;
+        zero<NTL>(t1, t2, t3);
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+            const int h = ks % kKP;
+            double2 v[4];
+            double vs[4];
+#pragma unroll
+            for (int j = 0; j < NTL; ++j) {
+                v[j] = mv[mrow[j] + ks * 4];
+                vs[j] = v[j].x + v[j].y;
+            }
+#pragma unroll
+            for (int j = 0; j < NTL; ++j) {
+                if (SA) dmma(t1[h][j][0], t1[h][j][1], sf[ks].x, v[j].x);
+                else dmma(t1[h][j][0], t1[h][j][1], v[j].x, sf[ks].x);
+            }
+#pragma unroll
+            for (int j = 0; j < NTL; ++j) {
+                if (SA) dmma(t2[h][j][0], t2[h][j][1], sf[ks].y, v[j].y);
+                else dmma(t2[h][j][0], t2[h][j][1], v[j].y, sf[ks].y);
+            }
+#pragma unroll
+            for (int j = 0; j < NTL; ++j) {
+                if (SA) dmma(t3[h][j][0], t3[h][j][1], ss[ks], vs[j]);
+                else dmma(t3[h][j][0], t3[h][j][1], vs[j], ss[ks]);
+            }
         }
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-            if (j < ntile) dmma(t1[j][0], t1[j][1], a[j].x, b[j].x);
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-            if (j < ntile) dmma(t2[j][0], t2[j][1], a[j].y, b[j].y);
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-            if (j < ntile) dmma(t3[j][0], t3[j][1], a[j].x + a[j].y, b[j].x + b[j].y);
+        finish<NTL>(t1, t2, t3, tm, tn, epi);
     }
+
+    template <int NTL, class Epi>
+    __device__ __forceinline__ void run_pairs(const int* ar, const int* br, const int* tm, const int* tn,
+                                              Epi& epi) const {
+        Acc t1, t2, t3;
+        zero<NTL>(t1, t2, t3);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        if (tm[j] < 0) break;
+        for (int ks = 0; ks < KS; ++ks) {
+            const int h = ks % kKP;
+            double2 a[4], b[4];
+            double as[4], bs[4];
 #pragma unroll
-        for (int i = 0; i < 2; ++i)
-            epi(tm[j] * 8 + r, tn[j] * 8 + 2 * kq + i,
-                make_double2(t1[j][i] - t2[j][i], t3[j][i] - t1[j][i] - t2[j][i]));
+            for (int j = 0; j < NTL; ++j) {
+                a[j] = A[ar[j] + ks * 4];
+                b[j] = B[br[j] + ks * 4];
+                as[j] = a[j].x + a[j].y;
+                bs[j] = b[j].x + b[j].y;
+            }
+#pragma unroll
+            for (int j = 0; j < NTL; ++j) dmma(t1[h][j][0], t1[h][j][1], a[j].x, b[j].x);
+#pragma unroll
+            for (int j = 0; j < NTL; ++j) dmma(t2[h][j][0], t2[h][j][1], a[j].y, b[j].y);
+#pragma unroll
+            for (int j = 0; j < NTL; ++j) dmma(t3[h][j][0], t3[h][j][1], as[j], bs[j]);
+        }
+        finish<NTL>(t1, t2, t3, tm, tn, epi);
     }
-}
+
+    template <class Epi>
+    __device__ __forceinline__ void operator()(Epi&& epi) const {
+        const int r = lane >> 2, kq = lane & 3;
+        if ((MT & 3) == 0 || (NT & 3) == 0) {
+            const bool sa = (MT & 3) == 0;
+            const int ST = sa ? MT : NT, OT = sa ? NT : MT;
+            const double2* S = sa ? A : B;
+            const double2* O = sa ? B : A;
+            const int slim = (sa ? am : bn) - 1, olim = (sa ? bn : am) - 1;
+            for (int st = q; st < ST; st += 4) {
+                double2 sf[KS];
+                double ss[KS];
+                const double2* srow = S + min(st * 8 + r, slim) * LD + kq;
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks) {
+                    sf[ks] = srow[ks * 4];
+                    ss[ks] = sf[ks].x + sf[ks].y;
+                }
+                for (int o0 = 0; o0 < OT; o0 += 4) {
+                    const int nt = min(4, OT - o0);
+                    int mrow[4], tm[4], tn[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        mrow[j] = min((o0 + j) * 8 + r, olim) * LD + kq;
+                        tm[j] = sa ? st : o0 + j;
+                        tn[j] = sa ? o0 + j : st;
+                    }
+                    if (sa) {
+                        switch (nt) {
+                            case 4: run_stat<4, true>(sf, ss, O, mrow, tm, tn, epi); break;
+                            case 3: run_stat<3, true>(sf, ss, O, mrow, tm, tn, epi); break;
+                            case 2: run_stat<2, true>(sf, ss, O, mrow, tm, tn, epi); break;
+                            default: run_stat<1, true>(sf, ss, O, mrow, tm, tn, epi); break;
+                        }
+                    } else {
+                        switch (nt) {
+                            case 4: run_stat<4, false>(sf, ss, O, mrow, tm, tn, epi); break;
+                            case 3: run_stat<3, false>(sf, ss, O, mrow, tm, tn, epi); break;
+                            case 2: run_stat<2, false>(sf, ss, O, mrow, tm, tn, epi); break;
+                            default: run_stat<1, false>(sf, ss, O, mrow, tm, tn, epi); break;
+                        }
+                    }
+                }
+            }
+            return;
+        }
+        const int total = MT * NT;
+        for (int t0 = q; t0 < total; t0 += 16) {
+            const int nt = min(4, (total - t0 + 3) / 4);
+            int tm[4], tn[4], ar[4], br[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int t = min(t0 + 4 * j, total - 1);
+                tm[j] = t % MT;
+                tn[j] = t / MT;
+                ar[j] = min(tm[j] * 8 + r, am - 1) * LD + kq;
+                br[j] = min(tn[j] * 8 + r, bn - 1) * LD + kq;
+            }
+            switch (nt) {
+                case 4: run_pairs<4>(ar, br, tm, tn, epi); break;
+                case 3: run_pairs<3>(ar, br, tm, tn, epi); break;
+                case 2: run_pairs<2>(ar, br, tm, tn, epi); break;
+                default: run_pairs<1>(ar, br, tm, tn, epi); break;
+            }
+        }
+    }
+};
 
 template <int P>
 __global__ void __launch_bounds__(kFThreads, 1) k_dd_fdm(FineGeom g, const FdmClassDev* __restrict__ classes,
                                                          const int4* __restrict__ work, const double2* __restrict__ r,
-                                                         double2* __restrict__ ystage, int nu_max) {
+                                                         double2* __restrict__ ystage, int nu_max, int rows,
+                                                         int fac_elems) {
+    constexpr int LD = FdmDims<P>::LD, KS = FdmDims<P>::KS;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    FdmSmem& sm = *reinterpret_cast<FdmSmem*>(smem_raw);
+    double2* fac = reinterpret_cast<double2*>(smem_raw);
     const int tid = threadIdx.x;
-    const int4 wk = work[blockIdx.x];  // first, end index into the class-sorted subdomain list
     const int grp = tid >> 7, gt = tid & 127, q = gt >> 5, lane = tid & 31;
-    double2 (*W)[kLDF] = sm.W[grp];
-    // segments of one class inside this CTA's range: reload the factors per segment
+    double2* X = fac + fac_elems + size_t(grp) * 2 * rows * LD;  // gathered tile, then Q o Dinv
+    double2* W = X + rows * LD;                                  // stage 1 / stage 3 products
+    {  // the k padding of the data buffers must be finite: zero them once
+        double2* data = fac + fac_elems;
+        for (int i = tid; i < kFGroups * 2 * rows * LD; i += kFThreads) data[i] = make_double2(0.0, 0.0);
+    }
+    const int4 wk = work[blockIdx.x];  // [first, end) of the class-sorted subdomain list
     int pos = wk.x;
     while (pos < wk.y) {
         int ci = 0;
         while (classes[ci].first + classes[ci].nsub <= pos) ++ci;
         const FdmClassDev c = classes[ci];
         const int seg_end = min(wk.y, c.first + c.nsub);
+        const int nx = c.nx, ny = c.ny, nux = c.nux, nuy = c.nuy;
+        double2* V1T = fac;              // [ix'][ix] = Vx[ix][ix']
+        double2* V2T = V1T + nx * LD;    // [iy'][iy] = Vy[iy][iy']
+        double2* V1U = V2T + ny * LD;    // [ixu][ix'] = Vx[ux0 + ixu][ix']
+        double2* V2U = V1U + nux * LD;   // [iyu][iy'] = Vy[uy0 + iyu][iy']
+        double2* D = V2U + nuy * LD;     // Dinv[ix'][iy']
         __syncthreads();  // previous segment finished with the factors
-        for (int i = tid; i < kNP * kLDF; i += kFThreads) {
-            const int a = i / kLDF, b = i % kLDF;
-            const double2 z = make_double2(0.0, 0.0);
-            sm.V1T[a][b] = (a < c.nx && b < c.nx) ? c.Vx[b * c.nx + a] : z;
-            sm.V2T[a][b] = (a < c.ny && b < c.ny) ? c.Vy[b * c.ny + a] : z;
-            sm.V1U[a][b] = (a < c.nux && b < c.nx) ? c.Vx[(c.ux0 + a) * c.nx + b] : z;
-            sm.V2U[a][b] = (a < c.nuy && b < c.ny) ? c.Vy[(c.uy0 + a) * c.ny + b] : z;
+        const double2 z = make_double2(0.0, 0.0);
+        for (int i = tid; i < (nx + ny + nux + nuy) * LD; i += kFThreads) {
+            const int a = i / LD, b = i - a * LD;
+            double2 v = z;
+            if (a < nx) v = b < nx ? c.Vx[b * nx + a] : z;
+            else if (a < nx + ny) v = b < ny ? c.Vy[b * ny + (a - nx)] : z;
+            else if (a < nx + ny + nux) v = b < nx ? c.Vx[(c.ux0 + a - nx - ny) * nx + b] : z;
+            else v = b < ny ? c.Vy[(c.uy0 + a - nx - ny - nux) * ny + b] : z;
+            fac[i] = v;
         }
-        for (int i = tid; i < kNP * kNP; i += kFThreads) {
-            const int a = i / kNP, b = i % kNP;
-            sm.D[a][b] = (a < c.nx && b < c.ny) ? c.Dinv[a * c.ny + b] : make_double2(0.0, 0.0);
-        }
-        // work buffers: padding must be zero for this class's extents
-        for (int i = gt; i < kNP * kLDF; i += 128) {
-            for (int b2 = 0; b2 < kXBuf; ++b2) (&sm.X[grp][b2][0][0])[i] = make_double2(0.0, 0.0);
-            (&W[0][0])[i] = make_double2(0.0, 0.0);
+        for (int i = tid; i < nx * ny; i += kFThreads) D[i] = c.Dinv[i];
+        // U row of each (ixu, iyu) of U
+        int* urow = reinterpret_cast<int*>(D + nx * ny) + kFGroups * 16;
+        for (int i = tid; i < nux * nuy; i += kFThreads) {
+            const int ixu = i / nuy, iyu = i - ixu * nuy;
+            urow[i] = c.rowmap[dof_index(c.onx, c.ony, P, c.ux0 + ixu, c.uy0 + iyu)];
         }
         __syncthreads();
-        const int MTx = (c.nx + 7) / 8, MTy = (c.ny + 7) / 8, MTux = (c.nux + 7) / 8, MTuy = (c.nuy + 7) / 8;
-        const int KSx = (c.nx + 3) / 4, KSy = (c.ny + 3) / 4;
-        const int nloc = c.nx * c.ny;
-        auto gather = [&](int sp, double2 (*X)[kLDF]) {
-            const int s = c.subs[sp - c.first];
-            const int so = c.sub_o[s];
-            const int ox = (so & 0xffff) * P, oy = (so >> 16) * P;
-            for (int l = gt; l < nloc; l += 128) {
-                const int iy = l / c.nx, ix = l - iy * c.nx;
-                cp_async16(&X[iy][ix], r + dof_index(g.nx, g.ny, P, ox + ix, oy + iy));
+        const int S = min(8, rows / max(nx, ny));  // subdomains per batch
+        const int nxy = nx * ny;
+        const float inv_nx = 1.0f / nx, inv_ny = 1.0f / ny, inv_nux = 1.0f / nux;
+        // subdomain ids of the group's batches (double-buffered by batch parity: the
+        // next batch is gathered while stage 4 of the current one still stores)
+        int* sid = reinterpret_cast<int*>(D + nx * ny) + grp * 16;
+        int par = 0;
+        auto gather = [&](int b0, int nb, int pr) {
+            if (gt < nb) sid[pr * 8 + gt] = c.subs[b0 - c.first + gt];
+            for (int s = 0; s < nb; ++s) {
+                const int so = c.sub_o[c.subs[b0 - c.first + s]];
+                const int ox = (so & 0xffff) * P, oy = (so >> 16) * P;
+                double2* xs = X + s * ny * LD;
+                for (int l = gt; l < nxy; l += 128) {
+                    const int iy = fdiv(l, inv_nx), ix = l - iy * nx;
+                    cp_async16(&xs[iy * LD + ix], r + dof_index(g.nx, g.ny, P, ox + ix, oy + iy));
+                }
             }
             asm volatile("cp.async.commit_group;\n" ::: "memory");
         };
-        int cur = 0;
-        if (pos + grp < seg_end) gather(pos + grp, sm.X[grp][0]);
-        for (int sp = pos + grp; sp < seg_end; sp += kGroups, cur ^= (kXBuf - 1)) {
-            double2 (*X)[kLDF] = sm.X[grp][cur];
-            const int s = c.subs[sp - c.first];
+        // batches of S subdomains, alternating between the two groups
+        int b0 = pos + grp * S;
+        if (b0 < seg_end) gather(b0, min(S, seg_end - b0), 0);
+        for (; b0 < seg_end; b0 += kFGroups * S, par ^= 1) {
+            const int nb = min(S, seg_end - b0);
             asm volatile("cp.async.wait_all;\n" ::: "memory");
             group_sync(grp);
-            if (kXBuf == 2 && sp + kGroups < seg_end) gather(sp + kGroups, sm.X[grp][cur ^ 1]);  // prefetch
-            // 1: P[ix'][iy] = sum_ix Vx[ix][ix'] G[ix][iy]  -> W[ix'][iy]
-            stage(sm.V1T, X, MTx, MTy, KSx, q, lane, [&](int m, int n, double2 v) {
-                if (m < c.nx && n < c.ny) W[m][n] = v;
-            });
-            group_sync(grp);
-            // 2: Q[ix'][iy'] = (sum_iy P[ix'][iy] Vy[iy][iy']) Dinv[ix'][iy']  -> X[iy'][ix']
-            stage(W, sm.V2T, MTx, MTy, KSy, q, lane, [&](int m, int n, double2 v) {
-                if (m < c.nx && n < c.ny) {
-                    const double2 d = sm.D[m][n];
-                    X[n][m] = make_double2(v.x * d.x - v.y * d.y, v.x * d.y + v.y * d.x);
+            // 1: P[ix'][(s,iy)] = sum_ix Vx[ix][ix'] G_s[ix][iy]  -> W[(s,ix')][iy]
+            Stage<LD, KS>{V1T, X, nx, nb * ny, (nx + 7) / 8, (nb * ny + 7) / 8, q, lane}([&](int m, int n, double2 v) {
+                if (m < nx && n < nb * ny) {
+                    const int s = fdiv(n, inv_ny);
+                    W[(s * nx + m) * LD + n - s * ny] = v;
                 }
             });
             group_sync(grp);
-            // 3: R[ixu][iy'] = sum_ix' Vx[ux0 + ixu][ix'] Q[ix'][iy']  -> W[ixu][iy']
-            stage(sm.V1U, X, MTux, MTy, KSx, q, lane, [&](int m, int n, double2 v) {
-                if (m < c.nux && n < c.ny) W[m][n] = v;
-            });
-            group_sync(grp);
-            // 4: Y[ixu][iyu] = sum_iy' R[ixu][iy'] Vy[uy0 + iyu][iy']  -> staging rows
-            stage(W, sm.V2U, MTux, MTuy, KSy, q, lane, [&](int m, int n, double2 v) {
-                if (m < c.nux && n < c.nuy) {
-                    const int li = int(dof_index(c.onx, c.ony, P, c.ux0 + m, c.uy0 + n));
-                    ystage[(size_t)s * nu_max + c.rowmap[li]] = v;
+            // 2: Q[(s,ix')][iy'] = (sum_iy P[(s,ix')][iy] Vy[iy][iy']) Dinv[ix'][iy']  -> X[(s,iy')][ix']
+            Stage<LD, KS>{W, V2T, nb * nx, ny, (nb * nx + 7) / 8, (ny + 7) / 8, q, lane}([&](int m, int n, double2 v) {
+                if (m < nb * nx && n < ny) {
+                    const int s = fdiv(m, inv_nx), ix = m - s * nx;
+                    const double2 d = D[ix * ny + n];
+                    X[(s * ny + n) * LD + ix] = make_double2(v.x * d.x - v.y * d.y, v.x * d.y + v.y * d.x);
                 }
             });
             group_sync(grp);
-            if (kXBuf == 1 && sp + kGroups < seg_end) gather(sp + kGroups, X);
+            // 3: R[ixu][(s,iy')] = sum_ix' Vx[ux0 + ixu][ix'] Q[(s,iy')][ix']  -> W[(s,ixu)][iy']
+            Stage<LD, KS>{V1U, X, nux, nb * ny, (nux + 7) / 8, (nb * ny + 7) / 8, q, lane}([&](int m, int n, double2 v) {
+                if (m < nux && n < nb * ny) {
+                    const int s = fdiv(n, inv_ny);
+                    W[(s * nux + m) * LD + n - s * ny] = v;
+                }
+            });
+            group_sync(grp);
+            // the gathered tile is free: fetch the group's next batch under stage 4
+            const int nb0 = b0 + kFGroups * S;
+            if (nb0 < seg_end) gather(nb0, min(S, seg_end - nb0), par ^ 1);
+            // 4: Y[(s,ixu)][iyu] = sum_iy' R[(s,ixu)][iy'] Vy[uy0 + iyu][iy']  -> staging rows
+            Stage<LD, KS>{W, V2U, nb * nux, nuy, (nb * nux + 7) / 8, (nuy + 7) / 8, q, lane}(
+                [&](int m, int n, double2 v) {
+                    if (m < nb * nux && n < nuy) {
+                        const int s = fdiv(m, inv_nux), ixu = m - s * nux;
+                        ystage[(size_t)sid[par * 8 + s] * nu_max + urow[ixu * nuy + n]] = v;
+                    }
+                });
+            group_sync(grp);  // W is rewritten by the next batch's stage 1
         }
         asm volatile("cp.async.wait_all;\n" ::: "memory");
         pos = seg_end;
     }
 }
 
+template <int P>
+int fdm_rows(int fac_elems) {
+    return (kSmemMax / int(sizeof(double2)) - fac_elems) / (kFGroups * 2 * FdmDims<P>::LD);
+}
+
 }  // namespace
 
-// One launch for every separable class: CTAs are split over the classes in
-// proportion to their subdomain counts (work table built once, on first use).
+bool fdm_supported(int p, int nx, int ny) {
+    if (p == 2) return nx <= 4 * FdmDims<2>::KS && ny <= 4 * FdmDims<2>::KS;
+    if (p == 4) return nx <= 4 * FdmDims<4>::KS && ny <= 4 * FdmDims<4>::KS;
+    return false;
+}
+
+// One launch for every separable class: CTAs take contiguous ranges of the
+// class-sorted subdomain list (work table built once, fdm_plan).
 void dd_fdm_launch(const FineGeom& g, const FdmLaunch& L, const double2* r, double2* ystage, int nu_max,
                    cudaStream_t st) {
     if (L.nwork == 0) return;
-    const size_t smem = sizeof(FdmSmem);
     static bool attr[9] = {};
     auto go = [&](auto kern, int p) {
         if (!attr[p]) {
-            HTG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            HTG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
             attr[p] = true;
         }
-        kern<<<L.nwork, kFThreads, smem, st>>>(g, L.classes, L.work, r, ystage, nu_max);
+        kern<<<L.nwork, kFThreads, L.smem, st>>>(g, L.classes, L.work, r, ystage, nu_max, L.rows, L.fac_elems);
     };
     switch (g.p) {
         case 2: go(k_dd_fdm<2>, 2); break;
         case 4: go(k_dd_fdm<4>, 4); break;
-        default: throw InvalidArgument("FDM subdomain kernel: p > 4 not supported (1-D extent > 32)");
+        default: throw InvalidArgument("FDM subdomain kernel: p must be 2 or 4");
     }
     HTG_CUDA(cudaGetLastError());
     count_launch();
 }
 
-// Contiguous ranges of the class-sorted subdomain list, one per SM (a CTA may
-// span a class boundary; it reloads the factors per class segment).
-std::vector<int4> fdm_work_table(std::vector<FdmClassDev>& cls, int nsm) {
-    int total = 0;
+// Shared-memory layout (factor region sized for the largest class, two data
+// buffers per group) and contiguous, equal ranges of the class-sorted
+// subdomain list, one per SM.
+std::vector<int4> fdm_plan(std::vector<FdmClassDev>& cls, int p, int nsm, FdmLaunch& L) {
+    const int LD = p == 2 ? FdmDims<2>::LD : FdmDims<4>::LD;
+    int total = 0, fac = 0, ext = 0;
     for (auto& c : cls) {
         c.first = total;
         total += c.nsub;
+        fac = std::max(fac, (c.nx + c.ny + c.nux + c.nuy) * LD + c.nx * c.ny + (kFGroups * 16 + c.nux * c.nuy + 3) / 4);
+        ext = std::max({ext, c.nx, c.ny});
     }
+    fac = (fac + 7) / 8 * 8;
+    L.fac_elems = fac;
+    L.rows = p == 2 ? fdm_rows<2>(fac) : fdm_rows<4>(fac);
+    if (L.rows < ext) throw RuntimeError("FDM subdomain kernel: shared memory too small for the class extents");
+    L.smem = size_t(fac + kFGroups * 2 * L.rows * LD) * sizeof(double2);
     std::vector<int4> work;
     if (total == 0) return work;
-    const int ctas = std::min(nsm, (total + kGroups - 1) / kGroups);
-    const int per = ((total + ctas - 1) / ctas + kGroups - 1) / kGroups * kGroups;
-    for (int s0 = 0; s0 < total; s0 += per) work.push_back(make_int4(s0, std::min(total, s0 + per), 0, 0));
+    const int ctas = std::min(nsm, total);
+    for (int i = 0; i < ctas; ++i) {
+        const int a = int((long long)total * i / ctas), b = int((long long)total * (i + 1) / ctas);
+        if (b > a) work.push_back(make_int4(a, b, 0, 0));
+    }
     return work;
 }
 

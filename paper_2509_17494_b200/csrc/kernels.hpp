@@ -84,12 +84,17 @@ struct FdmClassDev {
 };
 struct FdmLaunch {
     const FdmClassDev* classes;  // device copy of the class table
-    const int4* work;            // per CTA: class, first subdomain, count
+    const int4* work;            // per CTA: [first, end) of the class-sorted subdomain list
     int nwork;
+    int rows;                    // data rows per buffer (S = rows / max(nx, ny) subdomains per batch)
+    int fac_elems;               // factor region (double2) sized for the largest class
+    size_t smem;                 // dynamic shared memory per CTA
 };
 void dd_fdm_launch(const FineGeom& g, const FdmLaunch& L, const double2* r, double2* ystage, int nu_max,
                    cudaStream_t st);
-std::vector<int4> fdm_work_table(std::vector<FdmClassDev>& cls, int nsm);
+std::vector<int4> fdm_plan(std::vector<FdmClassDev>& cls, int p, int nsm, FdmLaunch& L);
+// p and 1-D extents of Omega the FDM kernel takes (others use the dense path)
+bool fdm_supported(int p, int nx, int ny);
 // out = u + sum_i y_i / L in subdomain order (u may be null -> 0); out may alias u
 void dd_combine_launch(const FineGeom& g, const DDDevice& d, const double2* ystage, const double2* u, double2* out,
                        cudaStream_t st);
