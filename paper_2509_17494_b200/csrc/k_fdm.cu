@@ -11,7 +11,10 @@
 // of every product (S = 2 at p = 4 with 4 groups: 50 data rows instead of
 // 2 x 25 padded to 2 x 32). Only the factor dimension is padded to the m8/n8
 // tile, and the contraction to the k4 step: 13% fewer DMMAs than one
-// subdomain per product. Four groups per CTA (one CTA per SM, 16 warps, the
+// subdomain per product. The factor is the stationary operand (its fragments
+// stay in registers across the data tiles); a factor dimension of 8 t + 1 or
+// 8 t + 2 (25 and 17 at p = 4) runs its last rows as DFMA dot products on the
+// CUDA cores instead of a DMMA tile that is 7/8 zeros (-28% DMMAs). Four groups per CTA (one CTA per SM, 16 warps, the
 // whole 227 KB of shared memory) alternate batches of the CTA's range; measured
 // at cfg4: 2 groups x S=4 0.265 ms, 3 x S=2 0.259 ms, 4 x S=2 0.242 ms.
 // Every product is mma.sync.m8n8k4.f64 in the Gauss (3M) form: three real
@@ -73,9 +76,12 @@ constexpr int kKP = HTG_FDM_KSPLIT;  // independent accumulator chains per produ
 
 template <int LD, int KS>
 struct Stage {
-    const double2* A;
-    const double2* B;
-    int am, bn, MT, NT, q, lane;
+    const double2* fac;  // factor operand [F][LD] (zero k padding)
+    int F;               // factor rows (the padded output dimension)
+    const double2* dat;  // data operand [nd][LD]
+    int nd;              // data rows of the batch
+    bool sa;             // the factor is the A operand (C[factor][data]); else B (C[data][factor])
+    int q, lane;
 
     using Acc = double[kKP][4][2];
     template <int NTL, class Epi>
@@ -139,97 +145,88 @@ struct Stage {
         finish<NTL>(t1, t2, t3, tm, tn, epi);
     }
 
-    template <int NTL, class Epi>
-    __device__ __forceinline__ void run_pairs(const int* ar, const int* br, const int* tm, const int* tn,
-                                              Epi& epi) const {
-        Acc t1, t2, t3;
-        zero<NTL>(t1, t2, t3);
-#pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
-            const int h = ks % kKP;
-            double2 a[4], b[4];
-            double as[4], bs[4];
-#pragma unroll
-            for (int j = 0; j < NTL; ++j) {
-                a[j] = A[ar[j] + ks * 4];
-                b[j] = B[br[j] + ks * 4];
-                as[j] = a[j].x + a[j].y;
-                bs[j] = b[j].x + b[j].y;
-            }
-#pragma unroll
-            for (int j = 0; j < NTL; ++j) dmma(t1[h][j][0], t1[h][j][1], a[j].x, b[j].x);
-#pragma unroll
-            for (int j = 0; j < NTL; ++j) dmma(t2[h][j][0], t2[h][j][1], a[j].y, b[j].y);
-#pragma unroll
-            for (int j = 0; j < NTL; ++j) dmma(t3[h][j][0], t3[h][j][1], as[j], bs[j]);
-        }
-        finish<NTL>(t1, t2, t3, tm, tn, epi);
-    }
-
+    // full 8-row tiles ST of the factor on DMMA, the last FR <= 2 factor rows
+    // on the CUDA cores (a padded tile would be 7/8 or 6/8 zeros)
     template <class Epi>
     __device__ __forceinline__ void operator()(Epi&& epi) const {
         const int r = lane >> 2, kq = lane & 3;
-        if ((MT & 3) == 0 || (NT & 3) == 0) {
-            const bool sa = (MT & 3) == 0;
-            const int ST = sa ? MT : NT, OT = sa ? NT : MT;
-            const double2* S = sa ? A : B;
-            const double2* O = sa ? B : A;
-            const int slim = (sa ? am : bn) - 1, olim = (sa ? bn : am) - 1;
-            for (int st = q; st < ST; st += 4) {
-                double2 sf[KS];
-                double ss[KS];
-                const double2* srow = S + min(st * 8 + r, slim) * LD + kq;
-#pragma unroll
-                for (int ks = 0; ks < KS; ++ks) {
-                    sf[ks] = srow[ks * 4];
-                    ss[ks] = sf[ks].x + sf[ks].y;
-                }
-                for (int o0 = 0; o0 < OT; o0 += 4) {
-                    const int nt = min(4, OT - o0);
-                    int mrow[4], tm[4], tn[4];
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        mrow[j] = min((o0 + j) * 8 + r, olim) * LD + kq;
-                        tm[j] = sa ? st : o0 + j;
-                        tn[j] = sa ? o0 + j : st;
-                    }
-                    if (sa) {
-                        switch (nt) {
-                            case 4: run_stat<4, true>(sf, ss, O, mrow, tm, tn, epi); break;
-                            case 3: run_stat<3, true>(sf, ss, O, mrow, tm, tn, epi); break;
-                            case 2: run_stat<2, true>(sf, ss, O, mrow, tm, tn, epi); break;
-                            default: run_stat<1, true>(sf, ss, O, mrow, tm, tn, epi); break;
-                        }
-                    } else {
-                        switch (nt) {
-                            case 4: run_stat<4, false>(sf, ss, O, mrow, tm, tn, epi); break;
-                            case 3: run_stat<3, false>(sf, ss, O, mrow, tm, tn, epi); break;
-                            case 2: run_stat<2, false>(sf, ss, O, mrow, tm, tn, epi); break;
-                            default: run_stat<1, false>(sf, ss, O, mrow, tm, tn, epi); break;
-                        }
-                    }
-                }
-            }
-            return;
+        const int FR = (F & 7) <= 2 ? (F & 7) : 0;
+        const int ST = (F - FR + 7) >> 3, OT = (nd + 7) >> 3;
+        // warp q: stationary tiles st0, st0 + sstep, ..; moving tiles [o_lo, o_hi);
+        // remainder items [i_lo, i_hi) of FR x nd
+        int st0 = q, sstep = 4, o_lo = 0, o_hi = OT, nrem = FR * nd, i_lo = 0, i_hi = 0;
+        if (ST == 3) {
+            if (q == 3) st0 = ST, i_hi = nrem;
+        } else if (ST == 2) {
+            const int h = (OT + 1) >> 1;
+            st0 = q & 1;
+            sstep = 2;
+            o_lo = (q >> 1) ? h : 0;
+            o_hi = (q >> 1) ? OT : h;
+            if (q >= 2) i_lo = (q - 2) * nrem / 2, i_hi = (q - 1) * nrem / 2;
+        } else if (ST == 1) {
+            st0 = 0;
+            sstep = 1 << 30;
+            o_lo = q * OT / 4;
+            o_hi = (q + 1) * OT / 4;
+            i_lo = q * nrem / 4, i_hi = (q + 1) * nrem / 4;
+        } else {
+            i_lo = q * nrem / 4, i_hi = (q + 1) * nrem / 4;
         }
-        const int total = MT * NT;
-        for (int t0 = q; t0 < total; t0 += 16) {
-            const int nt = min(4, (total - t0 + 3) / 4);
-            int tm[4], tn[4], ar[4], br[4];
+        const int flim = F - FR - 1, dlim = nd - 1;
+        for (int st = st0; st < ST; st += sstep) {
+            double2 sf[KS];
+            double ss[KS];
+            const double2* srow = fac + min(st * 8 + r, flim) * LD + kq;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int t = min(t0 + 4 * j, total - 1);
-                tm[j] = t % MT;
-                tn[j] = t / MT;
-                ar[j] = min(tm[j] * 8 + r, am - 1) * LD + kq;
-                br[j] = min(tn[j] * 8 + r, bn - 1) * LD + kq;
+            for (int ks = 0; ks < KS; ++ks) {
+                sf[ks] = srow[ks * 4];
+                ss[ks] = sf[ks].x + sf[ks].y;
             }
-            switch (nt) {
-                case 4: run_pairs<4>(ar, br, tm, tn, epi); break;
-                case 3: run_pairs<3>(ar, br, tm, tn, epi); break;
-                case 2: run_pairs<2>(ar, br, tm, tn, epi); break;
-                default: run_pairs<1>(ar, br, tm, tn, epi); break;
+            for (int o0 = o_lo; o0 < o_hi; o0 += 4) {
+                const int nt = min(4, o_hi - o0);
+                int mrow[4], tm[4], tn[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    mrow[j] = min((o0 + j) * 8 + r, dlim) * LD + kq;
+                    tm[j] = sa ? st : o0 + j;
+                    tn[j] = sa ? o0 + j : st;
+                }
+                if (sa) {
+                    switch (nt) {
+                        case 4: run_stat<4, true>(sf, ss, dat, mrow, tm, tn, epi); break;
+                        case 3: run_stat<3, true>(sf, ss, dat, mrow, tm, tn, epi); break;
+                        case 2: run_stat<2, true>(sf, ss, dat, mrow, tm, tn, epi); break;
+                        default: run_stat<1, true>(sf, ss, dat, mrow, tm, tn, epi); break;
+                    }
+                } else {
+                    switch (nt) {
+                        case 4: run_stat<4, false>(sf, ss, dat, mrow, tm, tn, epi); break;
+                        case 3: run_stat<3, false>(sf, ss, dat, mrow, tm, tn, epi); break;
+                        case 2: run_stat<2, false>(sf, ss, dat, mrow, tm, tn, epi); break;
+                        default: run_stat<1, false>(sf, ss, dat, mrow, tm, tn, epi); break;
+                    }
+                }
             }
+        }
+        // remainder: one complex dot product of a factor row and a data row per
+        // lane; k is xor-skewed by the data row so 8 lanes hit distinct banks
+        for (int it = i_lo + lane; it < i_hi; it += 32) {
+            const int f = it / nd, d = it - f * nd;
+            const double2* fr = fac + (F - FR + f) * LD;
+            const double2* dr = dat + d * LD;
+            const int sk = d & 3;
+            double re = 0.0, im = 0.0;
+#pragma unroll
+            for (int kk = 0; kk < 4 * KS; ++kk) {
+                const double2 a = fr[kk ^ sk], b = dr[kk ^ sk];
+                re = fma(a.x, b.x, re);
+                re = fma(-a.y, b.y, re);
+                im = fma(a.x, b.y, im);
+                im = fma(a.y, b.x, im);
+            }
+            if (sa) epi(F - FR + f, d, make_double2(re, im));
+            else epi(d, F - FR + f, make_double2(re, im));
         }
     }
 };
@@ -310,7 +307,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_dd_fdm(FineGeom g, const FdmCl
             asm volatile("cp.async.wait_all;\n" ::: "memory");
             group_sync(grp);
             // 1: P[ix'][(s,iy)] = sum_ix Vx[ix][ix'] G_s[ix][iy]  -> W[(s,ix')][iy]
-            Stage<LD, KS>{V1T, X, nx, nb * ny, (nx + 7) / 8, (nb * ny + 7) / 8, q, lane}([&](int m, int n, double2 v) {
+            Stage<LD, KS>{V1T, nx, X, nb * ny, true, q, lane}([&](int m, int n, double2 v) {
                 if (m < nx && n < nb * ny) {
                     const int s = fdiv(n, inv_ny);
                     W[(s * nx + m) * LD + n - s * ny] = v;
@@ -318,7 +315,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_dd_fdm(FineGeom g, const FdmCl
             });
             group_sync(grp);
             // 2: Q[(s,ix')][iy'] = (sum_iy P[(s,ix')][iy] Vy[iy][iy']) Dinv[ix'][iy']  -> X[(s,iy')][ix']
-            Stage<LD, KS>{W, V2T, nb * nx, ny, (nb * nx + 7) / 8, (ny + 7) / 8, q, lane}([&](int m, int n, double2 v) {
+            Stage<LD, KS>{V2T, ny, W, nb * nx, false, q, lane}([&](int m, int n, double2 v) {
                 if (m < nb * nx && n < ny) {
                     const int s = fdiv(m, inv_nx), ix = m - s * nx;
                     const double2 d = D[ix * ny + n];
@@ -327,7 +324,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_dd_fdm(FineGeom g, const FdmCl
             });
             group_sync(grp);
             // 3: R[ixu][(s,iy')] = sum_ix' Vx[ux0 + ixu][ix'] Q[(s,iy')][ix']  -> W[(s,ixu)][iy']
-            Stage<LD, KS>{V1U, X, nux, nb * ny, (nux + 7) / 8, (nb * ny + 7) / 8, q, lane}([&](int m, int n, double2 v) {
+            Stage<LD, KS>{V1U, nux, X, nb * ny, true, q, lane}([&](int m, int n, double2 v) {
                 if (m < nux && n < nb * ny) {
                     const int s = fdiv(n, inv_ny);
                     W[(s * nux + m) * LD + n - s * ny] = v;
@@ -338,7 +335,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_dd_fdm(FineGeom g, const FdmCl
             const int nb0 = b0 + kFGroups * S;
             if (nb0 < seg_end) gather(nb0, min(S, seg_end - nb0), par ^ 1);
             // 4: Y[(s,ixu)][iyu] = sum_iy' R[(s,ixu)][iy'] Vy[uy0 + iyu][iy']  -> staging rows
-            Stage<LD, KS>{W, V2U, nb * nux, nuy, (nb * nux + 7) / 8, (nuy + 7) / 8, q, lane}(
+            Stage<LD, KS>{V2U, nuy, W, nb * nux, false, q, lane}(
                 [&](int m, int n, double2 v) {
                     if (m < nb * nux && n < nuy) {
                         const int s = fdiv(m, inv_nux), ixu = m - s * nux;
