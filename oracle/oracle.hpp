@@ -11,7 +11,7 @@
 // cannot be built here (Eigen3, doctest and CLI11 are absent), see DESIGN.md.
 //
 // Scope: square elements on rectangle meshes (every BASELINE config), the
-// OptimizedFD (QSFEM) coarse level, CSDD and ExactShifted smoothers,
+// OptimizedFD (QSFEM) and GalerkinP coarse levels, CSDD and ExactShifted smoothers,
 // Richardson and GMRES outer loops. Eigen's sparse products become CSR
 // products, Eigen SparseLU becomes a banded LU with partial pivoting.
 #pragma once

@@ -312,7 +312,33 @@ std::unique_ptr<Ops> setup_two_grid(const Space& s, const Coeffs& c, const Tags&
         ops->IP = build_prolongation(s, ops->cspace, s.dirichlet_dofs(t), ops->cspace.dirichlet_dofs(ct));
         ops->Ac_factor = std::make_unique<BandLU>(ops->Ac);
     } else if (cfg.coarsening == Coarse::GalerkinP) {
-        throw std::invalid_argument("oracle: GalerkinP coarsening is not restated yet");
+        // proj/core/src/twogrid.cpp:189-219 (galerkin_p_coarse): the order-p/2 space on
+        // the same mesh, its Helmholtz matrix with alpha_c, and IP = the inclusion of the
+        // hierarchical order-p/2 functions among the order-p ones
+        const int p = s.p;
+        if (p % 2 != 0) throw std::invalid_argument("galerkin_p_coarse: order must be even");
+        const int pc = p / 2;
+        ops->crect = s.r;
+        ops->cspace = Space::build(s.r, pc);
+        ops->ccoeffs = c;
+        ops->ctags = t;
+        ops->Ac = assemble_helmholtz(ops->cspace, c, t, cfg.alpha_c);
+        std::vector<char> fdir(s.ndof, 0), cdir(ops->cspace.ndof, 0);
+        for (int d : s.dirichlet_dofs(t)) fdir[d] = 1;
+        for (int d : ops->cspace.dirichlet_dofs(t)) cdir[d] = 1;
+        std::vector<Trip> trips;
+        for (int ci = 0; ci < ops->cspace.ndof; ++ci) {
+            Space::Key k = ops->cspace.keys[ci];
+            if (k.kind == 'c') {  // interior index (dx-2)(pc-1)+(dy-2) -> (dx-2)(p-1)+(dy-2)
+                const int dx = k.off / std::max(pc - 1, 1), dy = k.off % std::max(pc - 1, 1);
+                k.off = dx * (p - 1) + dy;
+            }
+            const int fi = s.find(k);  // edge offsets carry over as-is
+            if (fi < 0) throw std::logic_error("galerkin_p_coarse: missing fine dof for inclusion");
+            if (!fdir[fi] && !cdir[ci]) trips.push_back({fi, ci, cplx(1.0, 0.0)});
+        }
+        ops->IP = Csr::from_triplets(s.ndof, ops->cspace.ndof, trips);
+        ops->Ac_factor = std::make_unique<BandLU>(ops->Ac);
     }
     return ops;
 }

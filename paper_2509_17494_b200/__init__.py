@@ -6,7 +6,8 @@ the reference's two-grid interface.
 """
 from ._lib import HtgError, build  # noqa: F401
 from .twogrid import (  # noqa: F401
-    ABSORBING, BOTTOM, CSDD, DIRICHLET, KRYLOV, LEFT, NEUMANN, OPTIMIZED_FD, RICHARDSON, RIGHT, TOP,
+    ABSORBING, BOTTOM, CSDD, DIRICHLET, EXACT_SHIFTED, GALERKIN_P, KRYLOV, LEFT, NEUMANN, NONE, OPTIMIZED_FD,
+    RICHARDSON, RIGHT, TOP,
     Problem, ProblemSpec, SolveResult, SolverConfig, TwoGridOperators, build_problem, dirichlet_mask,
     dof_index, fp64_tensor_peak_tflops, launch_count, reset_launch_count, setup_two_grid,
 )

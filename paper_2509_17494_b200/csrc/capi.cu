@@ -115,6 +115,12 @@ struct htg_handle {
     long long fdm_subs = 0;       // subdomains solved by fast diagonalisation
     // coarse solver
     std::unique_ptr<CoarseSolver> coarse;
+    // GalerkinP: inclusion map (coarse dof -> fine dof, -1 Dirichlet) and A_c (CSR)
+    int* cmap = nullptr;
+    int *ac_rp = nullptr, *ac_ci = nullptr;
+    double2* ac_v = nullptr;
+    // ExactShifted smoother: direct solver of the fine shifted operator A_s
+    std::unique_ptr<CoarseSolver> fine;
     // pinned host scalars
     double* hscal = nullptr;
     // CUDA graphs of the launch sequences, keyed by (kind, u, f); replayed on
@@ -136,6 +142,7 @@ struct htg_handle {
         if (ev_in) cudaEventDestroy(ev_in);
         if (ev_out) cudaEventDestroy(ev_out);
         coarse.reset();
+        fine.reset();
         if (hscal) cudaFreeHost(hscal);
         if (own_stream && st) cudaStreamDestroy(st);
     }
@@ -229,6 +236,31 @@ void build_handle(htg_handle* H, const htg_problem& prob, const htg_config& cfg)
         }
     }
     if (cfg.coarsening == HTG_COARSE_OPTIMIZED_FD) H->coarse = make_coarse_solver(hp, st);
+    if (cfg.coarsening == HTG_COARSE_GALERKIN_P) {
+        // proj/core/src/twogrid.cpp:189-219: order-p/2 space on the same mesh, A_c with
+        // alpha_c, IP = inclusion of the hierarchical order-p/2 functions
+        const int q = hp.p / 2;
+        const LatticeMatrix Ac = fe_lattice(hp, H->basis, q, cfg.alpha_c);
+        std::vector<int> map(size_t(H->cndof), -1);
+        const std::vector<char> fdir = fe_dirichlet(hp, hp.p), cdir = fe_dirichlet(hp, q);
+        const int Wf = hp.nx * hp.p + 1;
+        for (int Y = 0; Y < Ac.H; ++Y)
+            for (int X = 0; X < Ac.W; ++X) {
+                const int gx = X / q * hp.p + X % q, gy = Y / q * hp.p + Y % q;  // same function, order-p index
+                if (cdir[Y * Ac.W + X] || fdir[size_t(gy) * Wf + gx]) continue;
+                map[Ac.id[Y * Ac.W + X]] = int(dof_index(hp.nx, hp.ny, hp.p, gx, gy));
+            }
+        H->cmap = M.upload(map, st);
+        std::vector<double2> av(Ac.v.size());
+        for (size_t i = 0; i < av.size(); ++i) av[i] = make_double2(Ac.v[i].real(), Ac.v[i].imag());
+        // CSR rows are lattice-independent unknowns already (Ac.id order)
+        H->ac_rp = M.upload(Ac.rp, st);
+        H->ac_ci = M.upload(Ac.ci, st);
+        H->ac_v = M.upload(av, st);
+        H->coarse = make_nd_solver(Ac, st);
+    }
+    if (cfg.smoother == HTG_SMOOTHER_EXACT_SHIFTED)  // u += A_s^-1 (f - A u), twogrid.cpp:261-262
+        H->fine = make_nd_solver(fe_lattice(hp, H->basis, hp.p, cfg.alpha_s), st);
     HTG_CUDA(cudaStreamCreateWithFlags(&H->cap, cudaStreamNonBlocking));
     HTG_CUDA(cudaEventCreateWithFlags(&H->ev_in, cudaEventDisableTiming));
     HTG_CUDA(cudaEventCreateWithFlags(&H->ev_out, cudaEventDisableTiming));
@@ -302,9 +334,24 @@ void residual_norm2(htg_handle* H, const double2* f, const double2* u, int slot)
 }
 
 void residual_restrict(htg_handle* H, const double2* f, const double2* u, double2* rc) {
+    if (H->cfg.coarsening == HTG_COARSE_GALERKIN_P) {
+        residual(H, f, u, H->r, 0);
+        inclusion_restrict_launch(H->r, H->cmap, H->cndof, rc, H->st);
+        return;
+    }
     K1Args a = k1args(H, f, u, 0);
     a.rc = rc;
     k1_launch(kK1Restrict, a, H->st);
+}
+
+void prolong_add(htg_handle* H, double2* u, const double2* uc, double omega) {
+    if (H->cfg.coarsening == HTG_COARSE_GALERKIN_P) inclusion_prolong_launch(u, H->cmap, H->cndof, uc, omega, H->st);
+    else prolong_add_launch(H->g, u, uc, omega, H->st);
+}
+
+void coarse_apply(htg_handle* H, const double2* x, double2* y) {
+    if (H->cfg.coarsening == HTG_COARSE_GALERKIN_P) csr_apply_launch(H->ac_rp, H->ac_ci, H->ac_v, H->cndof, x, y, H->st);
+    else coarse_apply_launch(H->g, H->qtab, 0.0, x, y, H->st);
 }
 
 // all subdomain solves of a sweep: dense classes as one batched GEMM, separable
@@ -339,14 +386,25 @@ void csdd(htg_handle* H, double2* u, const double2* f) {
     vec_axpy(u, H->v, 1.0, H->ndof, H->st);
 }
 
+// smooth (proj/core/src/twogrid.cpp:257-264): CSDD sweep, or u += A_s^-1 (f - A u)
+void smooth(htg_handle* H, double2* u, const double2* f) {
+    if (H->cfg.smoother == HTG_SMOOTHER_CSDD) {
+        csdd(H, u, f);
+        return;
+    }
+    residual(H, f, u, H->r, 0);
+    H->fine->solve(H->r, H->v, H->st);
+    vec_axpy(u, H->v, 1.0, H->ndof, H->st);
+}
+
 void two_grid_step(htg_handle* H, double2* u, const double2* f) {
-    for (int i = 0; i < H->cfg.n_s; ++i) csdd(H, u, f);
+    for (int i = 0; i < H->cfg.n_s; ++i) smooth(H, u, f);
     if (H->cfg.coarsening != HTG_COARSE_NONE) {
         residual_restrict(H, f, u, H->rc);
         H->coarse->solve(H->rc, H->uc, H->st);
-        prolong_add_launch(H->g, u, H->uc, H->cfg.omega_c, H->st);
+        prolong_add(H, u, H->uc, H->cfg.omega_c);
     }
-    for (int i = 0; i < H->cfg.n_s; ++i) csdd(H, u, f);
+    for (int i = 0; i < H->cfg.n_s; ++i) smooth(H, u, f);
 }
 
 double host_norm2(htg_handle* H, int slot) {
@@ -555,7 +613,8 @@ int htg_info(const htg_handle* h, long long* out) {
         out[1] = h->cndof;
         out[2] = h->dd.nsub;
         out[3] = h->nclasses;
-        out[4] = (long long)h->mem.bytes + (h->coarse ? h->coarse->device_bytes() : 0);
+        out[4] = (long long)h->mem.bytes + (h->coarse ? h->coarse->device_bytes() : 0) +
+                 (h->fine ? h->fine->device_bytes() : 0);
         out[5] = h->coarse ? h->coarse->device_bytes() : 0;
         out[6] = h->hp.nx;
         out[7] = h->hp.ny;
@@ -605,6 +664,7 @@ int htg_csdd_smoother(htg_handle* h, double* u, const double* f) {
 
 int htg_restrict(htg_handle* h, const double* r, double* rc) {
     return guard([&] {
+        if (!h->coarse) throw InvalidArgument("handle has no coarse level");
         // IP^H r = restriction of the residual f - A u with u = 0, f = r
         vec_zero(h->tmp, h->ndof, h->st);
         residual_restrict(h, CD2(r), h->tmp, D2(rc));
@@ -612,15 +672,24 @@ int htg_restrict(htg_handle* h, const double* r, double* rc) {
 }
 
 int htg_residual_restrict(htg_handle* h, const double* f, const double* u, double* rc) {
-    return guard([&] { residual_restrict(h, CD2(f), CD2(u), D2(rc)); });
+    return guard([&] {
+        if (!h->coarse) throw InvalidArgument("handle has no coarse level");
+        residual_restrict(h, CD2(f), CD2(u), D2(rc));
+    });
 }
 
 int htg_prolong_add(htg_handle* h, double* u, const double* uc, double omega) {
-    return guard([&] { prolong_add_launch(h->g, D2(u), CD2(uc), omega, h->st); });
+    return guard([&] {
+        if (!h->coarse) throw InvalidArgument("handle has no coarse level");
+        prolong_add(h, D2(u), CD2(uc), omega);
+    });
 }
 
 int htg_coarse_apply(htg_handle* h, const double* x, double* y) {
-    return guard([&] { coarse_apply_launch(h->g, h->qtab, 0.0, CD2(x), D2(y), h->st); });
+    return guard([&] {
+        if (!h->coarse) throw InvalidArgument("handle has no coarse level");
+        coarse_apply(h, CD2(x), D2(y));
+    });
 }
 
 int htg_coarse_solve(htg_handle* h, const double* rc, double* uc) {
@@ -700,11 +769,11 @@ int htg_profile(htg_handle* h, double* u, const double* f, int reps, double* ms)
         ms[2] = timeit([&] { dd_combine_launch(h->g, h->dd, h->ystage, U, h->v, h->st); });
         ms[3] = h->coarse ? timeit([&] { residual_restrict(h, Fv, U, h->rc); }) : 0.0;
         ms[4] = h->coarse ? timeit([&] { h->coarse->solve(h->rc, h->uc, h->st); }) : 0.0;
-        ms[5] = h->coarse ? timeit([&] { prolong_add_launch(h->g, h->v, h->uc, 1.0, h->st); }) : 0.0;
+        ms[5] = h->coarse ? timeit([&] { prolong_add(h, h->v, h->uc, 1.0); }) : 0.0;
         ms[6] = timeit([&] { residual_norm2(h, Fv, U, 0); });
         ms[7] = timeit([&] { csdd(h, U, Fv); });
         ms[8] = timeit([&] { two_grid_step(h, U, Fv); });
-        ms[9] = h->coarse ? timeit([&] { coarse_apply_launch(h->g, h->qtab, 0.0, h->rc, h->uc, h->st); }) : 0.0;
+        ms[9] = h->coarse ? timeit([&] { coarse_apply(h, h->rc, h->uc); }) : 0.0;
         // graph replays of the same sequences
         ms[10] = timeit([&] { run_graph(h, 1, U, Fv, [&] { csdd(h, U, Fv); }); });
         ms[11] = timeit([&] { run_graph(h, 2, U, Fv, [&] { two_grid_step(h, U, Fv); }); });

@@ -273,11 +273,11 @@ __global__ void __launch_bounds__(kCT) k_nd_bwd(const Task* tasks, NDArgs a) {
 
 class NDSolver : public CoarseSolver {
   public:
-    NDSolver(const HostProblem& hp, cudaStream_t st) {
+    NDSolver(const LatticeMatrix& A, cudaStream_t st) {
         NDTree t;
         const char* pt = std::getenv("HTG_ND_PIVTOL");
-        nd_factor(hp, t, env_int("HTG_ND_LEAF", 16), pt ? std::atof(pt) : 0.3);
-        nv_ = (t.CX + 1) * (t.CY + 1);
+        nd_factor(A, t, env_int("HTG_ND_LEAF", 16), pt ? std::atof(pt) : 0.3);
+        nv_ = t.nv;
         delayed_ = t.delayed;
         upload(t, st);
     }
@@ -494,8 +494,12 @@ class NDSolver : public CoarseSolver {
 
 }  // namespace
 
+std::unique_ptr<CoarseSolver> make_nd_solver(const LatticeMatrix& A, cudaStream_t st) {
+    return std::make_unique<NDSolver>(A, st);
+}
+
 std::unique_ptr<CoarseSolver> make_coarse_solver(const HostProblem& hp, cudaStream_t st) {
-    return std::make_unique<NDSolver>(hp, st);
+    return make_nd_solver(qsfem_lattice(hp), st);
 }
 
 }  // namespace htg

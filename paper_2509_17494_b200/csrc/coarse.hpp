@@ -37,6 +37,32 @@ std::unique_ptr<CoarseSolver> make_coarse_solver(const HostProblem& hp, cudaStre
 // in the coarse p=1 vertex numbering (Y*(CX+1) + X), Dirichlet eliminated.
 std::vector<cplx> coarse_stencil(const HostProblem& hp);
 
+// ------------------------------------------------------------------ lattice matrices
+// A sparse matrix with one unknown per node of a W x H lattice. The nested
+// dissection cuts along lattice lines X % q == 0 (Y % q == 0): q = 1 for the
+// 9-point QSFEM lattice; for an order-q FE space on the fine mesh a line of
+// element-boundary nodes (vertices and edge functions of one mesh line)
+// separates the cells on its two sides.
+struct LatticeMatrix {
+    int W = 0, H = 0, q = 1;
+    std::vector<int> id;      // node Y * W + X -> unknown (row) index
+    std::vector<int> rp, ci;  // CSR over unknowns, columns sorted
+    std::vector<cplx> v;
+    cplx at(int i, int j) const;
+};
+// the QSFEM coarse matrix on the (n m + 1)^2 vertex lattice (lexicographic unknowns)
+LatticeMatrix qsfem_lattice(const HostProblem& hp);
+// the order-q Helmholtz matrix A = sum_cells [K_e - (k^2 (1 + i alpha) + i eps) h^2 M_e]
+// - sum_{absorbing edges} i k h m_e on the fine mesh, unknowns in the reference
+// dof numbering of the order-q space, Dirichlet rows / columns replaced by the
+// identity (proj/core/src/fespace.cpp:181-210,246-258). The order-q hierarchical
+// functions are the first q + 1 of the order-p family, so the element factors
+// are the leading blocks of the 1-D M, S.
+LatticeMatrix fe_lattice(const HostProblem& hp, const Basis1D& b, int q, double alpha);
+// per node (Y W + X) of the order-q lattice: on the closure of a Dirichlet edge
+// (proj/core/src/fespace.cpp:146-153)
+std::vector<char> fe_dirichlet(const HostProblem& hp, int q);
+
 // ------------------------------------------------------------------ nested dissection
 // Geometric nested dissection of the coarse vertex lattice. Each front is
 // factored by LU with threshold partial pivoting inside its pivot block;
@@ -57,14 +83,17 @@ struct NDNode {
     std::vector<cplx> Finv, L21, Uinv, Z, S;  // factor blocks (host, freed after upload)
 };
 struct NDTree {
-    int CX = 0, CY = 0;
+    int W = 0, H = 0, q = 1, nv = 0;
     std::vector<NDNode> nodes;  // postorder: children before parents, root last
     int max_depth = 0;
     long long delayed = 0;  // pivots delayed to an ancestor (summed over nodes)
     int max_front = 0;
 };
-// Build and factor the tree. leaf_max: vertices per leaf box; pivtol: the
+// Build and factor the tree. leaf_max: nodes per leaf box; pivtol: the
 // threshold-pivoting tolerance in (0, 1] (0 = plain partial pivoting inside the block).
-void nd_factor(const HostProblem& hp, NDTree& t, int leaf_max, double pivtol);
+void nd_factor(const LatticeMatrix& A, NDTree& t, int leaf_max, double pivtol);
+// the GPU direct solver of a lattice matrix (coarse.cu); make_coarse_solver is
+// make_nd_solver(qsfem_lattice(hp))
+std::unique_ptr<CoarseSolver> make_nd_solver(const LatticeMatrix& A, cudaStream_t st);
 
 }  // namespace htg

@@ -100,10 +100,153 @@ std::vector<cplx> coarse_stencil(const HostProblem& hp) {
     return A9;
 }
 
+// ------------------------------------------------------------------ lattice matrices
+cplx LatticeMatrix::at(int i, int j) const {
+    const auto b = ci.begin() + rp[i], e = ci.begin() + rp[i + 1];
+    const auto it = std::lower_bound(b, e, j);
+    return (it != e && *it == j) ? v[size_t(it - ci.begin())] : cplx(0.0);
+}
+
+namespace {
+// CSR from per-row (col, value) lists: sort, sum duplicates
+void finish_csr(LatticeMatrix& L, std::vector<std::vector<std::pair<int, cplx>>>& rows) {
+    const int n = int(rows.size());
+    L.rp.assign(n + 1, 0);
+    L.ci.clear();
+    L.v.clear();
+    for (int i = 0; i < n; ++i) {
+        auto& r = rows[i];
+        std::sort(r.begin(), r.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+        for (size_t k = 0; k < r.size(); ++k) {
+            if (!L.ci.empty() && int(L.ci.size()) > L.rp[i] && L.ci.back() == r[k].first) {
+                L.v.back() += r[k].second;
+            } else {
+                L.ci.push_back(r[k].first);
+                L.v.push_back(r[k].second);
+            }
+        }
+        L.rp[i + 1] = int(L.ci.size());
+        std::vector<std::pair<int, cplx>>().swap(r);
+    }
+}
+}  // namespace
+
+LatticeMatrix qsfem_lattice(const HostProblem& hp) {
+    const int m = hp.p / 2;
+    LatticeMatrix L;
+    L.W = hp.nx * m + 1;
+    L.H = hp.ny * m + 1;
+    L.q = 1;
+    const int nv = L.W * L.H;
+    L.id.resize(nv);
+    for (int i = 0; i < nv; ++i) L.id[i] = i;
+    const std::vector<cplx> A9 = coarse_stencil(hp);
+    std::vector<std::vector<std::pair<int, cplx>>> rows(nv);
+    for (int Y = 0; Y < L.H; ++Y)
+        for (int X = 0; X < L.W; ++X)
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                    const int WX = X + dx, WY = Y + dy;
+                    if (WX < 0 || WX >= L.W || WY < 0 || WY >= L.H) continue;
+                    const cplx a = A9[(size_t(Y) * L.W + X) * 9 + (dy + 1) * 3 + (dx + 1)];
+                    if (a != cplx(0.0)) rows[Y * L.W + X].push_back({WY * L.W + WX, a});
+                }
+    finish_csr(L, rows);
+    return L;
+}
+
+std::vector<char> fe_dirichlet(const HostProblem& hp, int q) {
+    const int W = hp.nx * q + 1, H = hp.ny * q + 1;
+    std::vector<char> d(size_t(W) * H, 0);
+    if (!hp.has_dirichlet) return d;
+    for (int cx = 0; cx < hp.nx; ++cx)
+        for (int j = 0; j <= q; ++j) {
+            if (hp.tb[cx] == kDirichlet) d[cx * q + j] = 1;
+            if (hp.tt[cx] == kDirichlet) d[size_t(H - 1) * W + cx * q + j] = 1;
+        }
+    for (int cy = 0; cy < hp.ny; ++cy)
+        for (int j = 0; j <= q; ++j) {
+            if (hp.tl[cy] == kDirichlet) d[size_t(cy * q + j) * W] = 1;
+            if (hp.tr[cy] == kDirichlet) d[size_t(cy * q + j) * W + W - 1] = 1;
+        }
+    return d;
+}
+
+LatticeMatrix fe_lattice(const HostProblem& hp, const Basis1D& b, int q, double alpha) {
+    if (q < 1 || q > hp.p) throw InvalidArgument("fe_lattice: order must lie in [1, p]");
+    LatticeMatrix L;
+    L.W = hp.nx * q + 1;
+    L.H = hp.ny * q + 1;
+    L.q = q;
+    const int nv = L.W * L.H;
+    L.id.resize(nv);
+    for (int Y = 0; Y < L.H; ++Y)
+        for (int X = 0; X < L.W; ++X) L.id[Y * L.W + X] = int(dof_index(hp.nx, hp.ny, q, X, Y));
+    // 1-D local index a (0, 1: vertices, >= 2: bubble of degree a) -> lattice offset in the cell
+    auto off = [&](int a) { return a == 0 ? 0 : (a == 1 ? q : a - 1); };
+    const int B = q + 1;
+    std::vector<std::vector<std::pair<int, cplx>>> rows(nv);
+    auto dof = [&](int cx, int cy, int a, int c) { return L.id[(cy * q + off(c)) * L.W + cx * q + off(a)]; };
+    const double h2 = hp.h * hp.h;
+    for (int cy = 0; cy < hp.ny; ++cy)
+        for (int cx = 0; cx < hp.nx; ++cx) {
+            const double k = hp.kc(cx, cy), e = hp.ec(cx, cy);
+            const cplx m = cplx(k * k, k * k * alpha + e) * h2;
+            for (int ay = 0; ay < B; ++ay)
+                for (int ax = 0; ax < B; ++ax) {
+                    auto& row = rows[dof(cx, cy, ax, ay)];
+                    for (int cy2 = 0; cy2 < B; ++cy2)
+                        for (int cx2 = 0; cx2 < B; ++cx2) {
+                            const double mm = b.M[ax][cx2] * b.M[ay][cy2];
+                            const double kk = b.S[ax][cx2] * b.M[ay][cy2] + b.M[ax][cx2] * b.S[ay][cy2];
+                            const cplx a = kk - m * mm;
+                            if (a != cplx(0.0)) row.push_back({dof(cx, cy, cx2, cy2), a});
+                        }
+                }
+        }
+    // Robin edges: - i k h times the 1-D mass along the edge
+    auto robin = [&](int cx, int cy, bool horiz, int side_local, double kh) {
+        if (kh == 0.0) return;
+        for (int a = 0; a < B; ++a)
+            for (int c = 0; c < B; ++c) {
+                const cplx val(0.0, -kh * b.M[a][c]);
+                if (horiz) rows[dof(cx, cy, a, side_local)].push_back({dof(cx, cy, c, side_local), val});
+                else rows[dof(cx, cy, side_local, a)].push_back({dof(cx, cy, side_local, c), val});
+            }
+    };
+    for (int cx = 0; cx < hp.nx; ++cx) {
+        robin(cx, 0, true, 0, hp.khb[cx]);
+        robin(cx, hp.ny - 1, true, 1, hp.kht[cx]);
+    }
+    for (int cy = 0; cy < hp.ny; ++cy) {
+        robin(0, cy, false, 0, hp.khl[cy]);
+        robin(hp.nx - 1, cy, false, 1, hp.khr[cy]);
+    }
+    finish_csr(L, rows);
+    if (hp.has_dirichlet) {  // closures of Dirichlet edges -> identity rows and columns
+        const std::vector<char> dn = fe_dirichlet(hp, q);
+        std::vector<char> dir(nv, 0);
+        for (int i = 0; i < nv; ++i) dir[L.id[i]] = dn[i];
+        for (int i = 0; i < nv; ++i)
+            for (int k = L.rp[i]; k < L.rp[i + 1]; ++k)
+                if (dir[i] || dir[L.ci[k]]) L.v[k] = L.ci[k] == i ? cplx(1.0) : cplx(0.0);
+    }
+    return L;
+}
+
 // ------------------------------------------------------------------ nested dissection
 namespace {
 
-int build_nd(NDTree& t, int x0, int x1, int y0, int y1, int depth, int leaf_max) {
+// a separator line strictly inside [a0, a1] on the stride-q grid, nearest the middle, or -1
+int pick_line(int a0, int a1, int q) {
+    const int mid = (a0 + a1) / 2;
+    int best = -1;
+    for (int c = (a0 / q + 1) * q; c < a1; c += q)
+        if (c > a0 && (best < 0 || std::abs(c - mid) < std::abs(best - mid))) best = c;
+    return best;
+}
+
+int build_nd(NDTree& t, const LatticeMatrix& A, int x0, int x1, int y0, int y1, int depth, int leaf_max) {
     NDNode n;
     n.x0 = x0;
     n.x1 = x1;
@@ -111,27 +254,31 @@ int build_nd(NDTree& t, int x0, int x1, int y0, int y1, int depth, int leaf_max)
     n.y1 = y1;
     n.depth = depth;
     const int w = x1 - x0 + 1, h = y1 - y0 + 1;
+    const auto node = [&](int x, int y) { return A.id[y * A.W + x]; };
     std::vector<int> kids;
-    if (w * h <= leaf_max || std::max(w, h) < 3) {
+    const int xl = pick_line(x0, x1, A.q), yl = pick_line(y0, y1, A.q);
+    const bool sx = xl >= 0 && (w >= h || yl < 0), sy = !sx && yl >= 0;  // cut the longer side if it can be cut
+    const int xm = sx ? xl : -1, ym = sy ? yl : -1;
+    if (w * h <= leaf_max || (!sx && !sy)) {
         n.leaf = true;
         for (int y = y0; y <= y1; ++y)
-            for (int x = x0; x <= x1; ++x) n.vars.push_back(y * (t.CX + 1) + x);
-    } else if (w >= h) {
-        const int xm = (x0 + x1) / 2;
-        kids.push_back(build_nd(t, x0, xm - 1, y0, y1, depth + 1, leaf_max));
-        kids.push_back(build_nd(t, xm + 1, x1, y0, y1, depth + 1, leaf_max));
-        for (int y = y0; y <= y1; ++y) n.vars.push_back(y * (t.CX + 1) + xm);
+            for (int x = x0; x <= x1; ++x) n.vars.push_back(node(x, y));
+    } else if (xm >= 0) {
+        kids.push_back(build_nd(t, A, x0, xm - 1, y0, y1, depth + 1, leaf_max));
+        kids.push_back(build_nd(t, A, xm + 1, x1, y0, y1, depth + 1, leaf_max));
+        for (int y = y0; y <= y1; ++y) n.vars.push_back(node(xm, y));
     } else {
-        const int ym = (y0 + y1) / 2;
-        kids.push_back(build_nd(t, x0, x1, y0, ym - 1, depth + 1, leaf_max));
-        kids.push_back(build_nd(t, x0, x1, ym + 1, y1, depth + 1, leaf_max));
-        for (int x = x0; x <= x1; ++x) n.vars.push_back(ym * (t.CX + 1) + x);
+        kids.push_back(build_nd(t, A, x0, x1, y0, ym - 1, depth + 1, leaf_max));
+        kids.push_back(build_nd(t, A, x0, x1, ym + 1, y1, depth + 1, leaf_max));
+        for (int x = x0; x <= x1; ++x) n.vars.push_back(node(x, ym));
     }
+    // box edges lie next to separator lines (or the domain boundary), so every
+    // coupling of the box leaves it through the one-node frame
     for (int y = y0 - 1; y <= y1 + 1; ++y)
         for (int x = x0 - 1; x <= x1 + 1; ++x) {
-            if (x < 0 || y < 0 || x > t.CX || y > t.CY) continue;
+            if (x < 0 || y < 0 || x >= A.W || y >= A.H) continue;
             if (x >= x0 && x <= x1 && y >= y0 && y <= y1) continue;
-            n.ring.push_back(y * (t.CX + 1) + x);
+            n.ring.push_back(node(x, y));
         }
     n.children = kids;
     t.max_depth = std::max(t.max_depth, depth);
@@ -188,7 +335,7 @@ void parallel_rows(int m, int nthreads, const std::function<void(int, int)>& bod
 // Pivoting restricted to one front cannot otherwise cope with the nearly
 // singular pivot blocks of boxes close to a Dirichlet resonance (Helmholtz),
 // and the growth it lets through costs ~cond * eps in backward error.
-void factor_node(NDTree& t, int id, const std::vector<cplx>& A9, std::vector<int>& rpos, std::vector<int>& cpos,
+void factor_node(NDTree& t, int id, const LatticeMatrix& A, std::vector<int>& rpos, std::vector<int>& cpos,
                  double pivtol, int nthreads) {
     NDNode& n = t.nodes[id];
     std::vector<int> rows = n.vars, cols = n.vars;
@@ -205,22 +352,18 @@ void factor_node(NDTree& t, int id, const std::vector<cplx>& A9, std::vector<int
         cpos[cols[i]] = i;
     }
     std::vector<cplx> Fm(size_t(F) * F, cplx(0.0));
-    const int W = t.CX + 1;
     // original entries not assembled below: own-var rows against own and ring
     // columns, and ring rows against own columns (a delayed variable's
     // couplings already sit in the child's contribution block)
     auto fresh = [&](int p) { return p >= 0 && (p < nown || p >= sN); };
     for (int i = 0; i < nown; ++i) {
-        const int v = n.vars[i], X = v % W, Y = v / W;
-        for (int dy = -1; dy <= 1; ++dy)
-            for (int dx = -1; dx <= 1; ++dx) {
-                const int WX = X + dx, WY = Y + dy;
-                if (WX < 0 || WX > t.CX || WY < 0 || WY > t.CY) continue;
-                const int w = WY * W + WX, pw = cpos[w];
-                if (!fresh(pw)) continue;
-                Fm[size_t(i) * F + pw] += A9[size_t(v) * 9 + (dy + 1) * 3 + (dx + 1)];
-                if (pw >= sN) Fm[size_t(rpos[w]) * F + i] += A9[size_t(w) * 9 + (1 - dy) * 3 + (1 - dx)];
-            }
+        const int v = n.vars[i];
+        for (int k = A.rp[v]; k < A.rp[v + 1]; ++k) {
+            const int w = A.ci[k], pw = cpos[w];
+            if (!fresh(pw)) continue;
+            Fm[size_t(i) * F + pw] += A.v[k];
+            if (pw >= sN) Fm[size_t(rpos[w]) * F + i] += A.at(w, v);
+        }
     }
     for (int c : n.children) {
         NDNode& ch = t.nodes[c];
@@ -283,7 +426,7 @@ void factor_node(NDTree& t, int id, const std::vector<cplx>& A9, std::vector<int
     n.ke = ke;
     n.rc.assign(F, -1);  // right-hand side entries injected at this front: own-var rows
     {
-        std::vector<char> own(size_t(t.CX + 1) * (t.CY + 1), 0);
+        std::vector<char> own(size_t(t.nv), 0);
         for (int v : n.vars) own[v] = 1;
         for (int i = 0; i < F; ++i)
             if (own[rows[i]]) n.rc[i] = rows[i];
@@ -331,13 +474,13 @@ void factor_node(NDTree& t, int id, const std::vector<cplx>& A9, std::vector<int
 
 }  // namespace
 
-void nd_factor(const HostProblem& hp, NDTree& t, int leaf_max, double pivtol) {
-    const int m = hp.p / 2;
-    t.CX = hp.nx * m;
-    t.CY = hp.ny * m;
-    const int nv = (t.CX + 1) * (t.CY + 1);
-    build_nd(t, 0, t.CX, 0, t.CY, 0, leaf_max);
-    const std::vector<cplx> A9 = coarse_stencil(hp);
+void nd_factor(const LatticeMatrix& A, NDTree& t, int leaf_max, double pivtol) {
+    t.W = A.W;
+    t.H = A.H;
+    t.q = A.q;
+    t.nv = A.W * A.H;
+    const int nv = t.nv;
+    build_nd(t, A, 0, A.W - 1, 0, A.H - 1, 0, leaf_max);
     // factor bottom-up by depth; nodes of one depth in parallel
     const int nthr = std::max(1, int(std::thread::hardware_concurrency()));
     std::vector<std::vector<int>> bydepth(t.max_depth + 1);
@@ -353,7 +496,7 @@ void nd_factor(const HostProblem& hp, NDTree& t, int leaf_max, double pivtol) {
                     try {
                         std::vector<int> rpos(nv, -1), cpos(nv, -1);
                         for (int i; (i = next++) < int(ids.size());)
-                            factor_node(t, ids[i], A9, rpos, cpos, pivtol, 1);
+                            factor_node(t, ids[i], A, rpos, cpos, pivtol, 1);
                     } catch (...) {
                         errs[w] = std::current_exception();
                     }
@@ -363,7 +506,7 @@ void nd_factor(const HostProblem& hp, NDTree& t, int leaf_max, double pivtol) {
                 if (e) std::rethrow_exception(e);
         } else {
             std::vector<int> rpos(nv, -1), cpos(nv, -1);
-            for (int id : ids) factor_node(t, id, A9, rpos, cpos, pivtol, nthr);
+            for (int id : ids) factor_node(t, id, A, rpos, cpos, pivtol, nthr);
         }
         for (int id : ids) {
             const NDNode& n = t.nodes[id];

@@ -1259,6 +1259,48 @@ void coarse_apply_launch(const FineGeom& g, const double4* qtab, double hc, cons
 }
 
 // ---------------------------------------------------------------- vectors
+// GalerkinP: r_c = IP^T r and u += omega IP u_c for the inclusion IP
+// (proj/core/src/twogrid.cpp:188-219,272-273): each coarse dof is one fine dof
+__global__ void k_incl_restrict(const double2* __restrict__ r, const int* __restrict__ map, long long nc,
+                                double2* __restrict__ rc) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nc; i += (long long)gridDim.x * blockDim.x) {
+        const int f = map[i];
+        rc[i] = f >= 0 ? r[f] : make_double2(0.0, 0.0);
+    }
+}
+__global__ void k_incl_prolong(double2* __restrict__ u, const int* __restrict__ map, long long nc,
+                               const double2* __restrict__ uc, double omega) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nc; i += (long long)gridDim.x * blockDim.x) {
+        const int f = map[i];
+        if (f >= 0) {
+            const double2 c = uc[i];
+            double2 v = u[f];
+            v.x = fma(omega, c.x, v.x);
+            v.y = fma(omega, c.y, v.y);
+            u[f] = v;
+        }
+    }
+}
+// one warp-quarter (8 lanes) per row
+__global__ void k_csr_apply(const int* __restrict__ rp, const int* __restrict__ ci, const double2* __restrict__ v,
+                            long long n, const double2* __restrict__ x, double2* __restrict__ y) {
+    const long long row = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 3;
+    const int l = threadIdx.x & 7;
+    double re = 0.0, im = 0.0;
+    if (row < n)
+        for (int k = rp[row] + l; k < rp[row + 1]; k += 8) {
+            const double2 a = v[k], b = x[ci[k]];
+            re = fma(a.x, b.x, fma(-a.y, b.y, re));
+            im = fma(a.x, b.y, fma(a.y, b.x, im));
+        }
+#pragma unroll
+    for (int o = 4; o; o >>= 1) {
+        re += __shfl_xor_sync(0xffffffffu, re, o);
+        im += __shfl_xor_sync(0xffffffffu, im, o);
+    }
+    if (row < n && l == 0) y[row] = make_double2(re, im);
+}
+
 __global__ void k_axpy(double2* __restrict__ y, const double2* __restrict__ x, double a, long long n) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
         y[i] = rfma(a, x[i], y[i]);
@@ -1272,6 +1314,23 @@ __global__ void k_zero(double2* __restrict__ y, long long n) {
         y[i] = make_double2(0.0, 0.0);
 }
 static unsigned vec_blocks(long long n) { return unsigned(std::min<long long>((n + 255) / 256, 148 * 8)); }
+void inclusion_restrict_launch(const double2* r, const int* map, long long nc, double2* rc, cudaStream_t st) {
+    k_incl_restrict<<<vec_blocks(nc), 256, 0, st>>>(r, map, nc, rc);
+    HTG_CUDA(cudaGetLastError());
+    count_launch();
+}
+void inclusion_prolong_launch(double2* u, const int* map, long long nc, const double2* uc, double omega,
+                              cudaStream_t st) {
+    k_incl_prolong<<<vec_blocks(nc), 256, 0, st>>>(u, map, nc, uc, omega);
+    HTG_CUDA(cudaGetLastError());
+    count_launch();
+}
+void csr_apply_launch(const int* rp, const int* ci, const double2* v, long long n, const double2* x, double2* y,
+                      cudaStream_t st) {
+    k_csr_apply<<<unsigned((n * 8 + 255) / 256), 256, 0, st>>>(rp, ci, v, n, x, y);
+    HTG_CUDA(cudaGetLastError());
+    count_launch();
+}
 void vec_axpy(double2* y, const double2* x, double a, long long n, cudaStream_t st) {
     k_axpy<<<vec_blocks(n), 256, 0, st>>>(y, x, a, n);
     HTG_CUDA(cudaGetLastError());

@@ -38,6 +38,14 @@ void prolong_add_launch(const FineGeom& g, double2* u, const double2* uc, double
 void coarse_apply_launch(const FineGeom& g, const double4* qtab, double hc, const double2* x, double2* y,
                          cudaStream_t st);
 
+// GalerkinP transfers (inclusion IP: coarse dof i <-> fine dof map[i], -1 for Dirichlet)
+void inclusion_restrict_launch(const double2* r, const int* map, long long nc, double2* rc, cudaStream_t st);
+void inclusion_prolong_launch(double2* u, const int* map, long long nc, const double2* uc, double omega,
+                              cudaStream_t st);
+// y = A x, complex CSR (GalerkinP coarse operator)
+void csr_apply_launch(const int* rp, const int* ci, const double2* v, long long n, const double2* x, double2* y,
+                      cudaStream_t st);
+
 // vectors
 void vec_axpy(double2* y, const double2* x, double a, long long n, cudaStream_t st);  // y += a x
 void vec_copy(double2* y, const double2* x, long long n, cudaStream_t st);

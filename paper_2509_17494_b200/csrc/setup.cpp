@@ -210,9 +210,11 @@ HostProblem make_problem(const htg_problem& pr) {
 void validate_config(const htg_config& c, const HostProblem& hp) {
     if (c.n_s < 0 || c.n_dd < 1 || c.max_iters < 0) throw InvalidArgument("invalid iteration counts");
     if (c.smoother == HTG_SMOOTHER_CSDD && c.l_dd < 2) throw InvalidArgument("partition: l_dd must be >= 2");
-    if (c.coarsening != HTG_COARSE_OPTIMIZED_FD && c.coarsening != HTG_COARSE_NONE)
-        throw InvalidArgument("coarsening: only 'opt' (QSFEM) and 'none' are implemented");
-    if (c.smoother != HTG_SMOOTHER_CSDD) throw InvalidArgument("smoother: only 'csdd' is implemented on the GPU");
+    if (c.coarsening != HTG_COARSE_OPTIMIZED_FD && c.coarsening != HTG_COARSE_GALERKIN_P &&
+        c.coarsening != HTG_COARSE_NONE)
+        throw InvalidArgument("unknown coarsening");
+    if (c.smoother != HTG_SMOOTHER_CSDD && c.smoother != HTG_SMOOTHER_EXACT_SHIFTED)
+        throw InvalidArgument("unknown smoother");
     if (c.outer != HTG_OUTER_RICHARDSON && c.outer != HTG_OUTER_KRYLOV) throw InvalidArgument("unknown outer iteration");
     if (c.coarsening == HTG_COARSE_OPTIMIZED_FD) {
         const double hc = 2.0 * hp.h / hp.p;

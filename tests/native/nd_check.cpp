@@ -40,13 +40,12 @@ int nd_stencil(const htg_problem* prob, double* a9, long long cap) {
 // Factor and solve A_c x = rc for nrhs right-hand sides (interleaved complex),
 // applying the explicit blocks exactly as the GPU level kernels do.
 // stats: [delayed pivots, max front, live nodes, 0]
-int nd_check(const htg_problem* prob, int leaf, double pivtol, const double* rc, double* x, int nrhs,
-             double* stats) {
+static int nd_run(const htg::LatticeMatrix& A, int leaf, double pivtol, const double* rc, double* x, int nrhs,
+                  double* stats) {
     try {
-        const htg::HostProblem hp = htg::make_problem(*prob);
         htg::NDTree t;
-        htg::nd_factor(hp, t, leaf, pivtol);
-        const int nv = (t.CX + 1) * (t.CY + 1);
+        htg::nd_factor(A, t, leaf, pivtol);
+        const int nv = t.nv;
         stats[0] = double(t.delayed);
         stats[1] = t.max_front;
         stats[2] = double(t.nodes.size());
@@ -93,6 +92,48 @@ int nd_check(const htg_problem* prob, int leaf, double pivtol, const double* rc,
             }
         }
         return 0;
+    } catch (const std::exception&) {
+        return 1;
+    }
+}
+
+int nd_check(const htg_problem* prob, int leaf, double pivtol, const double* rc, double* x, int nrhs,
+             double* stats) {
+    try {
+        const htg::HostProblem hp = htg::make_problem(*prob);
+        return nd_run(htg::qsfem_lattice(hp), leaf, pivtol, rc, x, nrhs, stats);
+    } catch (const std::exception&) {
+        return 1;
+    }
+}
+
+// the order-q FE lattice matrix of the product (GalerkinP coarse operator for
+// q = p/2, the shifted fine operator of the ExactShifted smoother for q = p)
+int nd_fe_apply(const htg_problem* prob, int q, double alpha, const double* xin, double* yout) {
+    try {
+        const htg::HostProblem hp = htg::make_problem(*prob);
+        const htg::Basis1D b = htg::make_basis(hp.p);
+        const htg::LatticeMatrix A = htg::fe_lattice(hp, b, q, alpha);
+        const cplx* X = reinterpret_cast<const cplx*>(xin);
+        cplx* Y = reinterpret_cast<cplx*>(yout);
+        const int n = A.W * A.H;
+        for (int i = 0; i < n; ++i) {
+            cplx acc = 0.0;
+            for (int k = A.rp[i]; k < A.rp[i + 1]; ++k) acc += A.v[k] * X[A.ci[k]];
+            Y[i] = acc;
+        }
+        return 0;
+    } catch (const std::exception&) {
+        return 1;
+    }
+}
+
+int nd_check_fe(const htg_problem* prob, int q, double alpha, int leaf, double pivtol, const double* rc, double* x,
+                int nrhs, double* stats) {
+    try {
+        const htg::HostProblem hp = htg::make_problem(*prob);
+        const htg::Basis1D b = htg::make_basis(hp.p);
+        return nd_run(htg::fe_lattice(hp, b, q, alpha), leaf, pivtol, rc, x, nrhs, stats);
     } catch (const std::exception&) {
         return 1;
     }

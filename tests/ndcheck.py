@@ -52,3 +52,27 @@ def coarse_check(problem, rc, leaf=16, pivtol=0.1):
         be.append(np.linalg.norm(y.ravel() - rc[r]) / np.linalg.norm(rc[r]))
     stats = dict(delayed=int(st[0]), max_front=int(st[1]), nodes=int(st[2]))
     return x, max(be), stats
+
+
+def fe_apply(problem, q, alpha, x):
+    """y = A x with the product's order-q FE lattice matrix (csrc/coarse_nd.cpp fe_lattice)."""
+    L = _lib()
+    cp, keep = _cproblem(problem)
+    x = np.ascontiguousarray(x, dtype=np.complex128)
+    y = np.zeros_like(x)
+    assert L.nd_fe_apply(C.byref(cp), int(q), C.c_double(alpha), x.ctypes.data_as(C.c_void_p),
+                         y.ctypes.data_as(C.c_void_p)) == 0
+    return y
+
+
+def fe_solve(problem, q, alpha, b, leaf=16, pivtol=0.3):
+    """Solve A x = b with the ND factors of the order-q FE lattice matrix; returns (x, stats)."""
+    L = _lib()
+    cp, keep = _cproblem(problem)
+    b = np.ascontiguousarray(np.atleast_2d(b), dtype=np.complex128)
+    x = np.zeros_like(b)
+    st = np.zeros(4)
+    assert L.nd_check_fe(C.byref(cp), int(q), C.c_double(alpha), int(leaf), C.c_double(pivtol),
+                         b.ctypes.data_as(C.c_void_p), x.ctypes.data_as(C.c_void_p), int(b.shape[0]),
+                         st.ctypes.data_as(C.c_void_p)) == 0
+    return x, dict(delayed=int(st[0]), max_front=int(st[1]), nodes=int(st[2]))

@@ -7,7 +7,7 @@ import pytest
 import paper_2509_17494_b200 as hb
 from oracle import pyoracle as po
 
-from ndcheck import coarse_check
+from ndcheck import coarse_check, fe_apply, fe_solve
 
 N_, A_ = hb.NEUMANN, hb.ABSORBING
 
@@ -45,3 +45,45 @@ def test_nd_delayed_pivots_near_resonance():
     assert st0["delayed"] == 0 and be0 > 1e-12  # the failure mode exists on this case
     assert st["delayed"] > 0 and be < 1e-12
     assert st["max_front"] <= st0["max_front"] + 8  # delays stay local
+
+
+D_ = hb.DIRICHLET
+FE_CASES = [dict(order=4, wavelengths=3, ppw=10),
+            dict(order=4, wavelengths=3, ppw=8, side_tags=(D_, A_, N_, A_)),
+            dict(order=2, wavelengths=3, ppw=8, side_tags=(A_, D_, A_, N_), layer_sides=(0,), layer_width_dofs=6),
+            dict(order=6, wavelengths=2, ppw=12)]
+
+
+@pytest.mark.parametrize("kw", FE_CASES)
+def test_fe_lattice_matches_oracle_assembly(kw):
+    """fe_lattice(q = p, alpha_s) == the oracle's A_s, and fe_lattice(q = p/2, alpha_c) == the
+    GalerkinP coarse matrix (proj/core/src/fespace.cpp:181-210, twogrid.cpp:189-219), applied to
+    seeded vectors."""
+    prob = hb.build_problem(hb.ProblemSpec(**kw))
+    cfg = po.SolverConfig(coarsening=1, alpha_c=0.05)
+    ses = po.Session(po.ProblemSpec(**kw), cfg)
+    g = np.random.default_rng(5)
+    x = g.standard_normal(ses.ndof) + 1j * g.standard_normal(ses.ndof)
+    want = ses.apply(1, x)
+    got = fe_apply(prob, kw["order"], cfg.alpha_s, x)
+    assert np.linalg.norm(got - want) / np.linalg.norm(want) < 1e-13
+    xc = g.standard_normal(ses.coarse_ndof) + 1j * g.standard_normal(ses.coarse_ndof)
+    want = ses.apply(2, xc)
+    got = fe_apply(prob, kw["order"] // 2, cfg.alpha_c, xc)
+    assert np.linalg.norm(got - want) / np.linalg.norm(want) < 1e-13
+
+
+@pytest.mark.parametrize("kw", FE_CASES[:3])
+def test_fe_nd_solve(kw):
+    """ND factors of the FE lattice matrices (separators on element-boundary lines) solve
+    A_s x = b and A_c x = b to rounding level."""
+    prob = hb.build_problem(hb.ProblemSpec(**kw))
+    p = kw["order"]
+    for q, alpha in ((p, 0.2), (p // 2, 0.05)):
+        n = (prob.n_cells * q + 1) ** 2
+        g = np.random.default_rng(q)
+        b = g.standard_normal((2, n)) + 1j * g.standard_normal((2, n))
+        x, st = fe_solve(prob, q, alpha, b)
+        for r in range(2):
+            res = fe_apply(prob, q, alpha, x[r]) - b[r]
+            assert np.linalg.norm(res) / np.linalg.norm(b[r]) < 1e-12, (q, st)

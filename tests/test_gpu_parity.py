@@ -25,6 +25,14 @@ CASES = {
     "p4_ndd2": (4, 3, 10, (A_, A_, A_, A_), (), {"n_dd": 2}),
     "p4_krylov": (4, 4, 10, (A_, A_, A_, A_), (), {"outer": 1}),
     "p2_krylov_dir": (2, 4, 8, (D_, A_, A_, A_), (), {"outer": 1}),
+    # GalerkinP coarse level (twogrid.cpp:189-219), acceptance C08/C09 settings
+    "p4_galerkin": (4, 6, 10, (A_, A_, A_, A_), (), {"coarsening": 1, "alpha_s": 0.02, "alpha_c": 0.02, "l_dd": 10}),
+    "p4_galerkin_dir": (4, 4, 10, (D_, A_, D_, A_), (), {"coarsening": 1, "alpha_s": 0.02, "alpha_c": 0.02}),
+    "p2_galerkin_neu": (2, 4, 8, (N_, A_, A_, D_), (), {"coarsening": 1, "alpha_c": 0.1, "n_s": 2}),
+    # ExactShifted smoother u += A_s^-1 (f - A u) (twogrid.cpp:257-264)
+    "p4_exact": (4, 4, 10, (A_, A_, A_, A_), (), {"smoother": 1}),
+    "p4_exact_galerkin_krylov": (4, 3, 10, (D_, A_, N_, A_), (), {"smoother": 1, "coarsening": 1, "outer": 1}),
+    "p2_exact_layer": (2, 4, 8, (N_, A_, N_, A_), (po.LEFT,), {"smoother": 1, "layer_width_dofs": 8}),
 }
 
 
@@ -114,6 +122,8 @@ def test_coarse(case):
 
 def test_dd_step_and_smoother(case):
     name, (oses, prob, ops) = case
+    if CASES[name][5].get("smoother", 0) != 0:
+        pytest.skip("dd_step / csdd_smoother belong to the CSDD smoother")
     n = oses.ndof
     u, f = po.random_vector(n, 401), po.random_vector(n, 402)
     out = dev(np.zeros(n))
