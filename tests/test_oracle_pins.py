@@ -300,8 +300,23 @@ def test_p2_prolongation_injection():  # proj/tests/test_twogrid.cpp:215-234
             assert nnz[d] == 0
 
 
-def test_two_grid_properties():  # proj/tests/test_twogrid.cpp:266-299
-    s = po.Session(po.ProblemSpec(order=4, wavelengths=3, ppw=10), _cfg(l_dd=4))
+def test_galerkin_p_coarsening():  # proj/tests/test_twogrid.cpp:236-264
+    d = desc(3, 4, k=10.0)
+    s = po.Session(desc=d, config=_cfg(coarsening=1, alpha_c=0.0))
+    assert s.coarse_ndof == 49  # (3*2+1)^2
+    IP = s.csr(3).toarray()
+    assert np.abs(IP.conj().T @ IP - np.eye(49)).max() < 1e-14  # 0/1 inclusion of an index subset
+    direct = po.Session(desc=desc(3, 2, k=10.0), config=_cfg(coarsening=2)).csr(0).toarray()
+    assert np.abs(s.csr(2).toarray() - direct).max() < 1e-14  # alpha_c = 0: plain order-2 matrix
+    uc = po.random_vector(49, 7)
+    uf = IP @ uc
+    for x, y in ((0.21, 0.67), (0.83, 0.12)):  # the included functions are the same functions
+        assert abs(s.evaluate(uf, x, y) - s.evaluate(uc, x, y, coarse=True)) < 1e-13
+
+
+@pytest.mark.parametrize("coarsening", [0, 1])
+def test_two_grid_properties(coarsening):  # proj/tests/test_twogrid.cpp:266-299 (OptimizedFD, GalerkinP)
+    s = po.Session(po.ProblemSpec(order=4, wavelengths=3, ppw=10), _cfg(l_dd=4, coarsening=coarsening))
     n = s.ndof
     f = po.random_vector(n, 31)
     u = po.lu_solve_csr(s.csr(0), f)
@@ -364,6 +379,20 @@ def test_readme_iters_7():  # proj/README.md:89-102: dofs=40401 iters=7; accepta
     assert s.ndof == 40401
     r = s.solve(s.rhs())
     assert r.converged and r.iterations == 7
+
+
+def test_c08_c09_galerkin_p():  # proj/tests/acceptance.cpp:228-282 at the oracle-sized W = 10, 20
+    kw = dict(alpha_s=0.02, alpha_c=0.02, l_dd=10, coarsening=1, outer=1)
+
+    def its(W, sides=(A_,) * 4):
+        s = po.Session(po.ProblemSpec(order=4, wavelengths=W, ppw=10, side_tags=sides), _cfg(**kw))
+        r = s.solve(s.rhs())
+        assert r.converged
+        return r.iterations
+
+    a10, a20, d20 = its(10), its(20), its(20, (D_, A_, D_, A_))
+    assert a10 < a20  # C08: increasing with size
+    assert 1.4 <= d20 / a20 <= 2.6  # C09: Dirichlet sides cost 1.4x-2.6x
 
 
 def test_c11_structural():  # proj/tests/acceptance.cpp:314-360
