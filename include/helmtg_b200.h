@@ -71,10 +71,15 @@ typedef struct htg_handle htg_handle;
 void htg_config_default(htg_config* cfg);
 const char* htg_last_error(void);
 
-/* setup_two_grid (twogrid.cpp:221-253): host setup (subdomain classes and
- * their restricted inverses, coarse QSFEM operator and its nested-dissection
- * factorization), upload to HBM. stream: the cudaStream_t every call of this
- * handle is ordered on (NULL: the legacy default stream). */
+/* setup_two_grid (twogrid.cpp:221-253): host setup, upload to HBM.
+ *   smoother CSDD: subdomain classes and their restricted inverses / fast
+ *     diagonalisation factors; ExactShifted: nested-dissection LU of the fine
+ *     shifted operator A_s (u += A_s^-1 (f - A u), twogrid.cpp:257-264);
+ *   coarsening OptimizedFD: the QSFEM operator (qsfem.cpp:118-149); GalerkinP:
+ *     the order-p/2 Helmholtz operator with alpha_c and the inclusion IP
+ *     (twogrid.cpp:189-219); both factored by nested dissection.
+ * stream: the cudaStream_t every call of this handle is ordered on (NULL: the
+ * legacy default stream). */
 int htg_create(const htg_problem* prob, const htg_config* cfg, void* stream, htg_handle** out);
 int htg_destroy(htg_handle* h);
 
@@ -93,17 +98,20 @@ int htg_set_stream(htg_handle* h, void* stream);
 int htg_residual(htg_handle* h, const double* f, const double* u, double* r, int shifted);
 /* ||f - A u||_2 written to *out (host); the stopping test of twogrid.cpp:287. */
 int htg_residual_norm(htg_handle* h, const double* f, const double* u, double* out);
-/* dd_step (twogrid.cpp:92-112): out = PoU-average of R_i u + (A_s^(i))^-1 R_i (f - A_s u). */
+/* dd_step (twogrid.cpp:92-112): out = PoU-average of R_i u + (A_s^(i))^-1 R_i (f - A_s u).
+ * dd_step and csdd_smoother need smoother = CSDD (else HTG_ERR_INVALID). */
 int htg_dd_step(htg_handle* h, const double* u, const double* f, double* out);
 /* csdd_smoother (twogrid.cpp:114-120), u updated in place. */
 int htg_csdd_smoother(htg_handle* h, double* u, const double* f);
-/* K3a: rc = IP^H r (twogrid.cpp:272). */
+/* K3a: rc = IP^H r (twogrid.cpp:272); the transfers and the coarse calls
+ * need coarsening != None (else HTG_ERR_INVALID). */
 int htg_restrict(htg_handle* h, const double* r, double* rc);
 /* K1+K3a fused: rc = IP^H (f - A u), the fine residual never materialised. */
 int htg_residual_restrict(htg_handle* h, const double* f, const double* u, double* rc);
 /* K3b: u += omega * IP uc (twogrid.cpp:273). */
 int htg_prolong_add(htg_handle* h, double* u, const double* uc, double omega);
-/* K4: y = A_c x, the QSFEM coarse operator (qsfem.cpp:118-149). */
+/* K4: y = A_c x, the QSFEM coarse stencil (qsfem.cpp:118-149), or the
+ * GalerkinP coarse matrix (CSR). */
 int htg_coarse_apply(htg_handle* h, const double* x, double* y);
 /* uc = A_c^-1 rc by the factored coarse operator (twogrid.cpp:273). */
 int htg_coarse_solve(htg_handle* h, const double* rc, double* uc);

@@ -524,7 +524,14 @@ __global__ void __launch_bounds__(kK1Threads) k1_residual(K1Args a) {
 // banks (p = 2) or two-way (p = 4). The x = nx column unit (p dofs) and the top
 // lattice row (p dofs per unit) are 1-D bulk copies; r is written back from
 // shared memory with coalesced stores.
-constexpr int kKCCells = 120;                        // cell slots per CTA (lanes per warp group)
+#ifndef HTG_KC_CELLS
+#define HTG_KC_CELLS 120
+#endif
+#ifndef HTG_KC_CPS
+#define HTG_KC_CPS 1
+#endif
+constexpr int kKCCells = HTG_KC_CELLS;               // cell slots per CTA (lanes per warp group)
+constexpr int kKCCtasPerSM = HTG_KC_CPS;             // resident CTAs per SM the launch is sized for
 constexpr int kKCGroupWarps = (kKCCells + 31) / 32;  // warps per group
 constexpr int kKCThreads = 2 * 32 * kKCGroupWarps;   // two warp groups
 
@@ -957,7 +964,7 @@ __device__ __forceinline__ void k1c_body(const K1Args& a, const CUtensorMap* tmu
 }
 
 template <int P, int MODE, bool DIR>
-__global__ void __launch_bounds__(kKCThreads, 1)
+__global__ void __launch_bounds__(kKCThreads, kKCCtasPerSM)
     k1_cells(const __grid_constant__ K1Args a, const __grid_constant__ CUtensorMap tmu,
              const __grid_constant__ CUtensorMap tmf) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1018,7 +1025,7 @@ static int kc_row_blocks(const FineGeom& g, int rows) {
     if (rows > 0) return (g.ny + rows - 1) / rows;
     static int nsm = 0;
     if (!nsm) HTG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
-    return std::max(1, std::min(nsm / kc_gx(g), g.ny / 2));
+    return std::max(1, std::min(nsm * kKCCtasPerSM / kc_gx(g), g.ny / 2));
 }
 
 int k1_partials(const FineGeom& g, int rows) {
