@@ -13,6 +13,8 @@ def load(path):
             continue
         if hdr and len(r) == len(hdr):
             d = dict(zip(hdr, r))
+            if d.get("Metric Name", "gpu__time_duration.sum") != "gpu__time_duration.sum":
+                continue
             t = float(d["Metric Value"])
             t *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(d["Metric Unit"], 1.0)
             d["us"] = t
