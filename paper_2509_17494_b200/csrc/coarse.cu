@@ -33,6 +33,9 @@ struct Task {
 };
 
 constexpr int kCT = 256;     // threads per CTA (8 warps)
+#ifndef HTG_ND_KU
+#define HTG_ND_KU 4
+#endif
 constexpr int kWarpFMax = 128;  // warp-tier shared buffers (fronts with s + u <= g_warpF)
 static int env_int(const char* name, int dflt) {
     const char* e = std::getenv(name);
@@ -78,7 +81,26 @@ __device__ __forceinline__ void rows_dot(const double2* __restrict__ M, int len,
             acc[q] = make_double2(0.0, 0.0);
             rr[q] = rb + q * step + gi;
         }
-        for (int k = gl; k < len; k += G) {
+        // KU k-steps per trip with their loads issued together: a warp often owns a
+        // single long row (large-tier tasks), so the loop must keep several
+        // DRAM loads in flight per lane
+        constexpr int KU = HTG_ND_KU;
+        int k = gl;
+        for (; k + (KU - 1) * G < len; k += KU * G) {
+            double2 m[U][KU], vk[KU];
+#pragma unroll
+            for (int j = 0; j < KU; ++j) vk[j] = v[k + j * G];
+#pragma unroll
+            for (int q = 0; q < U; ++q)
+#pragma unroll
+                for (int j = 0; j < KU; ++j)
+                    m[q][j] = rr[q] < r1 ? M[(size_t)rr[q] * len + k + j * G] : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int q = 0; q < U; ++q)
+#pragma unroll
+                for (int j = 0; j < KU; ++j) acc[q] = cfma(m[q][j], vk[j], acc[q]);
+        }
+        for (; k < len; k += G) {
             const double2 vk = v[k];
 #pragma unroll
             for (int q = 0; q < U; ++q)
@@ -127,6 +149,7 @@ __device__ __forceinline__ void cols_dot(const double2* __restrict__ M, int rows
 template <int STRIDE, class Sync>
 __device__ void gather_front(const NDArgs& a, const NodeDev& nd, double2* sv, int t, Sync&& sync) {
     const int F = nd.s + nd.u;
+#pragma unroll 4
     for (int i = t; i < F; i += STRIDE) {
         const int ri = a.idx[nd.off_rc + i];
         double2 v = ri >= 0 ? a.rc[ri] : make_double2(0.0, 0.0);
@@ -203,6 +226,7 @@ __global__ void __launch_bounds__(kCT) k_nd_fwd2(const Task* tasks, NDArgs a) {
     extern __shared__ double2 smem[];
     const Task tk = tasks[blockIdx.x];
     const NodeDev nd = tk.nd;
+#pragma unroll 4
     for (int i = threadIdx.x; i < nd.s; i += kCT) smem[i] = a.Y[a.idx[nd.off_var + i]];
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -239,7 +263,9 @@ __global__ void __launch_bounds__(kCT) k_nd_bwd_warp(const NodeDev* __restrict__
     if (id >= n) return;
     const NodeDev nd = list[id];
     double2* v = sv[w];
+#pragma unroll 4
     for (int i = lane; i < nd.s; i += 32) v[i] = a.Y[a.idx[nd.off_var + i]];
+#pragma unroll 4
     for (int i = lane; i < nd.u; i += 32) v[nd.s + i] = a.X[a.idx[nd.off_ring + i]];
     __syncwarp();
     // x1 = U^-1 y1 - Z x2 (column-major blocks)
@@ -265,7 +291,9 @@ __global__ void __launch_bounds__(kCT) k_nd_bwd(const Task* tasks, NDArgs a) {
     double2* y1 = smem;
     double2* x2 = smem + nd.s;
     double2* sz = smem + nd.s + nd.u;
+#pragma unroll 4
     for (int i = threadIdx.x; i < nd.s; i += kCT) y1[i] = a.Y[a.idx[nd.off_var + i]];
+#pragma unroll 4
     for (int i = threadIdx.x; i < nd.u; i += kCT) x2[i] = a.X[a.idx[nd.off_ring + i]];
     __syncthreads();
     bwd_rows(a, nd, y1, x2, sz, tk.r0, tk.r0 + tk.nr, threadIdx.x >> 5, kCT / 32, threadIdx.x & 31, sync_cta_fn);
