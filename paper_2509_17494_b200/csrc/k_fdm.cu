@@ -240,7 +240,11 @@ __global__ void __launch_bounds__(kFThreads, 1) k_dd_fdm(FineGeom g, const FdmCl
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double2* fac = reinterpret_cast<double2*>(smem_raw);
     const int tid = threadIdx.x;
-    const int grp = tid >> 7, gt = tid & 127, q = gt >> 5, lane = tid & 31;
+    const int grp = tid >> 7, gt = tid & 127, lane = tid & 31;
+    // role of this warp inside its group, rotated by group: warp q of every group
+    // runs on SM sub-partition q, so the rotation spreads the CUDA-core remainder
+    // rows (one role) over the four sub-partitions' FP64 pipes
+    const int q = ((gt >> 5) + grp) & 3;
     double2* X = fac + fac_elems + size_t(grp) * 2 * rows * LD;  // gathered tile, then Q o Dinv
     double2* W = X + rows * LD;                                  // stage 1 / stage 3 products
     {  // the k padding of the data buffers must be finite: zero them once
@@ -342,7 +346,8 @@ __global__ void __launch_bounds__(kFThreads, 1) k_dd_fdm(FineGeom g, const FdmCl
                         ystage[(size_t)sid[par * 8 + s] * nu_max + urow[ixu * nuy + n]] = v;
                     }
                 });
-            group_sync(grp);  // W is rewritten by the next batch's stage 1
+            // (no barrier here: the next batch's first barrier also orders this
+            // stage's reads of W before that batch's stage-1 writes)
         }
         asm volatile("cp.async.wait_all;\n" ::: "memory");
         pos = seg_end;
