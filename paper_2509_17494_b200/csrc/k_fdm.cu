@@ -303,11 +303,18 @@ __global__ void __launch_bounds__(kFThreads, 1) k_dd_fdm(FineGeom g, const FdmCl
             }
             asm volatile("cp.async.commit_group;\n" ::: "memory");
         };
-        // batches of S subdomains, alternating between the two groups
-        int b0 = pos + grp * S;
-        if (b0 < seg_end) gather(b0, min(S, seg_end - b0), 0);
-        for (; b0 < seg_end; b0 += kFGroups * S, par ^= 1) {
-            const int nb = min(S, seg_end - b0);
+        // this group's batches of the segment: full rounds of S subdomains per
+        // group, then the remainder (< groups x S) split evenly, so the groups of
+        // a CTA finish within one subdomain of each other
+        const int nseg = seg_end - pos, R = nseg / (kFGroups * S), rem = nseg - R * kFGroups * S;
+        const int tail_n = rem / kFGroups + (grp < rem % kFGroups ? 1 : 0);
+        const int tail_b = pos + R * kFGroups * S + grp * (rem / kFGroups) + min(grp, rem % kFGroups);
+        const int nbatch = R + (tail_n > 0 ? 1 : 0);
+        auto bstart = [&](int i) { return i < R ? pos + (i * kFGroups + grp) * S : tail_b; };
+        auto bsize = [&](int i) { return i < R ? S : tail_n; };
+        if (nbatch > 0) gather(bstart(0), bsize(0), 0);
+        for (int bi = 0; bi < nbatch; ++bi, par ^= 1) {
+            const int b0 = bstart(bi), nb = bsize(bi);
             asm volatile("cp.async.wait_all;\n" ::: "memory");
             group_sync(grp);
             // 1: P[ix'][(s,iy)] = sum_ix Vx[ix][ix'] G_s[ix][iy]  -> W[(s,ix')][iy]
@@ -336,8 +343,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_dd_fdm(FineGeom g, const FdmCl
             });
             group_sync(grp);
             // the gathered tile is free: fetch the group's next batch under stage 4
-            const int nb0 = b0 + kFGroups * S;
-            if (nb0 < seg_end) gather(nb0, min(S, seg_end - nb0), par ^ 1);
+            if (bi + 1 < nbatch) gather(bstart(bi + 1), bsize(bi + 1), par ^ 1);
             // 4: Y[(s,ixu)][iyu] = sum_iy' R[(s,ixu)][iy'] Vy[uy0 + iyu][iy']  -> staging rows
             Stage<LD, KS>{V2U, nuy, W, nb * nux, false, q, lane}(
                 [&](int m, int n, double2 v) {
