@@ -532,6 +532,14 @@ __global__ void __launch_bounds__(kK1Threads) k1_residual(K1Args a) {
 #endif
 constexpr int kKCCells = HTG_KC_CELLS;               // cell slots per CTA (lanes per warp group)
 constexpr int kKCCtasPerSM = HTG_KC_CPS;             // resident CTAs per SM the launch is sized for
+// row slots: u prefetched kKCU - 2 rows ahead, f one row ahead. With two f slots
+// (measured: 4 u + 2 f was slower for r = f - A u, 36.5 vs 34.8 us at cfg4) f(y+1) is issued
+// after row y's exchange barrier, when every read of f(y-1) -- residual and
+// r store -- is done, so two f slots suffice and the third slot deepens u)
+#ifndef HTG_KC_USLOTS
+#define HTG_KC_USLOTS 3
+#endif
+constexpr int kKCU = HTG_KC_USLOTS, kKCF = 6 - HTG_KC_USLOTS;
 constexpr int kKCGroupWarps = (kKCCells + 31) / 32;  // warps per group
 constexpr int kKCThreads = 2 * 32 * kKCGroupWarps;   // two warp groups
 
@@ -553,12 +561,12 @@ struct KCCfg {
 template <int P>
 struct __align__(1024) KCSmem {
     using C = KCCfg<P>;
-    double2 U[3][C::SLOT / 16];
-    double2 F[3][C::SLOT / 16];
+    double2 U[kKCU][C::SLOT / 16];  // u rows y, y+1 (the cell row) and the prefetched rows
+    double2 F[kKCF][C::SLOT / 16];  // f row y (r written in place) and f(y+1) in flight
     double2 X[2][2][kKCCells][C::NR];    // right-column exchange [row parity][group]
     double2 XP[kKCCells][C::MM + 1];     // restriction partials exchange
     double red[kKCThreads];
-    unsigned long long barU[3], barF[3];
+    unsigned long long barU[kKCU], barF[kKCF];
 };
 
 // double2 index of element k of staged unit u (rows below the top): the
@@ -619,13 +627,13 @@ __device__ __forceinline__ void k1c_body(const K1Args& a, const CUtensorMap* tmu
     const double2* mt = a.shifted ? g.mtabS : g.mtab0;
     const double2 m_uniform = mt[0];  // one coefficient class: loaded once
 
-    auto uslot = [&](int yy) { return sm.U[(yy - ystart) % 3]; };
-    auto fslot = [&](int yy) { return sm.F[(yy - yres0) % 3]; };
-    auto ubar = [&](int yy) { return &sm.barU[(yy - ystart) % 3]; };
-    auto fbar = [&](int yy) { return &sm.barF[(yy - yres0) % 3]; };
+    auto uslot = [&](int yy) { return sm.U[(yy - ystart) % kKCU]; };
+    auto fslot = [&](int yy) { return sm.F[(yy - yres0) % kKCF]; };
+    auto ubar = [&](int yy) { return &sm.barU[(yy - ystart) % kKCU]; };
+    auto fbar = [&](int yy) { return &sm.barF[(yy - yres0) % kKCF]; };
     // the k-th use of a slot completes its barrier's phase k
-    auto wait_u = [&](int yy) { mbar_wait(ubar(yy), unsigned(((yy - ystart) / 3) & 1)); };
-    auto wait_f = [&](int yy) { mbar_wait(fbar(yy), unsigned(((yy - yres0) / 3) & 1)); };
+    auto wait_u = [&](int yy) { mbar_wait(ubar(yy), unsigned(((yy - ystart) / kKCU) & 1)); };
+    auto wait_f = [&](int yy) { mbar_wait(fbar(yy), unsigned(((yy - yres0) / kKCF) & 1)); };
     // thread 0: stage row yy of u or f (rows < ny: tensor box + the x = nx unit; top row: linear)
     auto stage = [&](double2* dst, const double2* src, const CUtensorMap* map, int yy, unsigned long long* bar) {
         fence_async_smem();  // generic accesses to the slot precede the async-proxy writes
@@ -642,16 +650,13 @@ __device__ __forceinline__ void k1c_body(const K1Args& a, const CUtensorMap* tmu
         }
     };
     if (tid == 0) {
-        for (int i = 0; i < 3; ++i) {
-            mbar_init(&sm.barU[i], 1);
-            mbar_init(&sm.barF[i], 1);
-        }
+        for (int i = 0; i < kKCU; ++i) mbar_init(&sm.barU[i], 1);
+        for (int i = 0; i < kKCF; ++i) mbar_init(&sm.barF[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
     if (tid == 0) {
-        stage(uslot(ystart), a.u, tmu, ystart, ubar(ystart));
-        if (ystart + 1 <= ye) stage(uslot(ystart + 1), a.u, tmu, ystart + 1, ubar(ystart + 1));
+        for (int i = 0; i + 1 < kKCU && ystart + i <= ye; ++i) stage(uslot(ystart + i), a.u, tmu, ystart + i, ubar(ystart + i));
         if (ystart >= yres0) stage(fslot(ystart), a.f, tmf, ystart, fbar(ystart));
     }
 
@@ -692,14 +697,17 @@ __device__ __forceinline__ void k1c_body(const K1Args& a, const CUtensorMap* tmu
     auto own_idx = [&](int al, int bp) { return edge ? EDGE + (bp == 0 ? 0 : bp - 1) : kc_idx<P>(ct, upos<P>(al, bp)); };
 
     for (int y = ystart; y < ye; ++y) {
-        // Thread 0 prefetches u(y + 2) into the slot of u(y - 1) and f(y + 1) into
-        // the slot of f(y - 2). Every read of u(y - 1) precedes the last barrier of
-        // row y - 1 (compute: exchange barrier; Dirichlet reads: store / partials
-        // barrier, or the extra barrier below), and every read of f(y - 2) precedes
-        // the exchange barrier of row y - 1.
+        // Thread 0 prefetches u(y + kKCU - 1) into the slot of u(y - 1): every read
+        // of u(y - 1) precedes the last barrier of row y - 1 (compute: exchange
+        // barrier; Dirichlet reads: store / partials barrier, or the extra barrier
+        // below). f(y + 1) goes into the slot of f(y + 1 - kKCF): with three f slots
+        // at the top of the row (every read of f(y - 2) precedes the exchange barrier
+        // of row y - 1), with two after the exchange barrier of row y (every read
+        // of f(y - 1), residual and r store, precedes it).
+        const bool stage_f = y + 1 >= yres0 && (y + 1 < ye || (top && y + 1 == ny));
         if (tid == 0) {
-            if (y + 2 <= ye) stage(uslot(y + 2), a.u, tmu, y + 2, ubar(y + 2));
-            if (y + 1 >= yres0 && (y + 1 < ye || (top && y + 1 == ny))) stage(fslot(y + 1), a.f, tmf, y + 1, fbar(y + 1));
+            if (y + kKCU - 1 <= ye) stage(uslot(y + kKCU - 1), a.u, tmu, y + kKCU - 1, ubar(y + kKCU - 1));
+            if (kKCF >= 3 && stage_f) stage(fslot(y + 1), a.f, tmf, y + 1, fbar(y + 1));
         }
         wait_u(y);
         wait_u(y + 1);
@@ -727,7 +735,11 @@ __device__ __forceinline__ void k1c_body(const K1Args& a, const CUtensorMap* tmu
         for (int i = 0; i < B; ++i)
 #pragma unroll
             for (int j = 0; j < NRG; ++j) O[i][j] = zero;
+#ifdef HTG_K1_NOCOMP
+        if (false) {
+#else
         if (cell) {
+#endif
             const double2 m = g.cls ? mt[g.cls[(size_t)y * nx + ux]] : m_uniform;
 #pragma unroll
             for (int cl = 0; cl < B; ++cl) {
@@ -800,6 +812,7 @@ __device__ __forceinline__ void k1c_body(const K1Args& a, const CUtensorMap* tmu
 #pragma unroll
             for (int j = 0; j < NRG; ++j) Xb[ct][j] = O[1][j];
         __syncthreads();
+        if (kKCF < 3 && tid == 0 && stage_f) stage(fslot(y + 1), a.f, tmf, y + 1, fbar(y + 1));
         if (active && ct > 0)
 #pragma unroll
             for (int j = 0; j < NRG; ++j) O[0][j] = cadd(O[0][j], Xb[ct - 1][j]);
