@@ -311,44 +311,38 @@ class NDSolver : public CoarseSolver {
     }
     ~NDSolver() override {
         for (void* p : allocs_) cudaFree(p);
+        for (cudaStream_t x : bst_) cudaStreamDestroy(x);
+        for (cudaEvent_t e : ev_join_) cudaEventDestroy(e);
+        if (ev_fork_) cudaEventDestroy(ev_fork_);
     }
     size_t device_bytes() const override { return bytes_; }
-    int levels() const override { return int(levels_.size()); }
+    int levels() const override { return nlevels_; }
 
+    // Forward: the subtrees below the split depth run on forked streams (in a
+    // CUDA graph: parallel branches), deepest level first, then the top levels;
+    // backward in the reverse order. Levels with few fronts are latency-bound
+    // launches, so independent subtrees overlap them.
     void solve(const double2* rc, double2* uc, cudaStream_t st) override {
         NDArgs a = args_;
         a.rc = rc;
         a.X = uc;
-        for (int L = int(levels_.size()) - 1; L >= 0; --L) {  // forward: deepest level first
-            const Level& lv = levels_[L];
-            if (lv.nwarp) {
-                k_nd_fwd_warp<<<(lv.nwarp + 7) / 8, kCT, 0, st>>>(lv.warp, lv.nwarp, a);
-                count_launch();
-            }
-            if (lv.nmid) {
-                k_nd_fwd_mid<<<lv.nmid, kCT, lv.smem_mid, st>>>(lv.mid, a);
-                count_launch();
-            }
-            if (lv.nf1) {
-                k_nd_fwd1<<<lv.nf1, kCT, lv.smem_big, st>>>(lv.f1, a);
-                count_launch();
-            }
-            if (lv.nf2) {
-                k_nd_fwd2<<<lv.nf2, kCT, lv.smem_big, st>>>(lv.f2, a);
-                count_launch();
-            }
+        const int nb = int(br_.size()) - 1;  // branch 0: the top levels
+        HTG_CUDA(cudaEventRecord(ev_fork_, st));
+        for (int b = 1; b <= nb; ++b) {
+            HTG_CUDA(cudaStreamWaitEvent(bst_[b - 1], ev_fork_, 0));
+            for (int L = int(br_[b].size()) - 1; L >= 0; --L) fwd_level(br_[b][L], a, bst_[b - 1]);
+            HTG_CUDA(cudaEventRecord(ev_join_[b - 1], bst_[b - 1]));
         }
-        for (int L = 0; L < int(levels_.size()); ++L) {  // backward: root first
-            const Level& lv = levels_[L];
-            if (lv.nb) {
-                k_nd_bwd<<<lv.nb, kCT, lv.smem_b, st>>>(lv.b, a);
-                count_launch();
-            }
-            if (lv.nwarp) {
-                k_nd_bwd_warp<<<(lv.nwarp + 7) / 8, kCT, 0, st>>>(lv.warp, lv.nwarp, a);
-                count_launch();
-            }
+        for (int b = 1; b <= nb; ++b) HTG_CUDA(cudaStreamWaitEvent(st, ev_join_[b - 1], 0));
+        for (int L = int(br_[0].size()) - 1; L >= 0; --L) fwd_level(br_[0][L], a, st);
+        for (int L = 0; L < int(br_[0].size()); ++L) bwd_level(br_[0][L], a, st);
+        HTG_CUDA(cudaEventRecord(ev_fork_, st));
+        for (int b = 1; b <= nb; ++b) {
+            HTG_CUDA(cudaStreamWaitEvent(bst_[b - 1], ev_fork_, 0));
+            for (int L = 0; L < int(br_[b].size()); ++L) bwd_level(br_[b][L], a, bst_[b - 1]);
+            HTG_CUDA(cudaEventRecord(ev_join_[b - 1], bst_[b - 1]));
         }
+        for (int b = 1; b <= nb; ++b) HTG_CUDA(cudaStreamWaitEvent(st, ev_join_[b - 1], 0));
         HTG_CUDA(cudaGetLastError());
     }
 
@@ -359,7 +353,41 @@ class NDSolver : public CoarseSolver {
         int nwarp = 0, nmid = 0, nf1 = 0, nf2 = 0, nb = 0;
         size_t smem_mid = 0, smem_big = 0, smem_b = 0;
     };
-    std::vector<Level> levels_;
+    static void fwd_level(const Level& lv, const NDArgs& a, cudaStream_t st) {
+        if (lv.nwarp) {
+            k_nd_fwd_warp<<<(lv.nwarp + 7) / 8, kCT, 0, st>>>(lv.warp, lv.nwarp, a);
+            count_launch();
+        }
+        if (lv.nmid) {
+            k_nd_fwd_mid<<<lv.nmid, kCT, lv.smem_mid, st>>>(lv.mid, a);
+            count_launch();
+        }
+        if (lv.nf1) {
+            k_nd_fwd1<<<lv.nf1, kCT, lv.smem_big, st>>>(lv.f1, a);
+            count_launch();
+        }
+        if (lv.nf2) {
+            k_nd_fwd2<<<lv.nf2, kCT, lv.smem_big, st>>>(lv.f2, a);
+            count_launch();
+        }
+    }
+    static void bwd_level(const Level& lv, const NDArgs& a, cudaStream_t st) {
+        if (lv.nb) {
+            k_nd_bwd<<<lv.nb, kCT, lv.smem_b, st>>>(lv.b, a);
+            count_launch();
+        }
+        if (lv.nwarp) {
+            k_nd_bwd_warp<<<(lv.nwarp + 7) / 8, kCT, 0, st>>>(lv.warp, lv.nwarp, a);
+            count_launch();
+        }
+    }
+    // br_[0]: levels 0 .. split-1 (the top); br_[b]: the subtree of the b-th node at
+    // the split depth, indexed by depth - split
+    std::vector<std::vector<Level>> br_;
+    std::vector<cudaStream_t> bst_;
+    std::vector<cudaEvent_t> ev_join_;
+    cudaEvent_t ev_fork_ = nullptr;
+    int nlevels_ = 0;
     std::vector<void*> allocs_;
     size_t bytes_ = 0;
     int nv_ = 0;
@@ -466,50 +494,89 @@ class NDSolver : public CoarseSolver {
         args_.contrib = up(std::vector<double2>(std::max(contrib_total, 1)), st);
         args_.front = up(std::vector<double2>(std::max(front_total, 1)), st);
         args_.Y = up(std::vector<double2>(nv_), st);
-        // per depth: warp tier, CTA tier, large tier (8 rows per CTA task)
+        // Branches: the subtrees rooted at the nodes of depth `split` (env
+        // HTG_ND_SPLIT, default 3: eight subtrees) run on their own streams; the
+        // levels above them are branch 0. Per (branch, depth): warp tier, CTA
+        // tier, large tier (8 rows per CTA task).
+        const int split = std::max(0, env_int("HTG_ND_SPLIT", 3));
+        std::vector<int> branch(nn, 0);
+        int nbranch = 0;
+        {
+            std::vector<int> bid(nn, -1);
+            for (int i = nn - 1; i >= 0; --i)  // postorder reversed: parents before children
+                if (t.nodes[i].depth == split && split > 0) bid[i] = ++nbranch;
+            for (int i = nn - 1; i >= 0; --i) {
+                const int par = t.nodes[i].parent;
+                if (bid[i] < 0) bid[i] = (par >= 0 && t.nodes[i].depth > split) ? bid[par] : 0;
+                branch[i] = std::max(bid[i], 0);
+            }
+        }
         const int D = t.max_depth + 1;
-        levels_.resize(D);
-        std::vector<std::vector<NodeDev>> wp(D), md(D);
-        std::vector<std::vector<Task>> f1(D), f2(D), bw(D);
+        nlevels_ = D;
+        br_.assign(nbranch + 1, {});
+        for (int b = 0; b <= nbranch; ++b) br_[b].resize(b == 0 ? std::min(split > 0 ? split : D, D) : std::max(D - split, 0));
+        const int NL = D * (nbranch + 1);
+        auto li = [&](int b, int dep) { return b * D + dep; };
+        std::vector<Level> lvs(NL);
+        std::vector<std::vector<NodeDev>> wp(NL), md(NL);
+        std::vector<std::vector<Task>> f1(NL), f2(NL), bw(NL);
         size_t max_smem = 0;
         const long long midData = env_int("HTG_ND_MIDDATA", 16384);
         for (int i = 0; i < nn; ++i) {
-            const int dep = t.nodes[i].depth;
+            const int dep = t.nodes[i].depth, k = li(branch[i], dep);
             const NodeDev& d = nd[i];
-            Level& lv = levels_[dep];
+            Level& lv = lvs[k];
             const int F = d.s + d.u;
             if (F <= warpF) {
-                wp[dep].push_back(d);
+                wp[k].push_back(d);
             } else if ((long long)d.s * F <= midData) {
-                md[dep].push_back(d);
-                bw[dep].push_back({d, 0, d.s});
+                md[k].push_back(d);
+                bw[k].push_back({d, 0, d.s});
                 lv.smem_mid = std::max(lv.smem_mid, size_t(F + d.s) * sizeof(double2));
                 lv.smem_b = std::max(lv.smem_b, size_t(F + d.s) * sizeof(double2));
             } else {
                 const int rpt = env_int("HTG_ND_RPT", 8);
                 for (int r = 0; r < d.s; r += rpt) {
-                    f1[dep].push_back({d, r, std::min(rpt, d.s - r)});
-                    bw[dep].push_back({d, r, std::min(rpt, d.s - r)});
+                    f1[k].push_back({d, r, std::min(rpt, d.s - r)});
+                    bw[k].push_back({d, r, std::min(rpt, d.s - r)});
                 }
-                for (int r = 0; r < d.u; r += rpt) f2[dep].push_back({d, r, std::min(rpt, d.u - r)});
+                for (int r = 0; r < d.u; r += rpt) f2[k].push_back({d, r, std::min(rpt, d.u - r)});
                 lv.smem_big = std::max(lv.smem_big, size_t(F) * sizeof(double2));
                 lv.smem_b = std::max(lv.smem_b, size_t(F + rpt) * sizeof(double2));
             }
         }
-        for (int L = 0; L < D; ++L) {
-            Level& lv = levels_[L];
-            lv.nwarp = int(wp[L].size());
-            lv.nmid = int(md[L].size());
-            lv.nf1 = int(f1[L].size());
-            lv.nf2 = int(f2[L].size());
-            lv.nb = int(bw[L].size());
-            lv.warp = up(wp[L], st);
-            lv.mid = up(md[L], st);
-            lv.f1 = up(f1[L], st);
-            lv.f2 = up(f2[L], st);
-            lv.b = up(bw[L], st);
-            max_smem = std::max({max_smem, lv.smem_mid, lv.smem_big, lv.smem_b});
+        for (int b = 0; b <= nbranch; ++b)
+            for (int dep = 0; dep < D; ++dep) {
+                const int k = li(b, dep);
+                const int L = b == 0 ? dep : dep - split;  // level index inside the branch
+                if (L < 0 || L >= int(br_[b].size())) {
+                    if (!wp[k].empty() || !md[k].empty() || !f1[k].empty() || !bw[k].empty())
+                        throw RuntimeError("coarse solve: front outside its branch's level range");
+                    continue;
+                }
+                Level& lv = lvs[k];
+                lv.nwarp = int(wp[k].size());
+                lv.nmid = int(md[k].size());
+                lv.nf1 = int(f1[k].size());
+                lv.nf2 = int(f2[k].size());
+                lv.nb = int(bw[k].size());
+                lv.warp = up(wp[k], st);
+                lv.mid = up(md[k], st);
+                lv.f1 = up(f1[k], st);
+                lv.f2 = up(f2[k], st);
+                lv.b = up(bw[k], st);
+                max_smem = std::max({max_smem, lv.smem_mid, lv.smem_big, lv.smem_b});
+                br_[b][L] = lv;
+            }
+        for (int b = 0; b < nbranch; ++b) {
+            cudaStream_t x;
+            cudaEvent_t e;
+            HTG_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+            HTG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            bst_.push_back(x);
+            ev_join_.push_back(e);
         }
+        HTG_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
         if (max_smem > 227 * 1024) throw InvalidArgument("coarse front too large for shared memory");
         if (max_smem > 48 * 1024) {
             HTG_CUDA(cudaFuncSetAttribute(k_nd_fwd_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, int(max_smem)));
