@@ -541,7 +541,9 @@ constexpr int kKCCtasPerSM = HTG_KC_CPS;             // resident CTAs per SM the
 #endif
 constexpr int kKCU = HTG_KC_USLOTS, kKCF = 6 - HTG_KC_USLOTS;
 constexpr int kKCGroupWarps = (kKCCells + 31) / 32;  // warps per group
-constexpr int kKCThreads = 2 * 32 * kKCGroupWarps;   // two warp groups
+#ifndef HTG_KC_G3
+#define HTG_KC_G3 0
+#endif
 
 template <int P>
 struct KCCfg {
@@ -549,7 +551,11 @@ struct KCCfg {
     static constexpr int H = 2;                  // halo cells on the left (restrict mode needs 2)
     static constexpr int C = kKCCells - H - 1;   // owned cells per strip (one slot left for x = nx)
     static constexpr int NU = kKCCells + 1;      // staged units per row: cells + right neighbour
-    static constexpr int NR = B - 2 > 2 ? B - 2 : 2;  // most node rows of one group
+    // warp groups: node rows {0,1} | {2..p} or, with three groups at p = 4,
+    // {0,1} | {2,3} | {4} (12 warps, fewer registers per thread)
+    static constexpr int NG = (HTG_KC_G3 && P == 4) ? 3 : 2;
+    static constexpr int NT = NG * 32 * kKCGroupWarps;  // threads per CTA
+    static constexpr int NR = NG == 3 ? 2 : (B - 2 > 2 ? B - 2 : 2);  // most node rows of one group
     static constexpr int UB = P * P * 16;             // unit bytes
     static constexpr int RB = UB < 128 ? UB : 128;    // tensor-map sub-row bytes (= swizzle span)
     static constexpr int RPU = UB / RB;               // sub-rows per unit
@@ -563,9 +569,9 @@ struct __align__(1024) KCSmem {
     using C = KCCfg<P>;
     double2 U[kKCU][C::SLOT / 16];  // u rows y, y+1 (the cell row) and the prefetched rows
     double2 F[kKCF][C::SLOT / 16];  // f row y (r written in place) and f(y+1) in flight
-    double2 X[2][2][kKCCells][C::NR];    // right-column exchange [row parity][group]
+    double2 X[2][C::NG][kKCCells][C::NR];  // right-column exchange [row parity][group]
     double2 XP[kKCCells][C::MM + 1];     // restriction partials exchange
-    double red[kKCThreads];
+    double red[C::NT];
     unsigned long long barU[kKCU], barF[kKCF];
 };
 
@@ -599,8 +605,8 @@ template <int P, int MODE, int GRP, bool DIR>
 __device__ __forceinline__ void k1c_body(const K1Args& a, const CUtensorMap* tmu, const CUtensorMap* tmf,
                                          KCSmem<P>& sm, int ct) {
     using Cf = KCCfg<P>;
-    constexpr int B = Cf::B, MM = Cf::MM, NT = kKCThreads;
-    constexpr int R0 = GRP == 0 ? 0 : 2, R1 = GRP == 0 ? 2 : B, NRG = R1 - R0;  // node rows of this group
+    constexpr int B = Cf::B, MM = Cf::MM, NT = Cf::NT;
+    constexpr int R0 = GRP * 2, R1 = (GRP == Cf::NG - 1) ? B : R0 + 2, NRG = R1 - R0;  // node rows of this group
     constexpr int SL = P / 2 - 1;  // basis table slot
     constexpr int EDGE = Cf::BOX / 16;  // double2 offset of the x = nx unit inside a slot
     const FineGeom& g = a.g;
@@ -977,7 +983,7 @@ __device__ __forceinline__ void k1c_body(const K1Args& a, const CUtensorMap* tmu
 }
 
 template <int P, int MODE, bool DIR>
-__global__ void __launch_bounds__(kKCThreads, kKCCtasPerSM)
+__global__ void __launch_bounds__(KCCfg<P>::NT, kKCCtasPerSM)
     k1_cells(const __grid_constant__ K1Args a, const __grid_constant__ CUtensorMap tmu,
              const __grid_constant__ CUtensorMap tmf) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -989,9 +995,16 @@ __global__ void __launch_bounds__(kKCThreads, kKCCtasPerSM)
     // four schedulers by warp index mod 4, so each scheduler runs one group's
     // code only (the two unrolled bodies would otherwise thrash its icache).
     const int w = threadIdx.x >> 5;
-    const int ct = (w >> 1) * 32 + (threadIdx.x & 31);
-    if ((w & 1) == 0) k1c_body<P, MODE, 0, DIR>(a, &tmu, &tmf, sm, ct);
-    else k1c_body<P, MODE, 1, DIR>(a, &tmu, &tmf, sm, ct);
+    if constexpr (KCCfg<P>::NG == 3) {  // group = w / 4: every scheduler runs one warp of each group
+        const int ct = (w % kKCGroupWarps) * 32 + (threadIdx.x & 31), gsel = w / kKCGroupWarps;
+        if (gsel == 0) k1c_body<P, MODE, 0, DIR>(a, &tmu, &tmf, sm, ct);
+        else if (gsel == 1) k1c_body<P, MODE, 1, DIR>(a, &tmu, &tmf, sm, ct);
+        else k1c_body<P, MODE, 2, DIR>(a, &tmu, &tmf, sm, ct);
+    } else {
+        const int ct = (w >> 1) * 32 + (threadIdx.x & 31);
+        if ((w & 1) == 0) k1c_body<P, MODE, 0, DIR>(a, &tmu, &tmf, sm, ct);
+        else k1c_body<P, MODE, 1, DIR>(a, &tmu, &tmf, sm, ct);
+    }
 }
 
 }  // namespace htg
@@ -1080,7 +1093,7 @@ static void kc_launch_dir(const K1Args& a, cudaStream_t st) {
         attr = true;
     }
     const CUtensorMap tmu = kc_tensor_map<P>(a.g, a.u), tmf = kc_tensor_map<P>(a.g, a.f);
-    k1_cells<P, MODE, DIR><<<grid, kKCThreads, smem, st>>>(a, tmu, tmf);
+    k1_cells<P, MODE, DIR><<<grid, KCCfg<P>::NT, smem, st>>>(a, tmu, tmf);
 }
 
 template <int P, int MODE>
