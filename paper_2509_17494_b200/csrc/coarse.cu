@@ -457,7 +457,7 @@ class NDSolver : public CoarseSolver {
             }
             for (int k = 0; k < n.F; ++k) rpos[n.rows[k]] = -1;
         }
-        const int warpF = std::min(kWarpFMax, env_int("HTG_ND_WARPF", 64));
+        const int warpF = std::min(kWarpFMax, env_int("HTG_ND_WARPF", 96));
         void* facp = nullptr;
         HTG_CUDA(cudaMalloc(&facp, std::max<long long>(1, fac_total) * sizeof(double2)));
         allocs_.push_back(facp);
@@ -495,10 +495,10 @@ class NDSolver : public CoarseSolver {
         args_.front = up(std::vector<double2>(std::max(front_total, 1)), st);
         args_.Y = up(std::vector<double2>(nv_), st);
         // Branches: the subtrees rooted at the nodes of depth `split` (env
-        // HTG_ND_SPLIT, default 3: eight subtrees) run on their own streams; the
+        // HTG_ND_SPLIT, default 4: sixteen subtrees) run on their own streams; the
         // levels above them are branch 0. Per (branch, depth): warp tier, CTA
         // tier, large tier (8 rows per CTA task).
-        const int split = std::max(0, env_int("HTG_ND_SPLIT", 3));
+        const int split = std::max(0, env_int("HTG_ND_SPLIT", 4));
         std::vector<int> branch(nn, 0);
         int nbranch = 0;
         {
