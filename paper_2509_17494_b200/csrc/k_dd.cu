@@ -295,6 +295,30 @@ DDDevice upload_dd_impl(const DDSetup& dd, const HostProblem& hp, std::vector<vo
             f.Vx = put(vx);
             f.Vy = put(vy);
             f.Dinv = put(dv);
+            {  // relative gather offsets, shared by every member of the class (checked)
+                const int nx = f.nx, ny = f.ny;
+                std::vector<int> go(size_t(nx) * ny);
+                bool same = true;
+                for (size_t m = 0; m < subs[ci].size() && same; ++m) {
+                    const int sI = subs[ci][m];
+                    const int gx0 = dd.sub_ox[sI] * p, gy0 = dd.sub_oy[sI] * p;
+                    const long long base = dof_index(hp.nx, hp.ny, p, gx0, gy0);
+                    for (int iy = 0; iy < ny && same; ++iy)
+                        for (int ix = 0; ix < nx; ++ix) {
+                            const int o = int(dof_index(hp.nx, hp.ny, p, gx0 + ix, gy0 + iy) - base);
+                            if (m == 0) go[size_t(iy) * nx + ix] = o;
+                            else if (go[size_t(iy) * nx + ix] != o) { same = false; break; }
+                        }
+                }
+                if (same) {
+                    void* ptr = nullptr;
+                    HTG_CUDA(cudaMalloc(&ptr, go.size() * sizeof(int)));
+                    allocs.push_back(ptr);
+                    bytes += go.size() * sizeof(int);
+                    HTG_CUDA(cudaMemcpy(ptr, go.data(), go.size() * sizeof(int), cudaMemcpyHostToDevice));
+                    f.goff = static_cast<const int*>(ptr);
+                }
+            }
             fdm.push_back(f);
             continue;
         }

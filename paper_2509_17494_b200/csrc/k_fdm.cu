@@ -276,12 +276,15 @@ __global__ void __launch_bounds__(kFThreads, 1) k_dd_fdm(FineGeom g, const FdmCl
             fac[i] = v;
         }
         for (int i = tid; i < nx * ny; i += kFThreads) D[i] = c.Dinv[i];
-        // U row of each (ixu, iyu) of U
+        // U row of each (ixu, iyu) of U, and the class's relative gather offsets
         int* urow = reinterpret_cast<int*>(D + nx * ny) + kFGroups * 16;
         for (int i = tid; i < nux * nuy; i += kFThreads) {
             const int ixu = i / nuy, iyu = i - ixu * nuy;
             urow[i] = c.rowmap[dof_index(c.onx, c.ony, P, c.ux0 + ixu, c.uy0 + iyu)];
         }
+        int* gofs = urow + nux * nuy;
+        if (c.goff)
+            for (int i = tid; i < nx * ny; i += kFThreads) gofs[i] = c.goff[i];
         __syncthreads();
         const int S = min(8, rows / max(nx, ny));  // subdomains per batch
         const int nxy = nx * ny;
@@ -296,9 +299,17 @@ __global__ void __launch_bounds__(kFThreads, 1) k_dd_fdm(FineGeom g, const FdmCl
                 const int so = c.sub_o[c.subs[b0 - c.first + s]];
                 const int ox = (so & 0xffff) * P, oy = (so >> 16) * P;
                 double2* xs = X + s * ny * LD;
-                for (int l = gt; l < nxy; l += 128) {
-                    const int iy = fdiv(l, inv_nx), ix = l - iy * nx;
-                    cp_async16(&xs[iy * LD + ix], r + dof_index(g.nx, g.ny, P, ox + ix, oy + iy));
+                if (c.goff) {
+                    const double2* rb = r + dof_index(g.nx, g.ny, P, ox, oy);
+                    for (int l = gt; l < nxy; l += 128) {
+                        const int iy = fdiv(l, inv_nx), ix = l - iy * nx;
+                        cp_async16(&xs[iy * LD + ix], rb + gofs[l]);
+                    }
+                } else {
+                    for (int l = gt; l < nxy; l += 128) {
+                        const int iy = fdiv(l, inv_nx), ix = l - iy * nx;
+                        cp_async16(&xs[iy * LD + ix], r + dof_index(g.nx, g.ny, P, ox + ix, oy + iy));
+                    }
                 }
             }
             asm volatile("cp.async.commit_group;\n" ::: "memory");
@@ -404,7 +415,8 @@ std::vector<int4> fdm_plan(std::vector<FdmClassDev>& cls, int p, int nsm, FdmLau
     for (auto& c : cls) {
         c.first = total;
         total += c.nsub;
-        fac = std::max(fac, (c.nx + c.ny + c.nux + c.nuy) * LD + c.nx * c.ny + (kFGroups * 16 + c.nux * c.nuy + 3) / 4);
+        fac = std::max(fac, (c.nx + c.ny + c.nux + c.nuy) * LD + c.nx * c.ny +
+                                (kFGroups * 16 + c.nux * c.nuy + c.nx * c.ny + 3) / 4);
         ext = std::max({ext, c.nx, c.ny});
     }
     fac = (fac + 7) / 8 * 8;

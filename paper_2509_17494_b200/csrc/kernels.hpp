@@ -87,6 +87,8 @@ struct FdmClassDev {
     const int* rowmap;  // local Omega dof -> U row
     const int* subs;    // subdomains of the class
     const int* sub_o;   // Omega origin per subdomain
+    const int* goff;    // gather offsets: tile element iy * nx + ix -> dof offset from the
+                        // subdomain's first dof (identical for every member), or null
     int nsub;
     int first;          // offset of this class in the class-sorted subdomain list
 };
