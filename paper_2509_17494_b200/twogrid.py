@@ -71,10 +71,12 @@ class Problem:
     eps_cells: np.ndarray
     side_tags: tuple
     rhs: np.ndarray = field(repr=False)
+    ny: int | None = None  # cells in y (None: n_cells, the unit square of build_problem)
 
     @property
     def ndof(self) -> int:
-        return (self.n_cells * self.order + 1) ** 2
+        ny = self.ny or self.n_cells
+        return (self.n_cells * self.order + 1) * (ny * self.order + 1)
 
 
 def dof_index(nx: int, ny: int, p: int, gx, gy):
@@ -185,7 +187,7 @@ class TwoGridOperators:
         self._k = np.ascontiguousarray(problem.k_cells, dtype=np.float64)
         self._e = np.ascontiguousarray(problem.eps_cells, dtype=np.float64)
         n = problem.n_cells
-        cp = _lib.Problem(problem.order, n, n, problem.h, problem.k, 0.0,
+        cp = _lib.Problem(problem.order, n, problem.ny or n, problem.h, problem.k, 0.0,
                           self._k.ctypes.data_as(C.POINTER(C.c_double)),
                           self._e.ctypes.data_as(C.POINTER(C.c_double)),
                           (C.c_int * 4)(*problem.side_tags), None, None, None, None)
