@@ -63,7 +63,10 @@ struct NDArgs {
 // consecutive entries of a row and consecutive groups consecutive rows, so a
 // warp's loads are contiguous even for short rows. out(r, value) on the
 // group's first lane. warps/nw: this warp's index among the nw warps sharing the rows.
-template <class Out>
+// TRI: 0 dense; 1 lower triangular (row r has nonzeros k <= r: L^-1 P); 2 upper
+// triangular (k >= r: U^-1). The zero half of a triangular block is neither read
+// nor multiplied.
+template <int TRI = 0, class Out>
 __device__ __forceinline__ void rows_dot(const double2* __restrict__ M, int len, const double2* v, int r0, int r1,
                                          int warp, int nw, int lane, Out&& out) {
     int G = 32;
@@ -85,8 +88,11 @@ __device__ __forceinline__ void rows_dot(const double2* __restrict__ M, int len,
         // single long row (large-tier tasks), so the loop must keep several
         // DRAM loads in flight per lane
         constexpr int KU = HTG_ND_KU;
-        int k = gl;
-        for (; k + (KU - 1) * G < len; k += KU * G) {
+        const int rlast = min(rr[U - 1], r1 - 1);
+        const int kend = TRI == 1 ? min(len, rlast + 1) : len;
+        int k = TRI == 2 ? (rr[0] / G) * G + gl : gl;
+        auto live = [&](int q, int kk) { return rr[q] < r1 && (TRI != 1 || kk <= rr[q]) && (TRI != 2 || kk >= rr[q]); };
+        for (; k + (KU - 1) * G < kend; k += KU * G) {
             double2 m[U][KU], vk[KU];
 #pragma unroll
             for (int j = 0; j < KU; ++j) vk[j] = v[k + j * G];
@@ -94,17 +100,17 @@ __device__ __forceinline__ void rows_dot(const double2* __restrict__ M, int len,
             for (int q = 0; q < U; ++q)
 #pragma unroll
                 for (int j = 0; j < KU; ++j)
-                    m[q][j] = rr[q] < r1 ? M[(size_t)rr[q] * len + k + j * G] : make_double2(0.0, 0.0);
+                    m[q][j] = live(q, k + j * G) ? M[(size_t)rr[q] * len + k + j * G] : make_double2(0.0, 0.0);
 #pragma unroll
             for (int q = 0; q < U; ++q)
 #pragma unroll
                 for (int j = 0; j < KU; ++j) acc[q] = cfma(m[q][j], vk[j], acc[q]);
         }
-        for (; k < len; k += G) {
+        for (; k < kend; k += G) {
             const double2 vk = v[k];
 #pragma unroll
             for (int q = 0; q < U; ++q)
-                if (rr[q] < r1) acc[q] = cfma(M[(size_t)rr[q] * len + k], vk, acc[q]);
+                if (live(q, k)) acc[q] = cfma(M[(size_t)rr[q] * len + k], vk, acc[q]);
         }
 #pragma unroll
         for (int q = 0; q < U; ++q) {
@@ -121,7 +127,7 @@ __device__ __forceinline__ void rows_dot(const double2* __restrict__ M, int len,
 // row: lanes (i, part) with i = lane % R accumulate the k = part (mod S) terms
 // of row i, S = 32 / R parts combined with S - 1 shuffles. Column reads are
 // coalesced and there is no per-row reduction tree (short rows).
-template <class Out>
+template <int TRI = 0, class Out>
 __device__ __forceinline__ void cols_dot(const double2* __restrict__ M, int rows, int len, const double2* v, int lane,
                                          Out&& out) {
     int R = 32;
@@ -133,8 +139,11 @@ __device__ __forceinline__ void cols_dot(const double2* __restrict__ M, int rows
         const int i = rb + i0;
         double2 acc = make_double2(0.0, 0.0);
         if (i < rows) {
+            // triangular blocks: lane row i only walks its nonzero columns
+            const int kb = TRI == 2 ? part + ((max(i - part, 0) + S - 1) / S) * S : part;
+            const int ke = TRI == 1 ? min(len, i + 1) : len;
 #pragma unroll 4
-            for (int k = part; k < len; k += S) acc = cfma(M[(size_t)k * rows + i], v[k], acc);
+            for (int k = kb; k < ke; k += S) acc = cfma(M[(size_t)k * rows + i], v[k], acc);
         }
         for (int o = R; o < 32; o <<= 1) {
             acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
@@ -178,7 +187,7 @@ __global__ void __launch_bounds__(kCT) k_nd_fwd_warp(const NodeDev* __restrict__
     double2* v = sv[w];
     double2* y = sy[w];
     gather_front<32>(a, nd, v, lane, [] { __syncwarp(); });
-    cols_dot(a.fac + nd.off_F, nd.s, nd.s, v, lane, [&](int r, double2 acc) {
+    cols_dot<1>(a.fac + nd.off_F, nd.s, nd.s, v, lane, [&](int r, double2 acc) {
         y[r] = acc;
         a.Y[a.idx[nd.off_var + r]] = acc;
     });
@@ -197,7 +206,7 @@ __global__ void __launch_bounds__(kCT) k_nd_fwd_mid(const NodeDev* __restrict__ 
     double2* y = smem + nd.s + nd.u;
     gather_front<kCT>(a, nd, v, threadIdx.x, [] { __syncthreads(); });
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    rows_dot(a.fac + nd.off_F, nd.s, v, 0, nd.s, warp, kCT / 32, lane, [&](int r, double2 acc) {
+    rows_dot<1>(a.fac + nd.off_F, nd.s, v, 0, nd.s, warp, kCT / 32, lane, [&](int r, double2 acc) {
         y[r] = acc;
         a.Y[a.idx[nd.off_var + r]] = acc;
     });
@@ -217,7 +226,7 @@ __global__ void __launch_bounds__(kCT) k_nd_fwd1(const Task* tasks, NDArgs a) {
     if (tk.r0 == 0)
         for (int i = nd.s + threadIdx.x; i < nd.s + nd.u; i += kCT) a.front[nd.off_front + i] = smem[i];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    rows_dot(a.fac + nd.off_F, nd.s, smem, tk.r0, tk.r0 + tk.nr, warp, kCT / 32, lane,
+    rows_dot<1>(a.fac + nd.off_F, nd.s, smem, tk.r0, tk.r0 + tk.nr, warp, kCT / 32, lane,
              [&](int r, double2 acc) { a.Y[a.idx[nd.off_var + r]] = acc; });
 }
 
@@ -244,7 +253,7 @@ __device__ __forceinline__ void bwd_rows(const NDArgs& a, const NodeDev& nd, con
         rows_dot(a.fac + nd.off_Z, nd.u, x2, r0, r1, warp, nw, lane, [&](int r, double2 acc) { sz[r - r0] = acc; });
         sync();
     }
-    rows_dot(a.fac + nd.off_U, nd.s, y1, r0, r1, warp, nw, lane, [&](int r, double2 acc) {
+    rows_dot<2>(a.fac + nd.off_U, nd.s, y1, r0, r1, warp, nw, lane, [&](int r, double2 acc) {
         if (nd.u > 0) {
             acc.x -= sz[r - r0].x;
             acc.y -= sz[r - r0].y;
@@ -274,7 +283,7 @@ __global__ void __launch_bounds__(kCT) k_nd_bwd_warp(const NodeDev* __restrict__
         cols_dot(a.fac + nd.off_Z, nd.s, nd.u, v + nd.s, lane, [&](int r, double2 acc) { z[r] = acc; });
         __syncwarp();
     }
-    cols_dot(a.fac + nd.off_U, nd.s, nd.s, v, lane, [&](int r, double2 acc) {
+    cols_dot<2>(a.fac + nd.off_U, nd.s, nd.s, v, lane, [&](int r, double2 acc) {
         if (nd.u > 0) {
             acc.x -= z[r].x;
             acc.y -= z[r].y;
