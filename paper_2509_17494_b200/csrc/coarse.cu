@@ -156,8 +156,8 @@ __device__ __forceinline__ void cols_dot(const double2* __restrict__ M, int rows
 // front vector v = [rc(vars); 0] + the children's contribution vectors (each
 // position has at most two, added in child order), one pass, no barrier inside
 template <int STRIDE, class Sync>
-__device__ void gather_front(const NDArgs& a, const NodeDev& nd, double2* sv, int t, Sync&& sync) {
-    const int F = nd.s + nd.u;
+__device__ void gather_front(const NDArgs& a, const NodeDev& nd, double2* sv, int t, Sync&& sync, int gend = -1) {
+    const int F = gend >= 0 ? gend : nd.s + nd.u;  // positions [0, gend) only, when given
 #pragma unroll 4
     for (int i = t; i < F; i += STRIDE) {
         const int ri = a.idx[nd.off_rc + i];
@@ -222,7 +222,10 @@ __global__ void __launch_bounds__(kCT) k_nd_fwd1(const Task* tasks, NDArgs a) {
     extern __shared__ double2 smem[];
     const Task tk = tasks[blockIdx.x];
     const NodeDev nd = tk.nd;
-    gather_front<kCT>(a, nd, smem, threadIdx.x, [] { __syncthreads(); });
+    // rows [r0, r0 + nr) of the lower-triangular L^-1 P read v[0, r0 + nr) only; the
+    // r0 == 0 task also stashes v2 for the contribution tasks
+    gather_front<kCT>(a, nd, smem, threadIdx.x, [] { __syncthreads(); },
+                      tk.r0 == 0 ? nd.s + nd.u : min(nd.s, tk.r0 + tk.nr));
     if (tk.r0 == 0)
         for (int i = nd.s + threadIdx.x; i < nd.s + nd.u; i += kCT) a.front[nd.off_front + i] = smem[i];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -300,8 +303,10 @@ __global__ void __launch_bounds__(kCT) k_nd_bwd(const Task* tasks, NDArgs a) {
     double2* y1 = smem;
     double2* x2 = smem + nd.s;
     double2* sz = smem + nd.s + nd.u;
+    // the upper-triangular U^-1 rows [r0, ..) read y1[k >= r0] (from the 32-aligned
+    // block the row dots start at)
 #pragma unroll 4
-    for (int i = threadIdx.x; i < nd.s; i += kCT) y1[i] = a.Y[a.idx[nd.off_var + i]];
+    for (int i = (tk.r0 & ~31) + threadIdx.x; i < nd.s; i += kCT) y1[i] = a.Y[a.idx[nd.off_var + i]];
 #pragma unroll 4
     for (int i = threadIdx.x; i < nd.u; i += kCT) x2[i] = a.X[a.idx[nd.off_ring + i]];
     __syncthreads();
