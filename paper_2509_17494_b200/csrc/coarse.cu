@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(kCT) k_nd_fwd_mid(const NodeDev* __restrict__ 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     rows_dot<1>(a.fac + nd.off_F, nd.s, v, 0, nd.s, warp, kCT / 32, lane, [&](int r, double2 acc) {
         y[r] = acc;
-        a.Y[a.idx[nd.off_var + r]] = acc;
+        a.front[nd.off_front + r] = acc;  // y1, contiguous, for the backward pass
     });
     __syncthreads();
     rows_dot(a.fac + nd.off_L, nd.s, y, 0, nd.u, warp, kCT / 32, lane, [&](int r, double2 acc) {
@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(kCT) k_nd_fwd1(const Task* tasks, NDArgs a) {
         for (int i = nd.s + threadIdx.x; i < nd.s + nd.u; i += kCT) a.front[nd.off_front + i] = smem[i];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     rows_dot<1>(a.fac + nd.off_F, nd.s, smem, tk.r0, tk.r0 + tk.nr, warp, kCT / 32, lane,
-             [&](int r, double2 acc) { a.Y[a.idx[nd.off_var + r]] = acc; });
+             [&](int r, double2 acc) { a.front[nd.off_front + r] = acc; });
 }
 
 // forward, large tier phase 2: contribution rows c = v2 - L21 y1
@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(kCT) k_nd_fwd2(const Task* tasks, NDArgs a) {
     const Task tk = tasks[blockIdx.x];
     const NodeDev nd = tk.nd;
 #pragma unroll 4
-    for (int i = threadIdx.x; i < nd.s; i += kCT) smem[i] = a.Y[a.idx[nd.off_var + i]];
+    for (int i = threadIdx.x; i < nd.s; i += kCT) smem[i] = a.front[nd.off_front + i];
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     rows_dot(a.fac + nd.off_L, nd.s, smem, tk.r0, tk.r0 + tk.nr, warp, kCT / 32, lane, [&](int r, double2 acc) {
@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(kCT) k_nd_bwd(const Task* tasks, NDArgs a) {
     // the upper-triangular U^-1 rows [r0, ..) read y1[k >= r0] (from the 32-aligned
     // block the row dots start at)
 #pragma unroll 4
-    for (int i = (tk.r0 & ~31) + threadIdx.x; i < nd.s; i += kCT) y1[i] = a.Y[a.idx[nd.off_var + i]];
+    for (int i = (tk.r0 & ~31) + threadIdx.x; i < nd.s; i += kCT) y1[i] = a.front[nd.off_front + i];
 #pragma unroll 4
     for (int i = threadIdx.x; i < nd.u; i += kCT) x2[i] = a.X[a.idx[nd.off_ring + i]];
     __syncthreads();
