@@ -326,6 +326,9 @@ def run_ours(args):
                    "l2": "flushed (256 MB write) before every timed step"},
         "s_per_two_grid_iteration": s_per_iter,
         "kernel_ms": {k: round(v, 5) for k, v in prof.items()},
+        "kernel_ms_note": "*_graph entries replay the CUDA graph the public entry points use; the plain "
+                          "smoother_sweep / two_grid_step / coarse_solve entries launch every kernel from the "
+                          "host (the coarse solve's 16 subtree branches make that launch-bound)",
         "coarse_solve_ms": prof["coarse_solve_graph"],
         "roofline_dense_gemm": dense,
         "roofline": {"bound": "tensor",
