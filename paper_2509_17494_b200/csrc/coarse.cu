@@ -341,19 +341,28 @@ class NDSolver : public CoarseSolver {
         a.rc = rc;
         a.X = uc;
         const int nb = int(br_.size()) - 1;  // branch 0: the top levels
+#ifdef HTG_ND_TIMING_SKIP
+        static const int skip = env_int("HTG_ND_SKIP", 0);  // timing experiments only: 1 branches, 2 top
+#else
+        constexpr int skip = 0;
+#endif
         HTG_CUDA(cudaEventRecord(ev_fork_, st));
         for (int b = 1; b <= nb; ++b) {
             HTG_CUDA(cudaStreamWaitEvent(bst_[b - 1], ev_fork_, 0));
-            for (int L = int(br_[b].size()) - 1; L >= 0; --L) fwd_level(br_[b][L], a, bst_[b - 1]);
+            if (skip != 1)
+                for (int L = int(br_[b].size()) - 1; L >= 0; --L) fwd_level(br_[b][L], a, bst_[b - 1]);
             HTG_CUDA(cudaEventRecord(ev_join_[b - 1], bst_[b - 1]));
         }
         for (int b = 1; b <= nb; ++b) HTG_CUDA(cudaStreamWaitEvent(st, ev_join_[b - 1], 0));
-        for (int L = int(br_[0].size()) - 1; L >= 0; --L) fwd_level(br_[0][L], a, st);
-        for (int L = 0; L < int(br_[0].size()); ++L) bwd_level(br_[0][L], a, st);
+        if (skip != 2) {
+            for (int L = int(br_[0].size()) - 1; L >= 0; --L) fwd_level(br_[0][L], a, st);
+            for (int L = 0; L < int(br_[0].size()); ++L) bwd_level(br_[0][L], a, st);
+        }
         HTG_CUDA(cudaEventRecord(ev_fork_, st));
         for (int b = 1; b <= nb; ++b) {
             HTG_CUDA(cudaStreamWaitEvent(bst_[b - 1], ev_fork_, 0));
-            for (int L = 0; L < int(br_[b].size()); ++L) bwd_level(br_[b][L], a, bst_[b - 1]);
+            if (skip != 1)
+                for (int L = 0; L < int(br_[b].size()); ++L) bwd_level(br_[b][L], a, bst_[b - 1]);
             HTG_CUDA(cudaEventRecord(ev_join_[b - 1], bst_[b - 1]));
         }
         for (int b = 1; b <= nb; ++b) HTG_CUDA(cudaStreamWaitEvent(st, ev_join_[b - 1], 0));
@@ -549,7 +558,7 @@ class NDSolver : public CoarseSolver {
                 lv.smem_mid = std::max(lv.smem_mid, size_t(F + d.s) * sizeof(double2));
                 lv.smem_b = std::max(lv.smem_b, size_t(F + d.s) * sizeof(double2));
             } else {
-                const int rpt = env_int("HTG_ND_RPT", 8);
+                const int rpt = branch[i] == 0 ? env_int("HTG_ND_RPT_TOP", 8) : env_int("HTG_ND_RPT", 8);
                 for (int r = 0; r < d.s; r += rpt) {
                     f1[k].push_back({d, r, std::min(rpt, d.s - r)});
                     bw[k].push_back({d, r, std::min(rpt, d.s - r)});

@@ -5,7 +5,7 @@ set -e
 NAME=$1; shift
 ROOT=$(cd "$(dirname "$0")/.." && pwd)
 SRC=$ROOT/paper_2509_17494_b200/csrc
-OUT=$ROOT/exp/build_$NAME
+OUT=$ROOT/exp/build_$NAME  # object files stay here (.gpurunignore); only exp/$NAME.so travels
 mkdir -p $OUT
 FL="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3,-fcx-limited-range,-march=x86-64-v3 -I$SRC -I$ROOT/include --expt-relaxed-constexpr $*"
 pids=()
