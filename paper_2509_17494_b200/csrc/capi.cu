@@ -6,6 +6,9 @@
 // that is a sequence of stream-ordered kernel launches with no allocation.
 #include <cuda_runtime.h>
 
+#include <chrono>
+#include <cstdio>
+
 #include <cmath>
 #include <complex>
 #include <cstdlib>
@@ -150,7 +153,20 @@ struct htg_handle {
 
 namespace {
 
+// HTG_SETUP_TIMES=1 prints the host setup phases (seconds) to stderr
+struct SetupClock {
+    bool on = std::getenv("HTG_SETUP_TIMES") != nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    void mark(const char* what) {
+        if (!on) return;
+        const auto t1 = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "htg setup: %-28s %8.3f s\n", what, std::chrono::duration<double>(t1 - t0).count());
+        t0 = t1;
+    }
+};
+
 void build_handle(htg_handle* H, const htg_problem& prob, const htg_config& cfg) {
+    SetupClock clk;
     upload_tables_once();
     H->hp = make_problem(prob);
     validate_config(cfg, H->hp);
@@ -210,7 +226,9 @@ void build_handle(htg_handle* H, const htg_problem& prob, const htg_config& cfg)
     HTG_CUDA(cudaMallocHost(&H->hscal, 64 * sizeof(double)));
 
     if (cfg.smoother == HTG_SMOOTHER_CSDD) {
+        clk.mark("problem, vectors");
         DDSetup dd = build_dd(hp, H->basis, cfg.alpha_s, cfg.l_dd);
+        clk.mark("subdomain classes");
         H->nclasses = int(dd.classes.size());
         for (int sI = 0; sI < int(dd.sub_class.size()); ++sI) {
             const DDClass& c = dd.classes[dd.sub_class[sI]];
@@ -235,7 +253,9 @@ void build_handle(htg_handle* H, const htg_problem& prob, const htg_config& cfg)
             H->fdm_launch.nwork = int(work.size());
         }
     }
+    clk.mark("subdomain upload");
     if (cfg.coarsening == HTG_COARSE_OPTIMIZED_FD) H->coarse = make_coarse_solver(hp, st);
+    clk.mark("coarse factor + upload");
     if (cfg.coarsening == HTG_COARSE_GALERKIN_P) {
         // proj/core/src/twogrid.cpp:189-219: order-p/2 space on the same mesh, A_c with
         // alpha_c, IP = inclusion of the hierarchical order-p/2 functions

@@ -2,6 +2,10 @@
 // factors of the QSFEM coarse matrix (factored on the host in coarse_nd.cpp).
 #include <cuda_runtime.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+
 #include <algorithm>
 #include <atomic>
 #include <cstdlib>
@@ -318,7 +322,12 @@ class NDSolver : public CoarseSolver {
     NDSolver(const LatticeMatrix& A, cudaStream_t st) {
         NDTree t;
         const char* pt = std::getenv("HTG_ND_PIVTOL");
+        const auto t0 = std::chrono::steady_clock::now();
         nd_factor(A, t, env_int("HTG_ND_LEAF", 16), pt ? std::atof(pt) : 0.3);
+        if (std::getenv("HTG_SETUP_TIMES"))
+            std::fprintf(stderr, "htg setup:   nested-dissection factor %8.3f s (%d fronts, max front %d)\n",
+                         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(),
+                         int(t.nodes.size()), t.max_front);
         nv_ = t.nv;
         delayed_ = t.delayed;
         upload(t, st);
@@ -419,6 +428,7 @@ class NDSolver : public CoarseSolver {
 
     template <class T>
     T* up(const std::vector<T>& v, cudaStream_t st) {
+        if (v.empty()) return nullptr;  // empty per-(branch, level) lists: nothing to launch
         void* p = nullptr;
         HTG_CUDA(cudaMalloc(&p, std::max<size_t>(1, v.size()) * sizeof(T)));
         allocs_.push_back(p);
@@ -485,13 +495,37 @@ class NDSolver : public CoarseSolver {
         HTG_CUDA(cudaMalloc(&facp, std::max<long long>(1, fac_total) * sizeof(double2)));
         allocs_.push_back(facp);
         bytes_ += fac_total * sizeof(double2);
+        // all factor blocks go through one pinned staging buffer in large chunks
+        // (one cudaMemcpy per block took seconds at cfg4: 4 blocks x 68k fronts)
+        const size_t chunk = size_t(64) << 20;  // bytes
+        cplx* stage = nullptr;
+        HTG_CUDA(cudaMallocHost(&stage, chunk));
+        size_t fill = 0;        // bytes staged
+        long long dst0 = 0;     // factor offset (double2) of the staged run
+        auto flush = [&]() {
+            if (!fill) return;
+            HTG_CUDA(cudaMemcpy(static_cast<double2*>(facp) + dst0, stage, fill, cudaMemcpyHostToDevice));
+            dst0 += (long long)(fill / sizeof(cplx));
+            fill = 0;
+        };
         for (int i = 0; i < nn; ++i) {
             NDNode& n = t.nodes[i];
             const NodeDev& d = nd[i];
+            // blocks are laid out back to back in node order (off_F, off_L, off_U, off_Z)
             auto put = [&](std::vector<cplx>& v, long long off) {
-                if (v.empty()) return;
-                HTG_CUDA(cudaMemcpy(static_cast<double2*>(facp) + off, v.data(), v.size() * sizeof(cplx),
-                                    cudaMemcpyHostToDevice));
+                if (dst0 + (long long)(fill / sizeof(cplx)) != off) {  // keep the staged run contiguous
+                    flush();
+                    dst0 = off;
+                }
+                size_t done = 0;
+                while (done < v.size()) {
+                    const size_t room = (chunk - fill) / sizeof(cplx);
+                    const size_t nput = std::min(room, v.size() - done);
+                    std::memcpy(reinterpret_cast<char*>(stage) + fill, v.data() + done, nput * sizeof(cplx));
+                    fill += nput * sizeof(cplx);
+                    done += nput;
+                    if (fill == chunk) flush();
+                }
                 std::vector<cplx>().swap(v);
             };
             if (d.s + d.u <= warpF) {  // warp tier: column-major blocks (cols_dot)
@@ -511,6 +545,8 @@ class NDSolver : public CoarseSolver {
             put(n.Uinv, d.off_U);
             put(n.Z, d.off_Z);
         }
+        flush();
+        HTG_CUDA(cudaFreeHost(stage));
         args_.fac = static_cast<const double2*>(facp);
         args_.idx = up(idx, st);
         args_.gsrc = up(gsrc, st);

@@ -311,15 +311,6 @@ void gemm_sub(int m, int n, int k, const cplx* A, const cplx* B, cplx* C, int nt
     for (auto& x : th) x.join();
 }
 
-void parallel_rows(int m, int nthreads, const std::function<void(int, int)>& body, size_t work) {
-    if (nthreads <= 1 || work < 2000000) {
-        body(0, m);
-        return;
-    }
-    std::vector<std::thread> th;
-    for (int t = 0; t < nthreads; ++t) th.emplace_back(body, m * t / nthreads, m * (t + 1) / nthreads);
-    for (auto& x : th) x.join();
-}
 
 // Factor one front (children already factored). rpos/cpos: scratch
 // global -> front row / column maps (all -1 on entry and exit).
@@ -381,8 +372,26 @@ void factor_node(NDTree& t, int id, const LatticeMatrix& A, std::vector<int>& rp
         cpos[cols[i]] = -1;
     }
 
+    // Elimination. Large fronts use a team of threads that lives for the whole
+    // front: thread 0 makes the pivot decision (search, delay, swap), then every
+    // thread updates its share of the rows below; two spin barriers per pivot.
     int k = 0, last = sN;  // columns [k, last) are still candidates
-    while (k < last) {
+    const int team = (nthreads > 1 && F >= 192) ? nthreads : 1;
+    std::atomic<int> bar_count{0}, bar_gen{0};
+    auto barrier = [&]() {
+        const int g = bar_gen.load(std::memory_order_acquire);
+        if (bar_count.fetch_add(1, std::memory_order_acq_rel) == team - 1) {
+            bar_count.store(0, std::memory_order_relaxed);
+            bar_gen.store(g + 1, std::memory_order_release);
+        } else {
+            while (bar_gen.load(std::memory_order_acquire) == g) std::this_thread::yield();
+        }
+    };
+    bool done = false;
+    std::exception_ptr err;
+    cplx inv = 0.0;
+    // thread 0: one pivot decision; false when the column was delayed (no update)
+    auto decide = [&]() -> bool {
         int p = k;
         double best = std::abs(Fm[size_t(k) * F + k]);
         for (int i = k + 1; i < sN; ++i) {
@@ -399,26 +408,59 @@ void factor_node(NDTree& t, int id, const LatticeMatrix& A, std::vector<int>& rp
             --last;  // delay column k
             for (int i = 0; i < F; ++i) std::swap(Fm[size_t(i) * F + k], Fm[size_t(i) * F + last]);
             std::swap(cols[k], cols[last]);
-            continue;
+            return false;
         }
         if (p != k) {
             std::swap_ranges(Fm.begin() + size_t(k) * F, Fm.begin() + size_t(k) * F + F, Fm.begin() + size_t(p) * F);
             std::swap(rows[k], rows[p]);
         }
-        const cplx inv = 1.0 / Fm[size_t(k) * F + k];
+        inv = 1.0 / Fm[size_t(k) * F + k];
+        return true;
+    };
+    auto elim = [&](int i0, int i1) {  // rows k + 1 + [i0, i1)
         const cplx* rk = &Fm[size_t(k) * F];
-        auto elim = [&](int i0, int i1) {
-            for (int i = k + 1 + i0; i < k + 1 + i1; ++i) {
-                cplx* ri = &Fm[size_t(i) * F];
-                if (ri[k] == cplx(0.0)) continue;
-                const cplx l = ri[k] * inv;
-                ri[k] = l;
-                for (int j = k + 1; j < F; ++j) ri[j] -= l * rk[j];
+        for (int i = k + 1 + i0; i < k + 1 + i1; ++i) {
+            cplx* ri = &Fm[size_t(i) * F];
+            if (ri[k] == cplx(0.0)) continue;
+            const cplx l = ri[k] * inv;
+            ri[k] = l;
+            for (int j = k + 1; j < F; ++j) ri[j] -= l * rk[j];
+        }
+    };
+    if (team == 1) {
+        while (k < last) {
+            if (!decide()) continue;
+            elim(0, F - k - 1);
+            ++k;
+        }
+    } else {
+        bool piv = false;
+        auto worker = [&](int w) {
+            for (;;) {
+                if (w == 0) {
+                    try {
+                        piv = false;
+                        while (k < last && !(piv = decide())) {
+                        }
+                        done = k >= last;
+                    } catch (...) {
+                        err = std::current_exception();
+                        done = true;
+                    }
+                }
+                barrier();
+                if (done) return;
+                const int nrows = F - k - 1;
+                elim(nrows * w / team, nrows * (w + 1) / team);
+                barrier();
+                if (w == 0) ++k;
             }
         };
-        const int nrows = F - k - 1;
-        parallel_rows(nrows, nthreads, elim, size_t(nrows) * (F - k));
-        ++k;
+        std::vector<std::thread> th;
+        for (int w = 1; w < team; ++w) th.emplace_back(worker, w);
+        worker(0);
+        for (auto& x : th) x.join();
+        if (err) std::rethrow_exception(err);
     }
     const int ke = k, r = F - ke;  // eliminated here / handed to the parent
     n.sN = sN;
@@ -504,9 +546,22 @@ void nd_factor(const LatticeMatrix& A, NDTree& t, int leaf_max, double pivtol) {
             for (auto& x : th) x.join();
             for (auto& e : errs)
                 if (e) std::rethrow_exception(e);
-        } else {
-            std::vector<int> rpos(nv, -1), cpos(nv, -1);
-            for (int id : ids) factor_node(t, id, A, rpos, cpos, pivtol, nthr);
+        } else {  // fewer fronts than threads: all fronts at once, a thread team each
+            const int per = std::max(1, nthr / std::max(1, int(ids.size())));
+            std::vector<std::thread> th;
+            std::vector<std::exception_ptr> errs(ids.size());
+            for (size_t q = 0; q < ids.size(); ++q)
+                th.emplace_back([&, q] {
+                    try {
+                        std::vector<int> rpos(nv, -1), cpos(nv, -1);
+                        factor_node(t, ids[q], A, rpos, cpos, pivtol, per);
+                    } catch (...) {
+                        errs[q] = std::current_exception();
+                    }
+                });
+            for (auto& x : th) x.join();
+            for (auto& e : errs)
+                if (e) std::rethrow_exception(e);
         }
         for (int id : ids) {
             const NDNode& n = t.nodes[id];
