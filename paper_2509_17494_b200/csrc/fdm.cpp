@@ -16,6 +16,7 @@
 #include <complex>
 
 #include "setup.hpp"
+#include "kernels.hpp"
 
 namespace htg {
 
@@ -200,6 +201,12 @@ bool gen_eig(int n, const Mat& K, const std::vector<double>& M, std::vector<cplx
 }
 
 }  // namespace
+
+// 1-D extents the FDM kernel takes (k_fdm.cu: k steps cover 4 KS = 16 at p = 2, 28 at p = 4)
+bool fdm_supported(int p, int nx, int ny) {
+    const int lim = p == 2 ? 16 : (p == 4 ? 28 : 0);
+    return lim > 0 && nx <= lim && ny <= lim;
+}
 
 bool build_fdm(const HostProblem& hp, const Basis1D& b, double alpha_s, int ox, int oy, DDClass& c) {
     const int p = hp.p;

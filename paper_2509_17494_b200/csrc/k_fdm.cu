@@ -378,11 +378,8 @@ int fdm_rows(int fac_elems) {
 
 }  // namespace
 
-bool fdm_supported(int p, int nx, int ny) {
-    if (p == 2) return nx <= 4 * FdmDims<2>::KS && ny <= 4 * FdmDims<2>::KS;
-    if (p == 4) return nx <= 4 * FdmDims<4>::KS && ny <= 4 * FdmDims<4>::KS;
-    return false;
-}
+// fdm_supported (fdm.cpp) admits 1-D extents up to 4 KS
+static_assert(4 * FdmDims<2>::KS == 16 && 4 * FdmDims<4>::KS == 28, "fdm_supported limits out of date");
 
 // One launch for every separable class: CTAs take contiguous ranges of the
 // class-sorted subdomain list (work table built once, fdm_plan).

@@ -1,5 +1,6 @@
 // setup.cpp -- host setup: 1-D basis factors, problem tables, subdomain classes.
 #include "setup.hpp"
+#include "kernels.hpp"
 
 #include <algorithm>
 #include <cmath>
@@ -450,8 +451,11 @@ DDSetup build_dd(const HostProblem& hp, const Basis1D& b, double alpha_s, int l_
             c.B.resize(size_t(c.nu) * n);
             for (int r = 0; r < c.nu; ++r)
                 for (int l = 0; l < n; ++l) c.B[size_t(r) * n + l] = X[size_t(l) * c.nu + r];
+            // fast diagonalisation only where the FDM kernel takes the class (its
+            // validation against B is O(|U| |Omega|^2), seconds for large Omega)
             const char* fdm_env = std::getenv("HTG_FDM");
-            if (!(fdm_env && fdm_env[0] == '0')) c.fdm = build_fdm(hp, b, alpha_s, first[ci].ox, first[ci].oy, c);
+            if (!(fdm_env && fdm_env[0] == '0') && fdm_supported(p, c.onx * p + 1, c.ony * p + 1))
+                c.fdm = build_fdm(hp, b, alpha_s, first[ci].ox, first[ci].oy, c);
         } catch (...) {
             errs[ci] = std::current_exception();
         }
