@@ -209,6 +209,7 @@ int orc_coarse_solve(void* h, const double* rc, double* uc) {
         Session* s = static_cast<Session*>(h);
         const int n = s->ops->cspace.ndof;
         std::memcpy(uc, rc, n * sizeof(cplx));
+        if (!s->ops->Ac_factor) throw std::runtime_error("coarse operator not factored (ORC_NO_COARSE_FACTOR)");
         s->ops->Ac_factor->solve(Cm(uc));
     });
 }

@@ -10,6 +10,8 @@
 
 #include "oracle.hpp"
 
+#include <cstdlib>
+
 namespace orc {
 
 static int floordiv(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
@@ -310,7 +312,10 @@ std::unique_ptr<Ops> setup_two_grid(const Space& s, const Coeffs& c, const Tags&
         ops->ctags = ct;
         ops->Ac = qsfem_assemble(ops->cspace, ops->ccoeffs, ct);
         ops->IP = build_prolongation(s, ops->cspace, s.dirichlet_dofs(t), ops->cspace.dirichlet_dofs(ct));
-        ops->Ac_factor = std::make_unique<BandLU>(ops->Ac);
+        // ORC_NO_COARSE_FACTOR: leave A_c unfactored (full-size checks factor it with
+        // another direct solver, e.g. SuperLU from the exported CSR); coarse_solve
+        // and two_grid_step then raise
+        if (!std::getenv("ORC_NO_COARSE_FACTOR")) ops->Ac_factor = std::make_unique<BandLU>(ops->Ac);
     } else if (cfg.coarsening == Coarse::GalerkinP) {
         // proj/core/src/twogrid.cpp:189-219 (galerkin_p_coarse): the order-p/2 space on
         // the same mesh, its Helmholtz matrix with alpha_c, and IP = the inclusion of the
@@ -362,6 +367,7 @@ void two_grid_step(cvec& u, const cvec& f, const Ops& ops) {
         cvec r(u.size()), rc(ops.cspace.ndof), t(u.size());
         ops.A.residual(f.data(), u.data(), r.data());
         ops.IP.apply_adjoint(r.data(), rc.data());
+        if (!ops.Ac_factor) throw std::runtime_error("coarse operator not factored (ORC_NO_COARSE_FACTOR)");
         ops.Ac_factor->solve(rc.data());
         ops.IP.apply(rc.data(), t.data());
         for (std::size_t j = 0; j < u.size(); ++j) u[j] += ops.cfg.omega_c * t[j];
