@@ -63,3 +63,43 @@ def test_five_two_grid_iterations_match_oracle(W):
         print(f"W={W} iterate {k + 1}: rel l2 diff {err:.2e}, relative residual {rr:.4e} (oracle {want_res[k]:.4e})")
         assert abs(rr - want_res[k]) <= 1e-8 * want_res[k], (k, rr, want_res[k])
     ops.close()
+
+
+@pytest.mark.parametrize("W", [80, 160], ids=["cfg3", "cfg4"])
+def test_richardson_iterations_match_oracle(W):
+    """solve (twogrid.cpp:278-294, Richardson to 1e-6) on the build_problem RHS: the
+    iteration count equals the restated oracle's within +-1 and the solutions agree."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import scipy.sparse.linalg as spla
+    import paper_2509_17494_b200 as hb
+    po.build()
+    po.set_threads(os.cpu_count() or 1)
+    spec = dict(order=4, wavelengths=W, ppw=10)
+    prob = hb.build_problem(hb.ProblemSpec(**spec))
+    ops = hb.setup_two_grid(prob, hb.SolverConfig())
+    res = ops.solve(torch.from_numpy(prob.rhs).cuda())
+    os.environ["ORC_NO_COARSE_FACTOR"] = "1"
+    try:
+        ses = po.Session(po.ProblemSpec(**spec), po.SolverConfig())
+    finally:
+        os.environ.pop("ORC_NO_COARSE_FACTOR", None)
+    lu = spla.splu(ses.csr(2).tocsc(), permc_spec="COLAMD")
+    f = ses.rhs()
+    assert np.array_equal(f, prob.rhs)
+    nf = np.linalg.norm(f)
+    u = np.zeros(ses.ndof, np.complex128)
+    it = 0
+    while it < 200:
+        it += 1
+        u = ses.csdd_smoother(u, f)
+        u = u + ses.apply(3, lu.solve(ses.apply(4, ses.residual(f, u))))
+        u = ses.csdd_smoother(u, f)
+        if np.linalg.norm(ses.residual(f, u)) / nf <= 1e-6:
+            break
+    print(f"W={W}: GPU {res.iterations} iterations, restated oracle {it}")
+    assert res.converged and abs(res.iterations - it) <= 1
+    got = res.u.cpu().numpy()
+    assert np.linalg.norm(got - u) / np.linalg.norm(u) <= 1e-8
+    ops.close()
