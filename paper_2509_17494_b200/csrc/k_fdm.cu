@@ -52,7 +52,7 @@ __device__ __forceinline__ void group_sync(int g) {
 }
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
 // exact floor(n / d) for 0 <= n < 2^16 and small d (margin 0.5 / n >> fp32 rounding)
 __device__ __forceinline__ int fdiv(int n, float inv) { return __float2int_rz((float(n) + 0.5f) * inv); }
