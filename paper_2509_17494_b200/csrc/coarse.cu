@@ -268,7 +268,6 @@ __device__ __forceinline__ void bwd_rows(const NDArgs& a, const NodeDev& nd, con
         a.X[a.idx[nd.off_var + r]] = acc;
     });
 }
-__device__ void sync_warp_fn() { __syncwarp(); }
 __device__ void sync_cta_fn() { __syncthreads(); }
 
 __global__ void __launch_bounds__(kCT) k_nd_bwd_warp(const NodeDev* __restrict__ list, int n, NDArgs a) {

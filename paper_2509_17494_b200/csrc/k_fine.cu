@@ -193,8 +193,8 @@ __device__ __forceinline__ int unit_size(int nx, int ny, int x, int y) {
 template <int P, int MODE>
 __global__ void __launch_bounds__(kK1Threads) k1_residual(K1Args a) {
     using Cf = K1Cfg<P>;
-    constexpr int B = Cf::B, MM = Cf::MM, W = Cf::W;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
+    constexpr int B = Cf::B, MM = Cf::MM;
+    extern __shared__ __align__(16) unsigned char smem_raw[];  // one declaration for all kernels of this file
     K1Smem<P>& sm = *reinterpret_cast<K1Smem<P>*>(smem_raw);
     const FineGeom& g = a.g;
     const int tid = threadIdx.x;
