@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_dd_fdm(FineGeom g, const FdmCl
         }
         for (int i = tid; i < nx * ny; i += kFThreads) D[i] = c.Dinv[i];
         // U row of each (ixu, iyu) of U, and the class's relative gather offsets
-        int* urow = reinterpret_cast<int*>(D + nx * ny) + kFGroups * 16;
+        int* urow = reinterpret_cast<int*>(D + nx * ny) + kFGroups * 32;
         for (int i = tid; i < nux * nuy; i += kFThreads) {
             const int ixu = i / nuy, iyu = i - ixu * nuy;
             urow[i] = c.rowmap[dof_index(c.onx, c.ony, P, c.ux0 + ixu, c.uy0 + iyu)];
@@ -289,14 +289,16 @@ __global__ void __launch_bounds__(kFThreads, 1) k_dd_fdm(FineGeom g, const FdmCl
         const int S = min(8, rows / max(nx, ny));  // subdomains per batch
         const int nxy = nx * ny;
         const float inv_nx = 1.0f / nx, inv_ny = 1.0f / ny, inv_nux = 1.0f / nux;
-        // subdomain ids of the group's batches (double-buffered by batch parity: the
-        // next batch is gathered while stage 4 of the current one still stores)
-        int* sid = reinterpret_cast<int*>(D + nx * ny) + grp * 16;
+        // subdomain ids and origins of the group's batches, double-buffered by batch
+        // parity: the next batch's are loaded into registers under stages 1-3 and
+        // published before the stage-3 barrier, its tile is gathered under stage 4
+        // while stage 4 of the current batch still stores with the current ids
+        int* meta = reinterpret_cast<int*>(D + nx * ny) + grp * 32;  // [parity][sid 8 | origin 8]
+        int* sid = meta;  // sid[parity * 16 + s]
         int par = 0;
-        auto gather = [&](int b0, int nb, int pr) {
-            if (gt < nb) sid[pr * 8 + gt] = c.subs[b0 - c.first + gt];
+        auto gather = [&](int nb, int pr) {
             for (int s = 0; s < nb; ++s) {
-                const int so = c.sub_o[c.subs[b0 - c.first + s]];
+                const int so = meta[pr * 16 + 8 + s];
                 const int ox = (so & 0xffff) * P, oy = (so >> 16) * P;
                 double2* xs = X + s * ny * LD;
                 if (c.goff) {
@@ -323,11 +325,24 @@ __global__ void __launch_bounds__(kFThreads, 1) k_dd_fdm(FineGeom g, const FdmCl
         const int nbatch = R + (tail_n > 0 ? 1 : 0);
         auto bstart = [&](int i) { return i < R ? pos + (i * kFGroups + grp) * S : tail_b; };
         auto bsize = [&](int i) { return i < R ? S : tail_n; };
-        if (nbatch > 0) gather(bstart(0), bsize(0), 0);
+        if (nbatch > 0) {
+            if (gt < bsize(0)) {
+                const int id = c.subs[bstart(0) - c.first + gt];
+                meta[gt] = id;
+                meta[8 + gt] = c.sub_o[id];
+            }
+            group_sync(grp);
+            gather(bsize(0), 0);
+        }
         for (int bi = 0; bi < nbatch; ++bi, par ^= 1) {
-            const int b0 = bstart(bi), nb = bsize(bi);
+            const int nb = bsize(bi);
             asm volatile("cp.async.wait_all;\n" ::: "memory");
             group_sync(grp);
+            int nid = -1, nso = 0;  // next batch, one subdomain per lane gt < its size
+            if (bi + 1 < nbatch && gt < bsize(bi + 1)) {
+                nid = c.subs[bstart(bi + 1) - c.first + gt];
+                nso = c.sub_o[nid];
+            }
             // 1: P[ix'][(s,iy)] = sum_ix Vx[ix][ix'] G_s[ix][iy]  -> W[(s,ix')][iy]
             Stage<LD, KS>{V1T, nx, X, nb * ny, true, q, lane}([&](int m, int n, double2 v) {
                 if (m < nx && n < nb * ny) {
@@ -352,15 +367,19 @@ __global__ void __launch_bounds__(kFThreads, 1) k_dd_fdm(FineGeom g, const FdmCl
                     W[(s * nux + m) * LD + n - s * ny] = v;
                 }
             });
+            if (nid >= 0) {
+                meta[(par ^ 1) * 16 + gt] = nid;
+                meta[(par ^ 1) * 16 + 8 + gt] = nso;
+            }
             group_sync(grp);
             // the gathered tile is free: fetch the group's next batch under stage 4
-            if (bi + 1 < nbatch) gather(bstart(bi + 1), bsize(bi + 1), par ^ 1);
+            if (bi + 1 < nbatch) gather(bsize(bi + 1), par ^ 1);
             // 4: Y[(s,ixu)][iyu] = sum_iy' R[(s,ixu)][iy'] Vy[uy0 + iyu][iy']  -> staging rows
             Stage<LD, KS>{V2U, nuy, W, nb * nux, false, q, lane}(
                 [&](int m, int n, double2 v) {
                     if (m < nb * nux && n < nuy) {
                         const int s = fdiv(m, inv_nux), ixu = m - s * nux;
-                        ystage[(size_t)sid[par * 8 + s] * nu_max + urow[ixu * nuy + n]] = v;
+                        ystage[(size_t)sid[par * 16 + s] * nu_max + urow[ixu * nuy + n]] = v;
                     }
                 });
             // (no barrier here: the next batch's first barrier also orders this
@@ -413,7 +432,7 @@ std::vector<int4> fdm_plan(std::vector<FdmClassDev>& cls, int p, int nsm, FdmLau
         c.first = total;
         total += c.nsub;
         fac = std::max(fac, (c.nx + c.ny + c.nux + c.nuy) * LD + c.nx * c.ny +
-                                (kFGroups * 16 + c.nux * c.nuy + c.nx * c.ny + 3) / 4);
+                                (kFGroups * 32 + c.nux * c.nuy + c.nx * c.ny + 3) / 4);
         ext = std::max({ext, c.nx, c.ny});
     }
     fac = (fac + 7) / 8 * 8;
