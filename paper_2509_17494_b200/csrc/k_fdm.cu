@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 
 #include "common.hpp"
 #include "kernels.hpp"
@@ -251,6 +252,19 @@ __global__ void __launch_bounds__(kFThreads, 1) k_dd_fdm(FineGeom g, const FdmCl
         double2* data = fac + fac_elems;
         for (int i = tid; i < kFGroups * 2 * rows * LD; i += kFThreads) data[i] = make_double2(0.0, 0.0);
     }
+#ifdef HTG_FDM_CLOCKS
+    long long clk_acc[6] = {0, 0, 0, 0, 0, 0}, clk_prev = 0;
+#define HTG_CLK(i)                                  \
+    do {                                            \
+        const long long t_ = clock64();             \
+        if (i > 0) clk_acc[i - 1] += t_ - clk_prev; \
+        clk_prev = t_;                              \
+    } while (0)
+#else
+#define HTG_CLK(i) \
+    do {           \
+    } while (0)
+#endif
     const int4 wk = work[blockIdx.x];  // [first, end) of the class-sorted subdomain list
     int pos = wk.x;
     while (pos < wk.y) {
@@ -297,18 +311,26 @@ __global__ void __launch_bounds__(kFThreads, 1) k_dd_fdm(FineGeom g, const FdmCl
         int* sid = meta;  // sid[parity * 16 + s]
         int par = 0;
         auto gather = [&](int nb, int pr) {
+            // roles 2 and 3 issue the gather (roles 0 and 1 carry the larger share
+            // of stage 4's DMMA tiles; measured 0.216 -> 0.211 ms at cfg4)
+            if (q < 2) {
+                asm volatile("cp.async.commit_group;\n" ::: "memory");
+                return;
+            }
+            const int gt = (q - 2) * 32 + lane;
+            constexpr int kGS = 64;
             for (int s = 0; s < nb; ++s) {
                 const int so = meta[pr * 16 + 8 + s];
                 const int ox = (so & 0xffff) * P, oy = (so >> 16) * P;
                 double2* xs = X + s * ny * LD;
                 if (c.goff) {
                     const double2* rb = r + dof_index(g.nx, g.ny, P, ox, oy);
-                    for (int l = gt; l < nxy; l += 128) {
+                    for (int l = gt; l < nxy; l += kGS) {
                         const int iy = fdiv(l, inv_nx), ix = l - iy * nx;
                         cp_async16(&xs[iy * LD + ix], rb + gofs[l]);
                     }
                 } else {
-                    for (int l = gt; l < nxy; l += 128) {
+                    for (int l = gt; l < nxy; l += kGS) {
                         const int iy = fdiv(l, inv_nx), ix = l - iy * nx;
                         cp_async16(&xs[iy * LD + ix], r + dof_index(g.nx, g.ny, P, ox + ix, oy + iy));
                     }
@@ -336,8 +358,10 @@ __global__ void __launch_bounds__(kFThreads, 1) k_dd_fdm(FineGeom g, const FdmCl
         }
         for (int bi = 0; bi < nbatch; ++bi, par ^= 1) {
             const int nb = bsize(bi);
+            HTG_CLK(0);
             asm volatile("cp.async.wait_all;\n" ::: "memory");
             group_sync(grp);
+            HTG_CLK(1);
             int nid = -1, nso = 0;  // next batch, one subdomain per lane gt < its size
             if (bi + 1 < nbatch && gt < bsize(bi + 1)) {
                 nid = c.subs[bstart(bi + 1) - c.first + gt];
@@ -351,6 +375,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_dd_fdm(FineGeom g, const FdmCl
                 }
             });
             group_sync(grp);
+            HTG_CLK(2);
             // 2: Q[(s,ix')][iy'] = (sum_iy P[(s,ix')][iy] Vy[iy][iy']) Dinv[ix'][iy']  -> X[(s,iy')][ix']
             Stage<LD, KS>{V2T, ny, W, nb * nx, false, q, lane}([&](int m, int n, double2 v) {
                 if (m < nb * nx && n < ny) {
@@ -360,6 +385,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_dd_fdm(FineGeom g, const FdmCl
                 }
             });
             group_sync(grp);
+            HTG_CLK(3);
             // 3: R[ixu][(s,iy')] = sum_ix' Vx[ux0 + ixu][ix'] Q[(s,iy')][ix']  -> W[(s,ixu)][iy']
             Stage<LD, KS>{V1U, nux, X, nb * ny, true, q, lane}([&](int m, int n, double2 v) {
                 if (m < nux && n < nb * ny) {
@@ -372,8 +398,10 @@ __global__ void __launch_bounds__(kFThreads, 1) k_dd_fdm(FineGeom g, const FdmCl
                 meta[(par ^ 1) * 16 + 8 + gt] = nso;
             }
             group_sync(grp);
+            HTG_CLK(4);
             // the gathered tile is free: fetch the group's next batch under stage 4
             if (bi + 1 < nbatch) gather(bsize(bi + 1), par ^ 1);
+            HTG_CLK(5);
             // 4: Y[(s,ixu)][iyu] = sum_iy' R[(s,ixu)][iy'] Vy[uy0 + iyu][iy']  -> staging rows
             Stage<LD, KS>{V2U, nuy, W, nb * nux, false, q, lane}(
                 [&](int m, int n, double2 v) {
@@ -384,10 +412,16 @@ __global__ void __launch_bounds__(kFThreads, 1) k_dd_fdm(FineGeom g, const FdmCl
                 });
             // (no barrier here: the next batch's first barrier also orders this
             // stage's reads of W before that batch's stage-1 writes)
+            HTG_CLK(6);
         }
         asm volatile("cp.async.wait_all;\n" ::: "memory");
         pos = seg_end;
     }
+#ifdef HTG_FDM_CLOCKS
+    if (lane == 0 && blockIdx.x < 2)
+        printf("fdm clk cta %d grp %d role %d: top %lld s1 %lld s2 %lld s3 %lld gather %lld s4 %lld\n", blockIdx.x, grp,
+               q, clk_acc[0], clk_acc[1], clk_acc[2], clk_acc[3], clk_acc[4], clk_acc[5]);
+#endif
 }
 
 template <int P>
