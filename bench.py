@@ -334,8 +334,9 @@ def run_ours(args):
         "roofline": {"bound": "tensor",
                      "kernel": "subdomain solves of one sweep: k_dd_fdm (fast diagonalisation, DMMA) for the "
                                f"{ops.fdm_subdomains} separable subdomains, k_dd_gemm for the rest",
-                     "note": "algorithmic flops of the fast-diagonalised solves (4 small complex products per "
-                             "subdomain, 3.7x fewer than the dense product); DMMA tiles pad 25 -> 32",
+                     "note": "algorithmic flops (8 per complex multiply-add) of the fast-diagonalised solves: 4 "
+                             "small complex products per subdomain, 3.7x fewer than the dense product; executed as "
+                             "3M DMMAs on 8-row tiles (batches of 2 subdomains) plus DFMA remainder rows",
                      "achieved": dd_tf, "peak": fp64_peak, "unit": "TFLOP/s", "frac": dd_tf / fp64_peak,
                      "traffic": traffic,
                      "peak_source": "measured in this run: DMMA m8n8k4 f64 microbenchmark (no FP64 entry in "
