@@ -74,6 +74,10 @@ __device__ __forceinline__ int fdiv(int n, float inv) { return __float2int_rz((f
 #define HTG_FDM_KSPLIT 1
 #endif
 constexpr int kKP = HTG_FDM_KSPLIT;  // independent accumulator chains per product (k steps interleaved)
+#ifndef HTG_FDM_TG
+#define HTG_FDM_TG 4
+#endif
+constexpr int kTG = HTG_FDM_TG;  // moving tiles in flight per warp (one stationary fragment set)
 
 template <int LD, int KS>
 struct Stage {
@@ -84,7 +88,7 @@ struct Stage {
     bool sa;             // the factor is the A operand (C[factor][data]); else B (C[data][factor])
     int q, lane;
 
-    using Acc = double[kKP][4][2];
+    using Acc = double[kKP][kTG][2];
     template <int NTL, class Epi>
     __device__ __forceinline__ void finish(Acc& t1, Acc& t2, Acc& t3, const int* tm, const int* tn, Epi& epi) const {
         const int r = lane >> 2, kq = lane & 3;
@@ -120,8 +124,8 @@ struct Stage {
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
             const int h = ks % kKP;
-            double2 v[4];
-            double vs[4];
+            double2 v[kTG];
+            double vs[kTG];
 #pragma unroll
             for (int j = 0; j < NTL; ++j) {
                 v[j] = mv[mrow[j] + ks * 4];
@@ -144,6 +148,20 @@ struct Stage {
             }
         }
         finish<NTL>(t1, t2, t3, tm, tn, epi);
+    }
+
+    // run_stat for the tile count nt <= N (compile-time tile counts)
+    template <int N, class Epi>
+    __device__ __forceinline__ void dispatch(int nt, const double2 (&sf)[KS], const double (&ss)[KS], const int* mrow,
+                                             const int* tm, const int* tn, Epi& epi) const {
+        if constexpr (N >= 1) {
+            if (nt == N) {
+                if (sa) run_stat<N, true>(sf, ss, dat, mrow, tm, tn, epi);
+                else run_stat<N, false>(sf, ss, dat, mrow, tm, tn, epi);
+            } else {
+                dispatch<N - 1>(nt, sf, ss, mrow, tm, tn, epi);
+            }
+        }
     }
 
     // full 8-row tiles ST of the factor on DMMA, the last FR <= 2 factor rows
@@ -184,30 +202,16 @@ struct Stage {
                 sf[ks] = srow[ks * 4];
                 ss[ks] = sf[ks].x + sf[ks].y;
             }
-            for (int o0 = o_lo; o0 < o_hi; o0 += 4) {
-                const int nt = min(4, o_hi - o0);
-                int mrow[4], tm[4], tn[4];
+            for (int o0 = o_lo; o0 < o_hi; o0 += kTG) {
+                const int nt = min(kTG, o_hi - o0);
+                int mrow[kTG], tm[kTG], tn[kTG];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
+                for (int j = 0; j < kTG; ++j) {
                     mrow[j] = min((o0 + j) * 8 + r, dlim) * LD + kq;
                     tm[j] = sa ? st : o0 + j;
                     tn[j] = sa ? o0 + j : st;
                 }
-                if (sa) {
-                    switch (nt) {
-                        case 4: run_stat<4, true>(sf, ss, dat, mrow, tm, tn, epi); break;
-                        case 3: run_stat<3, true>(sf, ss, dat, mrow, tm, tn, epi); break;
-                        case 2: run_stat<2, true>(sf, ss, dat, mrow, tm, tn, epi); break;
-                        default: run_stat<1, true>(sf, ss, dat, mrow, tm, tn, epi); break;
-                    }
-                } else {
-                    switch (nt) {
-                        case 4: run_stat<4, false>(sf, ss, dat, mrow, tm, tn, epi); break;
-                        case 3: run_stat<3, false>(sf, ss, dat, mrow, tm, tn, epi); break;
-                        case 2: run_stat<2, false>(sf, ss, dat, mrow, tm, tn, epi); break;
-                        default: run_stat<1, false>(sf, ss, dat, mrow, tm, tn, epi); break;
-                    }
-                }
+                dispatch<kTG>(nt, sf, ss, mrow, tm, tn, epi);
             }
         }
         // remainder: one complex dot product of a factor row and a data row per
