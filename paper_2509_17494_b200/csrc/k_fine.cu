@@ -525,13 +525,20 @@ __global__ void __launch_bounds__(kK1Threads) k1_residual(K1Args a) {
 // lattice row (p dofs per unit) are 1-D bulk copies; r is written back from
 // shared memory with coalesced stores.
 #ifndef HTG_KC_CELLS
-#define HTG_KC_CELLS 120
+#define HTG_KC_CELLS 60
 #endif
 #ifndef HTG_KC_CPS
 #define HTG_KC_CPS 1
 #endif
 constexpr int kKCCells = HTG_KC_CELLS;               // cell slots per CTA (lanes per warp group)
 constexpr int kKCCtasPerSM = HTG_KC_CPS;             // resident CTAs per SM the launch is sized for
+#ifndef HTG_KC_STREAMS
+#define HTG_KC_STREAMS 2
+#endif
+// independent row pipelines per CTA, each a strip with its own slots and named
+// barrier: one pipeline's barrier / TMA waits overlap the other's arithmetic
+// (2 x 60-cell strips: 33.8 us at cfg4 vs 35.2 us for one 120-cell strip)
+constexpr int kKCStreams = HTG_KC_STREAMS;
 // row slots: u prefetched kKCU - 2 rows ahead, f one row ahead. With two f slots
 // (measured: 4 u + 2 f was slower for r = f - A u, 36.5 vs 34.8 us at cfg4) f(y+1) is issued
 // after row y's exchange barrier, when every read of f(y-1) -- residual and
@@ -603,18 +610,23 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
 
 template <int P, int MODE, int GRP, bool DIR>
 __device__ __forceinline__ void k1c_body(const K1Args& a, const CUtensorMap* tmu, const CUtensorMap* tmf,
-                                         KCSmem<P>& sm, int ct) {
+                                         KCSmem<P>& sm, int ct, int str) {
     using Cf = KCCfg<P>;
     constexpr int B = Cf::B, MM = Cf::MM, NT = Cf::NT;
     constexpr int R0 = GRP * 2, R1 = (GRP == Cf::NG - 1) ? B : R0 + 2, NRG = R1 - R0;  // node rows of this group
     constexpr int SL = P / 2 - 1;  // basis table slot
     constexpr int EDGE = Cf::BOX / 16;  // double2 offset of the x = nx unit inside a slot
     const FineGeom& g = a.g;
-    const int tid = threadIdx.x, nx = g.nx, ny = g.ny;
+    const int tid = threadIdx.x % NT, nx = g.nx, ny = g.ny;  // thread index inside this stream
     const double2 zero = make_double2(0.0, 0.0);
-
-    const int x0 = int((long long)blockIdx.x * nx / gridDim.x);
-    const int xe = int((long long)(blockIdx.x + 1) * nx / gridDim.x);
+    // one barrier per stream (the CTA-wide barrier when the CTA runs one stream)
+    auto sync = [&]() {
+        if (kKCStreams == 1) __syncthreads();
+        else asm volatile("bar.sync %0, %1;\n" ::"r"(1 + str), "r"(NT) : "memory");
+    };
+    const int vx = blockIdx.x * kKCStreams + str, gxv = gridDim.x * kKCStreams;  // this stream's strip
+    const int x0 = int((long long)vx * nx / gxv);
+    const int xe = int((long long)(vx + 1) * nx / gxv);
     const int H = MODE == kK1Restrict ? 2 : 1;
     const int xa = max(x0 - H, 0);
     const int xlast = xe == nx ? nx : xe - 1;  // last unit with outputs (x = nx: right boundary column)
@@ -660,7 +672,7 @@ __device__ __forceinline__ void k1c_body(const K1Args& a, const CUtensorMap* tmu
         for (int i = 0; i < kKCF; ++i) mbar_init(&sm.barF[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    __syncthreads();
+    sync();
     if (tid == 0) {
         for (int i = 0; i + 1 < kKCU && ystart + i <= ye; ++i) stage(uslot(ystart + i), a.u, tmu, ystart + i, ubar(ystart + i));
         if (ystart >= yres0) stage(fslot(ystart), a.f, tmf, ystart, fbar(ystart));
@@ -817,7 +829,7 @@ __device__ __forceinline__ void k1c_body(const K1Args& a, const CUtensorMap* tmu
         if (active)
 #pragma unroll
             for (int j = 0; j < NRG; ++j) Xb[ct][j] = O[1][j];
-        __syncthreads();
+        sync();
         if (kKCF < 3 && tid == 0 && stage_f) stage(fslot(y + 1), a.f, tmf, y + 1, fbar(y + 1));
         if (active && ct > 0)
 #pragma unroll
@@ -850,10 +862,10 @@ __device__ __forceinline__ void k1c_body(const K1Args& a, const CUtensorMap* tmu
                 }
             }
             if (MODE == kK1Write) {
-                __syncthreads();
+                sync();
                 if (y >= ys) store_row(y);
             }
-            if (MODE == kK1Norm && DIR) __syncthreads();  // Dirichlet reads of u(y) vs its re-fill
+            if (MODE == kK1Norm && DIR) sync();  // Dirichlet reads of u(y) vs its re-fill
             if (MODE == kK1Restrict) {
                 // node rows 2..m of group 1 -> group 0 through the idle exchange buffer
                 constexpr int NH = MM >= 2 ? MM - 1 : 1;
@@ -866,7 +878,7 @@ __device__ __forceinline__ void k1c_body(const K1Args& a, const CUtensorMap* tmu
                         for (int h = 0; h < NH; ++h) XR[(ct * B + al) * NH + h] = O[al][h];
                     }
                 }
-                __syncthreads();
+                sync();
                 double2 pt[MM + 1][MM + 1];  // partials at coarse nodes (jx, jy) of this cell
 #pragma unroll
                 for (int jx = 0; jx <= MM; ++jx)
@@ -901,7 +913,7 @@ __device__ __forceinline__ void k1c_body(const K1Args& a, const CUtensorMap* tmu
 #pragma unroll
                         for (int jy = 0; jy <= MM; ++jy) sm.XP[ct][jy] = pt[MM][jy];
                 }
-                __syncthreads();
+                sync();
                 if (GRP == 0) {
                     if (active && ct > 0)
 #pragma unroll
@@ -945,7 +957,7 @@ __device__ __forceinline__ void k1c_body(const K1Args& a, const CUtensorMap* tmu
             }
         }
         if (MODE == kK1Write) {
-            __syncthreads();
+            sync();
             store_top();
         }
         if (MODE == kK1Restrict) {
@@ -959,9 +971,9 @@ __device__ __forceinline__ void k1c_body(const K1Args& a, const CUtensorMap* tmu
                     pt[jx] = rfma(wgt(al, jx), Rt[al], pt[jx]);
                 }
             }
-            __syncthreads();  // exchange buffers may still be read by a neighbour
+            sync();  // exchange buffers may still be read by a neighbour
             if (GRP == 0 && active) sm.XP[ct][0] = pt[MM];
-            __syncthreads();
+            sync();
             if (GRP == 0) {
                 if (active && ct > 0) pt[0] = cadd(pt[0], sm.XP[ct - 1][0]);
                 if (owned)
@@ -973,37 +985,39 @@ __device__ __forceinline__ void k1c_body(const K1Args& a, const CUtensorMap* tmu
     }
     if (MODE == kK1Norm) {  // fixed-order block sum
         sm.red[tid] = acc;
-        __syncthreads();
+        sync();
         if (tid == 0) {
             double sacc = 0.0;
             for (int w = 0; w < NT; ++w) sacc += sm.red[w];
-            a.partial[blockIdx.y * gridDim.x + blockIdx.x] = sacc;
+            a.partial[blockIdx.y * gxv + vx] = sacc;
         }
     }
 }
 
 template <int P, int MODE, bool DIR>
-__global__ void __launch_bounds__(KCCfg<P>::NT, kKCCtasPerSM)
+__global__ void __launch_bounds__(KCCfg<P>::NT * kKCStreams, kKCCtasPerSM)
     k1_cells(const __grid_constant__ K1Args a, const __grid_constant__ CUtensorMap tmu,
              const __grid_constant__ CUtensorMap tmf) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // the swizzled TMA boxes need 1 KB aligned slots: align inside the allocation
     // (offset arithmetic on the shared pointer keeps the accesses LDS/STS)
     const unsigned pad = (1024u - (static_cast<unsigned>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u;
-    KCSmem<P>& sm = *reinterpret_cast<KCSmem<P>*>(smem_raw + pad);
+    // stream str of the CTA: its own slots, barriers and strip
+    const int str = int(threadIdx.x) / KCCfg<P>::NT;
+    KCSmem<P>& sm = reinterpret_cast<KCSmem<P>*>(smem_raw + pad)[str];
     // even warps: group 0, odd warps: group 1. Warps are assigned to the SM's
     // four schedulers by warp index mod 4, so each scheduler runs one group's
     // code only (the two unrolled bodies would otherwise thrash its icache).
-    const int w = threadIdx.x >> 5;
+    const int w = (threadIdx.x % KCCfg<P>::NT) >> 5;
     if constexpr (KCCfg<P>::NG == 3) {  // group = w / 4: every scheduler runs one warp of each group
         const int ct = (w % kKCGroupWarps) * 32 + (threadIdx.x & 31), gsel = w / kKCGroupWarps;
-        if (gsel == 0) k1c_body<P, MODE, 0, DIR>(a, &tmu, &tmf, sm, ct);
-        else if (gsel == 1) k1c_body<P, MODE, 1, DIR>(a, &tmu, &tmf, sm, ct);
-        else k1c_body<P, MODE, 2, DIR>(a, &tmu, &tmf, sm, ct);
+        if (gsel == 0) k1c_body<P, MODE, 0, DIR>(a, &tmu, &tmf, sm, ct, str);
+        else if (gsel == 1) k1c_body<P, MODE, 1, DIR>(a, &tmu, &tmf, sm, ct, str);
+        else k1c_body<P, MODE, 2, DIR>(a, &tmu, &tmf, sm, ct, str);
     } else {
         const int ct = (w >> 1) * 32 + (threadIdx.x & 31);
-        if ((w & 1) == 0) k1c_body<P, MODE, 0, DIR>(a, &tmu, &tmf, sm, ct);
-        else k1c_body<P, MODE, 1, DIR>(a, &tmu, &tmf, sm, ct);
+        if ((w & 1) == 0) k1c_body<P, MODE, 0, DIR>(a, &tmu, &tmf, sm, ct, str);
+        else k1c_body<P, MODE, 1, DIR>(a, &tmu, &tmf, sm, ct, str);
     }
 }
 
@@ -1045,13 +1059,16 @@ static int k1_row_blocks(const FineGeom& g, int rows) {
 
 // cell-per-thread kernel (p <= 4): one CTA per SM, strips of at most KCCfg::C cells
 template <int P>
-static int kc_strips(int nx) { return (nx + KCCfg<P>::C - 1) / KCCfg<P>::C; }
+static int kc_strips(int nx) {  // a multiple of the streams per CTA
+    const int st = (nx + KCCfg<P>::C - 1) / KCCfg<P>::C;
+    return (st + kKCStreams - 1) / kKCStreams * kKCStreams;
+}
 static int kc_gx(const FineGeom& g) { return g.p == 2 ? kc_strips<2>(g.nx) : kc_strips<4>(g.nx); }
 static int kc_row_blocks(const FineGeom& g, int rows) {
     if (rows > 0) return (g.ny + rows - 1) / rows;
     static int nsm = 0;
     if (!nsm) HTG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
-    return std::max(1, std::min(nsm * kKCCtasPerSM / kc_gx(g), g.ny / 2));
+    return std::max(1, std::min(nsm * kKCCtasPerSM * kKCStreams / kc_gx(g), g.ny / 2));
 }
 
 int k1_partials(const FineGeom& g, int rows) {
@@ -1085,15 +1102,15 @@ static CUtensorMap kc_tensor_map(const FineGeom& g, const double2* base) {
 
 template <int P, int MODE, bool DIR>
 static void kc_launch_dir(const K1Args& a, cudaStream_t st) {
-    dim3 grid(kc_strips<P>(a.g.nx), kc_row_blocks(a.g, a.rows));
-    const size_t smem = sizeof(KCSmem<P>) + 1024;
+    dim3 grid(kc_strips<P>(a.g.nx) / kKCStreams, kc_row_blocks(a.g, a.rows));
+    const size_t smem = kKCStreams * sizeof(KCSmem<P>) + 1024;
     static bool attr = false;
     if (!attr) {
         HTG_CUDA(cudaFuncSetAttribute(k1_cells<P, MODE, DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         attr = true;
     }
     const CUtensorMap tmu = kc_tensor_map<P>(a.g, a.u), tmf = kc_tensor_map<P>(a.g, a.f);
-    k1_cells<P, MODE, DIR><<<grid, KCCfg<P>::NT, smem, st>>>(a, tmu, tmf);
+    k1_cells<P, MODE, DIR><<<grid, KCCfg<P>::NT * kKCStreams, smem, st>>>(a, tmu, tmf);
 }
 
 template <int P, int MODE>
