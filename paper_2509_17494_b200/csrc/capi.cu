@@ -127,14 +127,13 @@ struct htg_handle {
     // pinned host scalars
     double* hscal = nullptr;
     // CUDA graphs of the launch sequences, keyed by (kind, u, f); replayed on
-    // an internal capture stream that is event-ordered with the user stream
+    // an internal capture stream and replayed on the handle's stream
     struct GraphEntry {
         cudaGraphExec_t exec;
         long long launches;
     };
     std::map<std::tuple<int, const void*, const void*>, GraphEntry> graphs;
     cudaStream_t cap = nullptr;
-    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
     bool use_graphs = true;
     // GMRES workspace (allocated on first Krylov solve)
     std::vector<double2*> krylov;
@@ -142,8 +141,6 @@ struct htg_handle {
     ~htg_handle() {
         for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
         if (cap) cudaStreamDestroy(cap);
-        if (ev_in) cudaEventDestroy(ev_in);
-        if (ev_out) cudaEventDestroy(ev_out);
         coarse.reset();
         fine.reset();
         if (hscal) cudaFreeHost(hscal);
@@ -282,8 +279,6 @@ void build_handle(htg_handle* H, const htg_problem& prob, const htg_config& cfg)
     if (cfg.smoother == HTG_SMOOTHER_EXACT_SHIFTED)  // u += A_s^-1 (f - A u), twogrid.cpp:261-262
         H->fine = make_nd_solver(fe_lattice(hp, H->basis, hp.p, cfg.alpha_s), st);
     HTG_CUDA(cudaStreamCreateWithFlags(&H->cap, cudaStreamNonBlocking));
-    HTG_CUDA(cudaEventCreateWithFlags(&H->ev_in, cudaEventDisableTiming));
-    HTG_CUDA(cudaEventCreateWithFlags(&H->ev_out, cudaEventDisableTiming));
     if (const char* e = std::getenv("HTG_NO_GRAPHS")) H->use_graphs = e[0] == '0';
     HTG_CUDA(cudaStreamSynchronize(st));
 }
@@ -321,11 +316,9 @@ void run_graph(htg_handle* H, int kind, const void* u, const void* f, F&& body) 
         count_launch(int(-n));  // captured, not launched
         it = H->graphs.emplace(key, htg_handle::GraphEntry{exec, n}).first;
     }
-    HTG_CUDA(cudaEventRecord(H->ev_in, H->st));
-    HTG_CUDA(cudaStreamWaitEvent(H->cap, H->ev_in, 0));
-    HTG_CUDA(cudaGraphLaunch(it->second.exec, H->cap));
-    HTG_CUDA(cudaEventRecord(H->ev_out, H->cap));
-    HTG_CUDA(cudaStreamWaitEvent(H->st, H->ev_out, 0));
+    // captured on the internal stream (a legacy default stream cannot capture),
+    // replayed directly on the caller's stream: stream order, no event hop
+    HTG_CUDA(cudaGraphLaunch(it->second.exec, H->st));
     count_launch(int(it->second.launches));
 }
 
