@@ -9,6 +9,9 @@ M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
 python tools/run_once.py --what step --reps 2 > gpurun_out/plain_step.log 2>&1
 ncu --metrics $M --clock-control none --csv --log-file gpurun_out/launches_step.csv \
     python tools/run_once.py --what step --reps 2 > gpurun_out/ncu_step.log 2>&1
+python tools/run_once.py --what sweep --reps 2 > gpurun_out/plain_sweep2.log 2>&1
+ncu --metrics $M --clock-control none --csv --log-file gpurun_out/launches_sweep.csv \
+    python tools/run_once.py --what sweep --reps 2 > gpurun_out/ncu_sweep.log 2>&1
 python tools/run_once.py --what coarse --reps 1 > gpurun_out/plain_coarse.log 2>&1
 ncu --metrics $M --clock-control none --csv --log-file gpurun_out/launches_coarse.csv \
     python tools/run_once.py --what coarse --reps 1 > gpurun_out/ncu_coarse.log 2>&1
