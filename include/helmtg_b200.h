@@ -89,7 +89,8 @@ int htg_destroy(htg_handle* h);
  * (fast diagonalisation for separable classes, 8 |U_i| |Omega_i| otherwise),
  * [10] nested-dissection levels of the coarse solver, [11] the dense-path
  * flops 8 |U_i| |Omega_i| summed, [12] subdomains solved by fast
- * diagonalisation. out must hold 13 entries. */
+ * diagonalisation, [13] CUDA graphs cached by the handle (bounded LRU).
+ * out must hold 14 entries. */
 int htg_info(const htg_handle* h, long long* out);
 int htg_set_stream(htg_handle* h, void* stream);
 

@@ -131,7 +131,11 @@ struct htg_handle {
     struct GraphEntry {
         cudaGraphExec_t exec;
         long long launches;
+        unsigned long long last_use;
     };
+    // bounded: callers that pass fresh buffers every call must not grow the cache
+    static constexpr size_t kMaxGraphs = 16;
+    unsigned long long graph_clock = 0;
     std::map<std::tuple<int, const void*, const void*>, GraphEntry> graphs;
     cudaStream_t cap = nullptr;
     bool use_graphs = true;
@@ -243,7 +247,7 @@ void build_handle(htg_handle* H, const htg_problem& prob, const htg_config& cfg)
             if (c.fdm) H->fdm_err = std::max(H->fdm_err, c.fdm_err);
         if (!H->fdm.empty()) {
             int nsm = 0;
-            HTG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
+            nsm = current_sm_count();
             const std::vector<int4> work = fdm_plan(H->fdm, hp.p, nsm, H->fdm_launch);  // sets FdmClassDev::first
             H->fdm_launch.classes = M.upload(H->fdm, st);
             H->fdm_launch.work = M.upload(work, st);
@@ -314,8 +318,17 @@ void run_graph(htg_handle* H, int kind, const void* u, const void* f, F&& body) 
         HTG_CUDA(e);
         const long long n = launch_count() - c0;
         count_launch(int(-n));  // captured, not launched
-        it = H->graphs.emplace(key, htg_handle::GraphEntry{exec, n}).first;
+        if (H->graphs.size() >= htg_handle::kMaxGraphs) {  // evict the least recently replayed
+            auto lru = H->graphs.begin();
+            for (auto jt = H->graphs.begin(); jt != H->graphs.end(); ++jt)
+                if (jt->second.last_use < lru->second.last_use) lru = jt;
+            HTG_CUDA(cudaStreamSynchronize(H->st));  // it may still be in flight on the caller's stream
+            cudaGraphExecDestroy(lru->second.exec);
+            H->graphs.erase(lru);
+        }
+        it = H->graphs.emplace(key, htg_handle::GraphEntry{exec, n, 0}).first;
     }
+    it->second.last_use = ++H->graph_clock;
     // captured on the internal stream (a legacy default stream cannot capture),
     // replayed directly on the caller's stream: stream order, no event hop
     HTG_CUDA(cudaGraphLaunch(it->second.exec, H->st));
@@ -636,6 +649,7 @@ int htg_info(const htg_handle* h, long long* out) {
         out[10] = h->coarse ? h->coarse->levels() : 0;
         out[11] = (long long)h->dd_flops_dense;
         out[12] = h->fdm_subs;
+        out[13] = (long long)h->graphs.size();
     });
 }
 

@@ -1,5 +1,6 @@
 // coarse.cu -- level-batched GPU solves with the nested-dissection multifrontal
 // factors of the QSFEM coarse matrix (factored on the host in coarse_nd.cpp).
+#include <mutex>
 #include <cuda_runtime.h>
 
 #include <chrono>
@@ -636,12 +637,17 @@ class NDSolver : public CoarseSolver {
         }
         HTG_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
         if (max_smem > 227 * 1024) throw InvalidArgument("coarse front too large for shared memory");
-        if (max_smem > 48 * 1024) {
-            HTG_CUDA(cudaFuncSetAttribute(k_nd_fwd_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, int(max_smem)));
-            HTG_CUDA(cudaFuncSetAttribute(k_nd_fwd1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(max_smem)));
-            HTG_CUDA(cudaFuncSetAttribute(k_nd_fwd2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(max_smem)));
-            HTG_CUDA(cudaFuncSetAttribute(k_nd_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, int(max_smem)));
-        }
+        // The attribute is process-global: always grant the opt-in maximum (it is a
+        // permission, not a reservation), so handles of different sizes never lower
+        // each other's limit.
+        static std::once_flag smem_once;
+        std::call_once(smem_once, [] {
+            const int kOptIn = 227 * 1024;
+            HTG_CUDA(cudaFuncSetAttribute(k_nd_fwd_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, kOptIn));
+            HTG_CUDA(cudaFuncSetAttribute(k_nd_fwd1, cudaFuncAttributeMaxDynamicSharedMemorySize, kOptIn));
+            HTG_CUDA(cudaFuncSetAttribute(k_nd_fwd2, cudaFuncAttributeMaxDynamicSharedMemorySize, kOptIn));
+            HTG_CUDA(cudaFuncSetAttribute(k_nd_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kOptIn));
+        });
     }
 };
 

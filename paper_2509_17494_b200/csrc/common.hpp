@@ -26,6 +26,14 @@ struct RuntimeError : std::runtime_error {
                                       " at " __FILE__ ":" + std::to_string(__LINE__));          \
     } while (0)
 
+// SM count of the calling thread's current device (handles may live on any device)
+inline int current_sm_count() {
+    int dev = 0, n = 0;
+    HTG_CUDA(cudaGetDevice(&dev));
+    HTG_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    return n;
+}
+
 constexpr int kMaxP = 8;
 constexpr int8_t kDirichlet = 0, kNeumann = 1, kAbsorbing = 2;
 

@@ -55,9 +55,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_dd_gemm(FineGeom g, DDDevice d,
     const int4 tile = d.tiles[blockIdx.x];
     const int c = tile.x, m0 = tile.y, n0 = tile.z;
     const int* ci = d.cls_info + 8 * c;
-    const int nu = ci[3], kpad = ci[4], boff = ci[5], loff = ci[6], ncol = ci[7];
+    const int nu = ci[3], kpad = ci[4], loff = ci[6], ncol = ci[7];
     const int sub0 = tile.w;  // offset of this class's subdomain list
-    const double2* Bc = d.Bmat + (size_t)boff;
+    const double2* Bc = d.Bmat + d.cls_boff[c];
     const int* locg = d.loc_g + loff;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp >> 2, wn = warp & 3;
@@ -231,6 +231,7 @@ DDDevice upload_dd_impl(const DDSetup& dd, const HostProblem& hp, std::vector<vo
     d.l_dd = dd.l_dd;
     const int p = hp.p;
     std::vector<int> info(8 * nc), locg, rowmap, class_subs;
+    std::vector<long long> boff(nc);
     std::vector<double2> Bm;
     std::vector<int4> tiles;
     std::vector<std::vector<int>> subs(nc);
@@ -247,7 +248,8 @@ DDDevice upload_dd_impl(const DDSetup& dd, const HostProblem& hp, std::vector<vo
         in[2] = c.nloc;
         in[3] = c.nu;
         in[4] = kpad;
-        in[5] = int(Bm.size());
+        in[5] = 0;
+        boff[ci] = (long long)Bm.size();
         in[6] = int(locg.size());
         in[7] = int(subs[ci].size());
         const size_t b0 = Bm.size();
@@ -367,6 +369,7 @@ DDDevice upload_dd_impl(const DDSetup& dd, const HostProblem& hp, std::vector<vo
         return static_cast<const T*>(ptr);
     };
     d.cls_info = up(info);
+    d.cls_boff = up(boff);
     d.Bmat = up(Bm);
     d.loc_g = up(locg);
     d.rowmap = up(rowmap);
@@ -418,7 +421,7 @@ extern "C" int htg_measure_fp64_tensor_peak(double* tflops) {
     using namespace htg;
     try {
         int sms = 0;
-        HTG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+        sms = current_sm_count();
         const int blocks = sms * 2, threads = 512, iters = 4096;
         double* out = nullptr;
         HTG_CUDA(cudaMalloc(&out, sizeof(double) * blocks * threads));

@@ -1051,7 +1051,7 @@ constexpr int kK1CtasPerSM = 3;
 static int k1_row_blocks(const FineGeom& g, int rows) {
     if (rows > 0) return (g.ny + rows - 1) / rows;
     static int nsm = 0;
-    if (!nsm) HTG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
+    if (!nsm) nsm = current_sm_count();
     const int strips = k1_gx(g);
     const int nb = std::max(1, nsm * kK1CtasPerSM / strips);
     return std::max(1, std::min(nb, g.ny / 4));
@@ -1067,7 +1067,7 @@ static int kc_gx(const FineGeom& g) { return g.p == 2 ? kc_strips<2>(g.nx) : kc_
 static int kc_row_blocks(const FineGeom& g, int rows) {
     if (rows > 0) return (g.ny + rows - 1) / rows;
     static int nsm = 0;
-    if (!nsm) HTG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
+    if (!nsm) nsm = current_sm_count();
     return std::max(1, std::min(nsm * kKCCtasPerSM * kKCStreams / kc_gx(g), g.ny / 2));
 }
 

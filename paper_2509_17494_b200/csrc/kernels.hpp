@@ -62,7 +62,8 @@ struct DDDevice {
     int nu_max = 0;           // staging stride per subdomain
     int ntiles = 0;
     // per class
-    const int* cls_info;      // [nclass][8]: onx, ony, nloc, nu, kpad, b_off(lo), b_off(hi), loc_off
+    const int* cls_info;      // [nclass][8]: onx, ony, nloc, nu, kpad, (unused), loc_off, n_subdomains
+    const long long* cls_boff;  // [nclass]: offset of the class's B block in Bmat (64-bit: B can exceed 2^31 entries)
     const double2* Bmat;      // all classes, [rows_pad][kpad] each
     const int* loc_g;         // per class per local dof: lgx | lgy << 16
     const int* rowmap;        // per class per local dof: U row or -1

@@ -156,16 +156,24 @@ def dirichlet_mask(nx: int, ny: int, p: int, side_tags) -> np.ndarray:
     return out
 
 
-def _dptr(t) -> C.c_void_p:
+def _dptr(t, n: int | None = None, device: int | None = None) -> C.c_void_p:
+    """Device pointer of a contiguous complex128 CUDA tensor of exactly n entries on the
+    handle's device (the C-ABI reads/writes n entries: a short tensor would be overrun)."""
     import torch
     if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.complex128 and t.is_contiguous()):
         raise HtgError(_lib.HTG_ERR_INVALID, "device vectors must be contiguous complex128 CUDA tensors")
+    if n is not None and t.numel() != n:
+        raise HtgError(_lib.HTG_ERR_INVALID, f"device vector has {t.numel()} entries, expected {n}")
+    if device is not None and t.device.index != device:
+        raise HtgError(_lib.HTG_ERR_INVALID, f"device vector on cuda:{t.device.index}, handle on cuda:{device}")
     return C.c_void_p(t.data_ptr())
 
 
-def _hptr(a: np.ndarray) -> C.c_void_p:
-    if not (a.dtype == np.complex128 and a.flags.c_contiguous):
+def _hptr(a: np.ndarray, n: int | None = None) -> C.c_void_p:
+    if not (isinstance(a, np.ndarray) and a.dtype == np.complex128 and a.flags.c_contiguous):
         raise HtgError(_lib.HTG_ERR_INVALID, "host vectors must be contiguous complex128 arrays")
+    if n is not None and a.size != n:
+        raise HtgError(_lib.HTG_ERR_INVALID, f"host vector has {a.size} entries, expected {n}")
     return a.ctypes.data_as(C.c_void_p)
 
 
@@ -193,13 +201,14 @@ class TwoGridOperators:
                           (C.c_int * 4)(*problem.side_tags), None, None, None, None)
         cfg = config._c()
         h = C.c_void_p()
+        import torch
+        self.device = torch.cuda.current_device()
         if stream is None:
-            import torch
             stream = torch.cuda.current_stream()  # order the handle with torch's work
         st = C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
         check(L.htg_create(C.byref(cp), C.byref(cfg), st, C.byref(h)))
         self._h = h
-        info = (C.c_longlong * 13)()
+        info = (C.c_longlong * 14)()
         check(L.htg_info(h, info))
         (self.ndof, self.coarse_ndof, self.n_subdomains, self.n_classes, self.device_bytes,
          self.coarse_factor_bytes) = (int(v) for v in info[:6])
@@ -207,6 +216,18 @@ class TwoGridOperators:
         self.coarse_levels = int(info[10])
         self.dd_flops_dense = int(info[11])
         self.fdm_subdomains = int(info[12])
+
+    def _f(self, t):  # fine-space device vector
+        return _dptr(t, self.ndof, self.device)
+
+    def _c(self, t):  # coarse-space device vector
+        return _dptr(t, self.coarse_ndof, self.device)
+
+    @property
+    def cached_graphs(self) -> int:
+        info = (C.c_longlong * 14)()
+        check(lib().htg_info(self._h, info))
+        return int(info[13])
 
     def close(self):
         if getattr(self, "_h", None):
@@ -224,44 +245,44 @@ class TwoGridOperators:
 
     # ---------------------------------------------------------------- device API
     def residual(self, f, u, r, shifted: bool = False):
-        check(lib().htg_residual(self._h, _dptr(f), _dptr(u), _dptr(r), int(shifted)))
+        check(lib().htg_residual(self._h, self._f(f), self._f(u), self._f(r), int(shifted)))
         return r
 
     def residual_norm(self, f, u) -> float:
         out = C.c_double()
-        check(lib().htg_residual_norm(self._h, _dptr(f), _dptr(u), C.byref(out)))
+        check(lib().htg_residual_norm(self._h, self._f(f), self._f(u), C.byref(out)))
         return out.value
 
     def dd_step(self, u, f, out):
-        check(lib().htg_dd_step(self._h, _dptr(u), _dptr(f), _dptr(out)))
+        check(lib().htg_dd_step(self._h, self._f(u), self._f(f), self._f(out)))
         return out
 
     def csdd_smoother(self, u, f):
-        check(lib().htg_csdd_smoother(self._h, _dptr(u), _dptr(f)))
+        check(lib().htg_csdd_smoother(self._h, self._f(u), self._f(f)))
         return u
 
     def restrict(self, r, rc):
-        check(lib().htg_restrict(self._h, _dptr(r), _dptr(rc)))
+        check(lib().htg_restrict(self._h, self._f(r), self._c(rc)))
         return rc
 
     def residual_restrict(self, f, u, rc):
-        check(lib().htg_residual_restrict(self._h, _dptr(f), _dptr(u), _dptr(rc)))
+        check(lib().htg_residual_restrict(self._h, self._f(f), self._f(u), self._c(rc)))
         return rc
 
     def prolong_add(self, u, uc, omega: float):
-        check(lib().htg_prolong_add(self._h, _dptr(u), _dptr(uc), float(omega)))
+        check(lib().htg_prolong_add(self._h, self._f(u), self._c(uc), float(omega)))
         return u
 
     def coarse_apply(self, x, y):
-        check(lib().htg_coarse_apply(self._h, _dptr(x), _dptr(y)))
+        check(lib().htg_coarse_apply(self._h, self._c(x), self._c(y)))
         return y
 
     def coarse_solve(self, rc, uc):
-        check(lib().htg_coarse_solve(self._h, _dptr(rc), _dptr(uc)))
+        check(lib().htg_coarse_solve(self._h, self._c(rc), self._c(uc)))
         return uc
 
     def two_grid_step(self, u, f):
-        check(lib().htg_two_grid_step(self._h, _dptr(u), _dptr(f)))
+        check(lib().htg_two_grid_step(self._h, self._f(u), self._f(f)))
         return u
 
     def solve(self, f, u=None) -> SolveResult:
@@ -271,14 +292,14 @@ class TwoGridOperators:
         cap = self.config.max_iters + 1
         hist = np.zeros(cap)
         it, conv = C.c_int(), C.c_int()
-        check(lib().htg_solve(self._h, _dptr(f), _dptr(u), hist.ctypes.data_as(C.c_void_p), cap, C.byref(it),
+        check(lib().htg_solve(self._h, self._f(f), self._f(u), hist.ctypes.data_as(C.c_void_p), cap, C.byref(it),
                               C.byref(conv)), allow_not_converged=True)
         return SolveResult(u, it.value, list(hist[: it.value]), bool(conv.value))
 
     def profile(self, u, f, reps: int = 10) -> dict:
         """Mean device time (ms) of each hot-path phase (CUDA events, handle stream)."""
         ms = (C.c_double * 13)()
-        check(lib().htg_profile(self._h, _dptr(u), _dptr(f), int(reps), ms))
+        check(lib().htg_profile(self._h, self._f(u), self._f(f), int(reps), ms))
         keys = ("residual", "dd_gemm", "dd_combine", "residual_restrict", "coarse_solve", "prolong",
                 "residual_norm", "smoother_sweep", "two_grid_step", "coarse_apply", "smoother_sweep_graph",
                 "two_grid_step_graph", "coarse_solve_graph")
@@ -291,16 +312,16 @@ class TwoGridOperators:
         cap = self.config.max_iters + 1
         hist = np.zeros(cap)
         it, conv = C.c_int(), C.c_int()
-        check(lib().htg_solve_host(self._h, _hptr(f), _hptr(u), hist.ctypes.data_as(C.c_void_p), cap, C.byref(it),
+        check(lib().htg_solve_host(self._h, _hptr(f, self.ndof), _hptr(u, self.ndof), hist.ctypes.data_as(C.c_void_p), cap, C.byref(it),
                                    C.byref(conv)), allow_not_converged=True)
         return SolveResult(u, it.value, list(hist[: it.value]), bool(conv.value))
 
     def two_grid_step_host(self, u: np.ndarray, f: np.ndarray) -> np.ndarray:
-        check(lib().htg_two_grid_step_host(self._h, _hptr(u), _hptr(f)))
+        check(lib().htg_two_grid_step_host(self._h, _hptr(u, self.ndof), _hptr(f, self.ndof)))
         return u
 
     def csdd_smoother_host(self, u: np.ndarray, f: np.ndarray) -> np.ndarray:
-        check(lib().htg_csdd_smoother_host(self._h, _hptr(u), _hptr(f)))
+        check(lib().htg_csdd_smoother_host(self._h, _hptr(u, self.ndof), _hptr(f, self.ndof)))
         return u
 
 

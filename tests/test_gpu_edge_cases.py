@@ -119,3 +119,40 @@ def test_minimal_meshes(nx, ny, p):
     want = ses.two_grid_step(np.zeros(ses.ndof, complex), f)
     assert np.linalg.norm(u.cpu().numpy() - want) <= 1e-10 * np.linalg.norm(want)
     ops.close()
+
+
+def test_vector_lengths_and_devices_are_checked():
+    """A short vector would be overrun by the C-ABI (it reads/writes ndof entries):
+    rejected with HTG_ERR_INVALID before any launch, device and host paths alike."""
+    torch = _torch()
+    import paper_2509_17494_b200 as hb
+    prob = hb.build_problem(hb.ProblemSpec(order=4, wavelengths=3, ppw=10))
+    ops = hb.setup_two_grid(prob)
+    z = lambda n: torch.zeros(n, dtype=torch.complex128, device="cuda")  # noqa: E731
+    with pytest.raises(hb.HtgError):
+        ops.residual(z(ops.ndof), z(ops.ndof - 1), z(ops.ndof))
+    with pytest.raises(hb.HtgError):
+        ops.coarse_solve(z(ops.coarse_ndof), z(ops.ndof))
+    with pytest.raises(hb.HtgError):
+        ops.prolong_add(z(ops.ndof), z(ops.coarse_ndof + 1), 1.0)
+    with pytest.raises(hb.HtgError):
+        ops.two_grid_step_host(np.zeros(ops.ndof - 3, np.complex128), np.zeros(ops.ndof, np.complex128))
+    with pytest.raises(hb.HtgError):
+        ops.residual(z(ops.ndof).cpu(), z(ops.ndof), z(ops.ndof))
+    ops.close()
+
+
+def test_graph_cache_is_bounded():
+    """solve() with a fresh u every call must not grow the per-handle graph cache."""
+    torch = _torch()
+    import paper_2509_17494_b200 as hb
+    prob = hb.build_problem(hb.ProblemSpec(order=4, wavelengths=3, ppw=10))
+    ops = hb.setup_two_grid(prob)
+    f = torch.from_numpy(prob.rhs).cuda()
+    first = ops.solve(f)
+    for _ in range(24):
+        res = ops.solve(f)
+        assert res.iterations == first.iterations
+    assert 1 <= ops.cached_graphs <= 16
+    assert torch.equal(res.u, first.u)
+    ops.close()
