@@ -13,9 +13,10 @@ A step is one smoother sweep. L2 (126 MB) is flushed before every timed step.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
---impl reference times the reference algorithm's CPU implementation (the C++
-oracle restatement in oracle/, the reference itself needs Eigen3 and is not
-buildable here) on the host cores, on a bounded sample of the same workload.
+--impl reference times the reference's own CPU implementation on the host cores
+on the same cfg4 problem: its hot-path sources compiled unmodified against the
+Eigen-subset shim (oracle/_ref/libhelmtg_ref.so, oracle/Makefile.ref), one
+csdd_smoother sweep per step, all host threads in its parallel_for.
 N > 1 runs N independent replicas (the path is single-GPU by the north star).
 """
 from __future__ import annotations
@@ -37,12 +38,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOAD = dict(order=4, wavelengths=160.0, ppw=10.0)
+CFG3 = dict(order=4, wavelengths=80.0, ppw=10.0)
 WORKLOAD_NAME = ("BASELINE cfg4: unit square, Q4 hierarchical quads, 160 wavelengths at 10 dofs/wavelength "
                  "(400x400 cells, 2,563,201 complex-fp64 dofs), all-absorbing, seeded complex Gaussian RHS "
                  "(numpy default_rng(1004)), CSDD alpha_s=0.2 l_dd=4 n_dd=1, QSFEM coarse level")
-# CPU sample: the same element, subdomain size and k*h (identical interior subdomain
-# operators), 100x100 cells -- cfg3/cfg4 per-dof work on a bounded problem
-CPU_SAMPLE = dict(order=4, wavelengths=40.0, ppw=10.0)
 METRIC = "smoother+residual DoF/s"
 UNIT = "DoF/s"
 BYTES_PER_DOF_RESIDUAL = 48  # read u, f; write r (complex fp64)
@@ -149,30 +148,70 @@ def seeded_rhs(ndof: int, seed: int) -> np.ndarray:
     return re + 1j * im
 
 
-# ------------------------------------------------------------------ CPU (oracle) leg
-def cpu_sample(steps: int, seconds: float):
-    """Oracle smoother sweeps on CPU_SAMPLE; returns (DoF/s, cores, sample text, per-step s)."""
+# ------------------------------------------------------------------ CPU legs
+def reference_session(spec: dict):
+    """The reference's own code on the host cores: proj/core/src/*.cpp compiled
+    unmodified against oracle/eigen_shim (oracle/_ref/libhelmtg_ref.so, built here
+    and shipped with the snapshot). setup_two_grid with CoarseKind::None builds
+    exactly what csdd_smoother needs: A, A_s, the partition and one SparseLU
+    factor per subdomain (twogrid.cpp:79-89; no sharing). Falls back to the C++
+    restatement (oracle/, kind "port") only if the library is missing."""
     from oracle import pyoracle as po
-    po.build()
     cores = os.cpu_count() or 1
-    po.set_threads(cores)
-    ses = po.Session(po.ProblemSpec(**CPU_SAMPLE), po.SolverConfig(coarsening=2))
+    t0 = time.perf_counter()
+    try:
+        from oracle import pyref
+        if not os.path.exists(pyref.LIB_PATH):
+            pyref.build()
+        pyref.set_threads(cores)
+        ses = pyref.RefSession(po.ProblemSpec(**spec), po.SolverConfig(coarsening=2))
+        kind = "reference"
+    except Exception:
+        po.build()
+        po.set_threads(cores)
+        ses = po.Session(po.ProblemSpec(**spec), po.SolverConfig(coarsening=2))
+        kind = "port"
+    return ses, kind, cores, time.perf_counter() - t0
+
+
+def reference_sweeps(ses, kind: str, u: np.ndarray, f: np.ndarray, steps: int) -> float:
+    """`steps` csdd_smoother sweeps in place on u; wall seconds of the loop."""
+    if kind == "reference":
+        return ses.bench_csdd(u, f, steps)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        u[:] = ses.csdd_smoother(u, f)
+    return time.perf_counter() - t0
+
+
+def host_desc(cores: int) -> str:
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    return f"{cores} host threads ({model})" if model else f"{cores} host threads"
+
+
+def cpu_sample(steps: int, seconds: float):
+    """Reference csdd_smoother sweeps on the cfg4 problem itself, bounded to about
+    `seconds` of CPU work; returns (DoF/s, cores, kind, sample text)."""
+    ses, kind, cores, setup_s = reference_session(WORKLOAD)
     f = seeded_rhs(ses.ndof, 1004)
     u = np.zeros(ses.ndof, np.complex128)
-    u = ses.csdd_smoother(u, f)  # warm
-    times = []
-    t_end = time.perf_counter() + seconds
-    for _ in range(max(1, steps)):
-        t0 = time.perf_counter()
-        u = ses.csdd_smoother(u, f)
-        times.append(time.perf_counter() - t0)
-        if time.perf_counter() > t_end and len(times) >= 3:
-            break
-    per = statistics.median(times)
-    sample = (f"oracle (C++ restatement, reference thread model: single-thread CSR SpMV, per-subdomain LU solves "
-              f"in parallel_for over {cores} threads) csdd_smoother sweeps on a 100x100-cell Q4 problem "
-              f"({ses.ndof} dofs, same k*h and l_dd as cfg4), {len(times)} sweeps, median {per * 1e3:.1f} ms/sweep")
-    return ses.ndof / per, cores, sample, per, len(times)
+    t1 = reference_sweeps(ses, kind, u, f, 1)  # warm-up sweep, sizes the sample
+    n = max(2, min(steps, int(seconds / max(t1, 1e-9))))
+    T = reference_sweeps(ses, kind, u, f, n)
+    who = ("the reference's own csdd_smoother (proj/core/src/twogrid.cpp:114-120, compiled unmodified with "
+           "oracle/eigen_shim)" if kind == "reference" else "the C++ restatement (oracle/)")
+    sample = (f"{who} on cfg4 itself ({ses.ndof} dofs, {ses.n_subdomains} subdomains, one factor each), "
+              f"{n} sweeps after 1 warm-up, {T / n:.3f} s/sweep, {host_desc(cores)}, reference thread model "
+              f"(single-thread SpMV, parallel_for over subdomains); setup {setup_s:.1f} s untimed")
+    return ses.ndof * n / T, cores, kind, sample
 
 
 def run_reference(args):
@@ -180,28 +219,25 @@ def run_reference(args):
     if ws > 1 and rank != 0:
         return 0
     warm = max(0, args.warmup)
-    from oracle import pyoracle as po
-    po.build()
-    cores = os.cpu_count() or 1
-    po.set_threads(cores)
-    ses = po.Session(po.ProblemSpec(**CPU_SAMPLE), po.SolverConfig(coarsening=2))
+    ses, kind, cores, setup_s = reference_session(WORKLOAD)
     f = seeded_rhs(ses.ndof, 1004)
     u = np.zeros(ses.ndof, np.complex128)
-    for _ in range(warm):
-        u = ses.csdd_smoother(u, f)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        u = ses.csdd_smoother(u, f)
-    T = time.perf_counter() - t0
+    if warm:
+        reference_sweeps(ses, kind, u, f, warm)
+    T = reference_sweeps(ses, kind, u, f, args.steps)
     value = ses.ndof * args.steps / T
-    sample = (f"oracle csdd_smoother sweeps on a 100x100-cell Q4 problem ({ses.ndof} dofs, same k*h and l_dd as "
-              f"cfg4), {args.steps} timed sweeps after {warm} warm-up")
+    who = ("reference csdd_smoother (its own twogrid.cpp/fespace.cpp/... compiled unmodified against "
+           "oracle/eigen_shim; SparseLU restated as nested-dissection + left-looking LU)" if kind == "reference"
+           else "C++ restatement (oracle/) csdd_smoother")
+    sample = (f"{who}: {args.steps} timed full cfg4 sweeps ({ses.ndof} dofs) after {warm} warm-up, "
+              f"{host_desc(cores)}; setup {setup_s:.1f} s untimed")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": warm, "ms_per_step": T / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": WORKLOAD_NAME, "sample": "100x100 cells of the cfg4 per-dof work"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "config": {"workload": WORKLOAD_NAME, "ndof": ses.ndof, "subdomains": ses.n_subdomains,
+                   "subdomain_factors": ses.n_factors, "setup_s": setup_s},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -209,6 +245,81 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ GPU leg
+def kernel_rooflines(ops, prob, prof: dict, hbm_peak: float) -> dict:
+    """Achieved GB/s and fraction of the HBM roofline of every bandwidth-bound kernel
+    family, from SURVEY 8(d)'s algorithmic bytes per unit x the units one launch
+    processes, over the cold-L2 per-launch device time of htg_profile."""
+    n, nc, p = ops.ndof, ops.coarse_ndof, prob.order
+    m = p // 2
+    nx = prob.n_cells
+    ny = prob.ny or nx
+    # fine dofs with a nonzero prolongation row: vertices, the degree <= m edge
+    # functions and the (m-1)^2 lowest interior functions per cell (stage_interp, q = m)
+    ip_rows = (nx + 1) * (ny + 1) + (nx * (ny + 1) + ny * (nx + 1)) * (m - 1) + nx * ny * (m - 1) ** 2
+    fam = {
+        "k1_residual": ("r = f - A u: read u, f; write r", 48 * n, prof["residual"]),
+        "k1_k3a_residual_restrict": ("r_c = IP^H (f - A u): read u, f; write r_c", 32 * n + 16 * nc,
+                                     prof["residual_restrict"]),
+        "k1_residual_norm": ("||f - A u||^2: read u, f", 32 * n, prof["residual_norm"]),
+        "k2_combine": ("u += PoU average: read u, source map (4 B), staged y (sum |U_i|); write u",
+                       36 * n + 16 * ops.sum_u, prof["dd_combine"]),
+        "k3b_prolong": ("u += w IP u_c: read u_c; read+write the fine dofs with a nonzero IP row",
+                        16 * nc + 32 * ip_rows, prof["prolong"]),
+        "k4_coarse_apply": ("y = A_c x (QSFEM 9-point): read x, write y", 32 * nc, prof["coarse_apply"]),
+        "coarse_solve": ("A_c^-1 r_c, nested-dissection LU: nonzero halves of the pivot-block inverses "
+                         "and the off-diagonal blocks, + r_c in, u_c out", ops.coarse_read_bytes + 32 * nc,
+                         prof["coarse_solve_graph"]),
+    }
+    out = {}
+    for k, (what, nbytes, ms) in fam.items():
+        if not ms:
+            continue
+        gbs = nbytes / (ms * 1e-3) / 1e9
+        out[k] = {"bytes": nbytes, "what": what, "ms": round(ms, 5), "achieved": round(gbs, 1), "peak": hbm_peak,
+                  "unit": "GB/s", "frac": round(gbs / hbm_peak, 4)}
+    return out
+
+
+def measure_config(hb, torch, spec: dict, steps: int, flush, stream, fp64_peak: float, hbm_peak: float) -> dict:
+    """Sweep DoF/s, s per two-grid iteration and kernel rooflines of one more BASELINE
+    config (cfg3, the north star's 80-wavelength target) in the same run."""
+    prob = hb.build_problem(hb.ProblemSpec(**spec))
+    ops = hb.setup_two_grid(prob, hb.SolverConfig())
+    n = ops.ndof
+    f = torch.from_numpy(seeded_rhs(n, 1003)).cuda()
+    u = torch.zeros(n, dtype=torch.complex128, device="cuda")
+
+    def timed(fn, k):
+        evs = []
+        for _ in range(k):
+            flush.fill_(1.0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            evs.append((e0, e1))
+        torch.cuda.synchronize()
+        return sum(a.elapsed_time(b) for a, b in evs)
+
+    for _ in range(3):
+        ops.csdd_smoother(u, f)
+    T = timed(lambda: ops.csdd_smoother(u, f), steps)
+    T2 = timed(lambda: ops.two_grid_step(u, f), max(3, min(steps, 20)))
+    prof = ops.profile(u, f, reps=10)
+    dd_tf = ops.dd_flops / (prof["dd_gemm"] * 1e-3) / 1e12
+    res_gbs = BYTES_PER_DOF_RESIDUAL * n / (prof["residual"] * 1e-3) / 1e9
+    out = {"workload": f"BASELINE cfg3: Q4, {spec['wavelengths']:.0f} wavelengths, {n} dofs, seeded Gaussian RHS",
+           "ndof": n, "value": n * steps / (T * 1e-3), "unit": UNIT, "ms_per_step": T / steps,
+           "s_per_two_grid_iteration": T2 / max(3, min(steps, 20)) * 1e-3,
+           "roofline_fdm": {"achieved": dd_tf, "peak": fp64_peak, "unit": "TFLOP/s", "frac": dd_tf / fp64_peak,
+                            "algorithmic_flops_per_launch": ops.dd_flops},
+           "roofline_residual": {"achieved": res_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": res_gbs / hbm_peak},
+           "kernel_ms": {k: round(v, 5) for k, v in prof.items()},
+           "rooflines": kernel_rooflines(ops, prob, prof, hbm_peak)}
+    ops.close()
+    return out
+
+
 def run_ours(args):
     import torch
     import paper_2509_17494_b200 as hb
@@ -291,13 +402,19 @@ def run_ours(args):
     hbm_peak, hbm_src = peaks()
     res_gbs = BYTES_PER_DOF_RESIDUAL * n / (prof["residual"] * 1e-3) / 1e9
     traffic = res_traffic = None
+    traffic_src = os.path.join("profiles", "ncu_traffic.json")
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh_:
+        with open(os.path.join(ROOT, traffic_src)) as fh_:
             tj = json.load(fh_)
             traffic = tj.get("dd_dram_bytes_per_launch")
             res_traffic = tj.get("residual_dram_bytes_per_launch")
+            traffic_src = f"{traffic_src}: {tj.get('source', 'ncu --set full capture')}"
     except Exception:
-        pass
+        traffic_src = None
+    rooflines = kernel_rooflines(ops, prob, prof, hbm_peak)
+    cfg3 = None
+    if not args.no_cfg3:
+        cfg3 = measure_config(hb, torch, CFG3, max(3, min(args.steps, 20)), flush, stream, fp64_peak, hbm_peak)
     # the general dense path (every class as one batched DMMA GEMM), measured on a
     # second handle with fast diagonalisation disabled and no coarse level
     dense = None
@@ -338,23 +455,27 @@ def run_ours(args):
                              "small complex products per subdomain, 3.7x fewer than the dense product; executed as "
                              "3M DMMAs on 8-row tiles (batches of 2 subdomains) plus DFMA remainder rows",
                      "achieved": dd_tf, "peak": fp64_peak, "unit": "TFLOP/s", "frac": dd_tf / fp64_peak,
-                     "traffic": traffic,
+                     "traffic": traffic, "traffic_source": traffic_src,
                      "peak_source": "measured in this run: DMMA m8n8k4 f64 microbenchmark (no FP64 entry in "
                                     "MEASURED_PEAKS.json)",
                      "algorithmic_flops_per_launch": ops.dd_flops},
         "roofline_residual": {"bound": "hbm", "kernel": "k1_cells (r = f - A u, one thread per cell)",
                               "achieved": res_gbs, "peak": hbm_peak,
                               "unit": "GB/s", "frac": res_gbs / hbm_peak, "peak_source": hbm_src,
-                              "traffic": res_traffic,
+                              "traffic": res_traffic, "traffic_source": traffic_src,
                               "algorithmic_bytes_per_launch": BYTES_PER_DOF_RESIDUAL * n},
+        "rooflines": rooflines,
+        "rooflines_note": "every bandwidth-bound kernel family: algorithmic bytes (SURVEY 8(d)) over the mean "
+                          "cold-L2 launch time of htg_profile (10 reps, 256 MB L2 flush before each)",
+        "cfg3": cfg3,
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clocks,
         "setup_s": t_setup,
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        v, cores, sample, per, nsw = cpu_sample(args.steps, args.cpu_seconds)
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+        v, cores, kind, sample = cpu_sample(args.steps, args.cpu_seconds)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:
@@ -371,6 +492,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-dense", action="store_true", help="skip the dense-GEMM path measurement")
+    ap.add_argument("--no-cfg3", action="store_true", help="skip the cfg3 (80 wavelengths) record")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

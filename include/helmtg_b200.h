@@ -89,8 +89,10 @@ int htg_destroy(htg_handle* h);
  * (fast diagonalisation for separable classes, 8 |U_i| |Omega_i| otherwise),
  * [10] nested-dissection levels of the coarse solver, [11] the dense-path
  * flops 8 |U_i| |Omega_i| summed, [12] subdomains solved by fast
- * diagonalisation, [13] CUDA graphs cached by the handle (bounded LRU).
- * out must hold 14 entries. */
+ * diagonalisation, [13] CUDA graphs cached by the handle (bounded LRU),
+ * [14] sum of |U_i| (values staged per sweep), [15] sum of |Omega_i| (values
+ * gathered per sweep), [16] algorithmic bytes one coarse solve reads.
+ * out must hold 17 entries. */
 int htg_info(const htg_handle* h, long long* out);
 int htg_set_stream(htg_handle* h, void* stream);
 
@@ -132,7 +134,8 @@ int htg_csdd_smoother_host(htg_handle* h, double* u_host, const double* f_host);
 /* Measured FP64 tensor-core (DMMA) throughput of this GPU, TFLOP/s (the
  * roofline denominator of the dense subdomain batch). */
 int htg_measure_fp64_tensor_peak(double* tflops);
-/* Per-phase device time (ms, CUDA events on the handle's stream, mean of reps):
+/* Per-phase device time (ms, CUDA events on the handle's stream, mean of reps;
+ * every rep starts on a cold L2, a 256 MB write outside the events):
  * [0] K1 residual, [1] K2 batched subdomain GEMM, [2] K2 PoU combine,
  * [3] K1+K3a residual-restrict, [4] coarse solve, [5] K3b prolongation,
  * [6] K1 residual norm, [7] csdd_smoother sweep, [8] two_grid_step,

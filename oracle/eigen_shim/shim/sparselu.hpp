@@ -138,6 +138,7 @@ class SparseLU {
             Up_[std::size_t(k + 1)] = Index(Ui_.size());
         }
         for (auto& i : Li_) i = int(pinv_[std::size_t(i)]);
+        Li_.shrink_to_fit(); Lx_.shrink_to_fit(); Ui_.shrink_to_fit(); Ux_.shrink_to_fit();
         prow_.assign(std::size_t(n), 0);
         for (Index i = 0; i < n; ++i) prow_[std::size_t(pinv_[std::size_t(i)])] = i;
     }

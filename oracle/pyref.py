@@ -67,6 +67,8 @@ def lib():
         _lib.ref_solve.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
                                    C.POINTER(C.c_int), C.POINTER(C.c_int)]
         _lib.ref_dirichlet.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int]
+        for name in ("ref_bench_csdd", "ref_bench_two_grid"):
+            getattr(_lib, name).argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_double)]
         _lib.ref_set_threads.argtypes = [C.c_int]
         _lib.ref_set_threads.restype = None
     return _lib
@@ -200,6 +202,19 @@ class RefSession:
         it, conv = C.c_int(), C.c_int()
         _check(lib().ref_solve(self._h, _p(f), _p(u), _p(hist), cap, C.byref(it), C.byref(conv)))
         return SolveResult(u, it.value, list(hist[: it.value]), bool(conv.value))
+
+    def bench_csdd(self, u: np.ndarray, f, steps: int) -> float:
+        """`steps` reference csdd_smoother sweeps in place on u; returns the loop's wall seconds."""
+        assert u.dtype == np.complex128 and u.flags.c_contiguous and u.size == self.ndof
+        t = C.c_double()
+        _check(lib().ref_bench_csdd(self._h, _p(u), _p(cvec(f)), int(steps), C.byref(t)))
+        return t.value
+
+    def bench_two_grid(self, u: np.ndarray, f, steps: int) -> float:
+        assert u.dtype == np.complex128 and u.flags.c_contiguous and u.size == self.ndof
+        t = C.c_double()
+        _check(lib().ref_bench_two_grid(self._h, _p(u), _p(cvec(f)), int(steps), C.byref(t)))
+        return t.value
 
     def multiplicity(self) -> np.ndarray:
         out = np.zeros(self.ndof)

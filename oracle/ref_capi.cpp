@@ -14,6 +14,7 @@
 // rectangle-with-per-cell-coefficients constructor built from the reference's
 // own StructuredMesh::rectangle / tag_boundary / CoefficientField::set_k|set_eps.
 // Vectors cross the ABI as interleaved complex doubles (std::complex<double>[]).
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -364,6 +365,37 @@ int ref_partition_sizes(void* h, int* out) {
             out[k++] = int(sub.global_dofs.size());
             out[k++] = int(sub.u_members.size());
         }
+    });
+}
+
+// Timing loop in the style of BM_TwoGridStep (proj/benchmarks/bench_solver.cpp:9-22):
+// `steps` calls of the reference's csdd_smoother on caller-owned u, f (no copies in
+// the loop). Returns the wall seconds of the loop (steady_clock) in *seconds.
+int ref_bench_csdd(void* h, double* u, const double* f, int steps, double* seconds) {
+    return guard([&] {
+        const TwoGridOperators& o = ops_of(h);
+        if (!o.dd) throw std::invalid_argument("no domain decomposition (smoother is not CSDD)");
+        const long n = o.A.rows();
+        ComplexVector uu = vin(u, n);
+        const ComplexVector ff = vin(f, n);
+        const auto t0 = std::chrono::steady_clock::now();
+        for (int i = 0; i < steps; ++i) csdd_smoother(uu, ff, o.A, o.As, *o.dd, S(h)->cfg.n_dd);
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        vout(uu, u);
+    });
+}
+
+// Same for two_grid_step (coarse solve included).
+int ref_bench_two_grid(void* h, double* u, const double* f, int steps, double* seconds) {
+    return guard([&] {
+        const TwoGridOperators& o = ops_of(h);
+        const long n = o.A.rows();
+        ComplexVector uu = vin(u, n);
+        const ComplexVector ff = vin(f, n);
+        const auto t0 = std::chrono::steady_clock::now();
+        for (int i = 0; i < steps; ++i) two_grid_step(uu, ff, o, S(h)->cfg);
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        vout(uu, u);
     });
 }
 

@@ -340,6 +340,7 @@ class NDSolver : public CoarseSolver {
     }
     size_t device_bytes() const override { return bytes_; }
     int levels() const override { return nlevels_; }
+    size_t solve_read_bytes() const override { return read_bytes_; }
 
     // Forward: the subtrees below the split depth run on forked streams (in a
     // CUDA graph: parallel branches), deepest level first, then the top levels;
@@ -422,6 +423,7 @@ class NDSolver : public CoarseSolver {
     int nlevels_ = 0;
     std::vector<void*> allocs_;
     size_t bytes_ = 0;
+    size_t read_bytes_ = 0;
     int nv_ = 0;
     long long delayed_ = 0;
     NDArgs args_{};
@@ -586,6 +588,7 @@ class NDSolver : public CoarseSolver {
             const NodeDev& d = nd[i];
             Level& lv = lvs[k];
             const int F = d.s + d.u;
+            read_bytes_ += sizeof(double2) * (size_t(d.s) * (d.s + 1) + 2 * size_t(d.s) * d.u);
             if (F <= warpF) {
                 wp[k].push_back(d);
             } else if ((long long)d.s * F <= midData) {

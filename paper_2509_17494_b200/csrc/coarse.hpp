@@ -30,6 +30,9 @@ class CoarseSolver {
     virtual void solve(const double2* rc, double2* uc, cudaStream_t st) = 0;
     virtual size_t device_bytes() const = 0;
     virtual int levels() const = 0;
+    // algorithmic bytes one solve reads: the nonzero halves of the triangular
+    // pivot-block inverses plus the off-diagonal factor blocks, 16 B per entry
+    virtual size_t solve_read_bytes() const = 0;
 };
 std::unique_ptr<CoarseSolver> make_coarse_solver(const HostProblem& hp, cudaStream_t st);
 
