@@ -785,17 +785,23 @@ int htg_profile(htg_handle* h, double* u, const double* f, int reps, double* ms)
         if (!h->dd.nsub) throw InvalidArgument("handle has no CSDD smoother");
         double2* U = D2(u);
         const double2* Fv = CD2(f);
-        // every rep runs on a cold L2: a 256 MB write (> the 126 MB L2) precedes it,
-        // outside the events; the mean of the per-rep event intervals is reported
+        // every rep runs on a cold, clean L2: a 256 MB write (> the 126 MB L2) and then
+        // a 256 MB read of another buffer precede it, outside the events (the read
+        // writes back the lines the flush write left dirty, which would otherwise be
+        // charged to the kernel); the mean of the per-rep event intervals is reported
         void* flush = nullptr;
         const size_t flush_bytes = size_t(256) << 20;
-        HTG_CUDA(cudaMalloc(&flush, flush_bytes));
+        HTG_CUDA(cudaMalloc(&flush, 2 * flush_bytes + 64));
+        char* flush_rd = static_cast<char*>(flush) + flush_bytes;
+        double* sink = reinterpret_cast<double*>(flush_rd + flush_bytes);
+        HTG_CUDA(cudaMemsetAsync(flush_rd, 0, flush_bytes, h->st));
         std::vector<cudaEvent_t> ev(2 * size_t(std::max(reps, 1)));
         for (auto& e : ev) HTG_CUDA(cudaEventCreate(&e));
         auto timeit = [&](auto&& fn) {
             fn();  // warm (captures graphs, first-touch)
             for (int i = 0; i < reps; ++i) {
                 HTG_CUDA(cudaMemsetAsync(flush, i & 0xff, flush_bytes, h->st));
+                l2_read(flush_rd, flush_bytes, sink, h->st);
                 HTG_CUDA(cudaEventRecord(ev[2 * i], h->st));
                 fn();
                 HTG_CUDA(cudaEventRecord(ev[2 * i + 1], h->st));

@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.hpp"
 #include "kernels.hpp"
@@ -37,11 +38,18 @@ namespace {
 constexpr int kFGroups = HTG_FDM_GROUPS, kFThreads = kFGroups * 128;
 constexpr int kSmemMax = 232448;  // opt-in dynamic shared memory per block (227 KB)
 
-// Row pitch of every operand (double2): 4 mod 8 keeps the 128-bit fragment
-// loads of 8 lanes (2 rows x 4 k) on distinct banks; k steps cover [0, 4 KS).
+// Row pitch of every operand (double2). An odd pitch puts the 8 rows x 4 k of a
+// 128-bit fragment load, the 8 rows x 2 columns of an epilogue store (row-major
+// and transposed) and 8 consecutive rows of a remainder dot on distinct bank
+// groups (a pitch of 4 mod 8 left the epilogue stores and the dots two-way
+// conflicted); k steps cover [0, 4 KS).
+#ifndef HTG_FDM_ODD_LD
+#define HTG_FDM_ODD_LD 1
+#endif
 template <int P> struct FdmDims;
-template <> struct FdmDims<2> { static constexpr int LD = 20, KS = 4; };  // extents <= 16
-template <> struct FdmDims<4> { static constexpr int LD = 28, KS = 7; };  // extents <= 28
+template <> struct FdmDims<2> { static constexpr int LD = HTG_FDM_ODD_LD ? 17 : 20, KS = 4; };  // extents <= 16
+template <> struct FdmDims<4> { static constexpr int LD = HTG_FDM_ODD_LD ? 29 : 28, KS = 7; };  // extents <= 28
+constexpr bool kSkew = !HTG_FDM_ODD_LD;  // xor-skew the k of remainder dots (even pitch only)
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -78,8 +86,12 @@ constexpr int kKP = HTG_FDM_KSPLIT;  // independent accumulator chains per produ
 #define HTG_FDM_TG 4
 #endif
 constexpr int kTG = HTG_FDM_TG;  // moving tiles in flight per warp (one stationary fragment set)
+#ifndef HTG_FDM_DR
+#define HTG_FDM_DR 0
+#endif
+constexpr bool kDataRem = HTG_FDM_DR != 0;  // data-row remainders on the CUDA cores (group kernel)
 
-template <int LD, int KS>
+template <int LD, int KS, bool FTR = false>
 struct Stage {
     const double2* fac;  // factor operand [F][LD] (zero k padding)
     int F;               // factor rows (the padded output dimension)
@@ -87,6 +99,9 @@ struct Stage {
     int nd;              // data rows of the batch
     bool sa;             // the factor is the A operand (C[factor][data]); else B (C[data][factor])
     int q, lane;
+    int fo = 0;          // FTR (transposed factor): row f, k at fac[k * LD + fo + f]
+
+    __device__ __forceinline__ double2 fval(int f, int k) const { return FTR ? fac[k * LD + fo + f] : fac[f * LD + k]; }
 
     using Acc = double[kKP][kTG][2];
     template <int NTL, class Epi>
@@ -165,15 +180,19 @@ struct Stage {
     }
 
     // full 8-row tiles ST of the factor on DMMA, the last FR <= 2 factor rows
-    // on the CUDA cores (a padded tile would be 7/8 or 6/8 zeros)
+    // on the CUDA cores (a padded tile would be 7/8 or 6/8 zeros); likewise the
+    // last DR <= 2 data rows (HTG_FDM_DR, default on: 50 = 6 x 8 + 2 data rows
+    // of a two-subdomain batch at p = 4)
     template <class Epi>
     __device__ __forceinline__ void operator()(Epi&& epi) const {
         const int r = lane >> 2, kq = lane & 3;
         const int FR = (F & 7) <= 2 ? (F & 7) : 0;
-        const int ST = (F - FR + 7) >> 3, OT = (nd + 7) >> 3;
+        const int DR = kDataRem && (nd & 7) <= 2 ? (nd & 7) : 0;
+        const int ST = (F - FR + 7) >> 3, OT = (nd - DR + 7) >> 3;
+        const int FT = F - FR, n1 = FR * nd, n2 = DR * FT;
         // warp q: stationary tiles st0, st0 + sstep, ..; moving tiles [o_lo, o_hi);
-        // remainder items [i_lo, i_hi) of FR x nd
-        int st0 = q, sstep = 4, o_lo = 0, o_hi = OT, nrem = FR * nd, i_lo = 0, i_hi = 0;
+        // remainder items [i_lo, i_hi) of the n1 + n2 dot products
+        int st0 = q, sstep = 4, o_lo = 0, o_hi = OT, nrem = n1 + n2, i_lo = 0, i_hi = 0;
         if (ST == 3) {
             if (q == 3) st0 = ST, i_hi = nrem;
         } else if (ST == 2) {
@@ -192,14 +211,14 @@ struct Stage {
         } else {
             i_lo = q * nrem / 4, i_hi = (q + 1) * nrem / 4;
         }
-        const int flim = F - FR - 1, dlim = nd - 1;
+        const int flim = FT - 1, dlim = nd - DR - 1;
         for (int st = st0; st < ST; st += sstep) {
             double2 sf[KS];
             double ss[KS];
-            const double2* srow = fac + min(st * 8 + r, flim) * LD + kq;
+            const int frow = min(st * 8 + r, flim);
 #pragma unroll
             for (int ks = 0; ks < KS; ++ks) {
-                sf[ks] = srow[ks * 4];
+                sf[ks] = fval(frow, ks * 4 + kq);
                 ss[ks] = sf[ks].x + sf[ks].y;
             }
             for (int o0 = o_lo; o0 < o_hi; o0 += kTG) {
@@ -217,21 +236,34 @@ struct Stage {
         // remainder: one complex dot product of a factor row and a data row per
         // lane; k is xor-skewed by the data row so 8 lanes hit distinct banks
         for (int it = i_lo + lane; it < i_hi; it += 32) {
-            const int f = it / nd, d = it - f * nd;
-            const double2* fr = fac + (F - FR + f) * LD;
+            int f, d;
+            if (it < n1) {
+                const int a = it / nd;
+                f = FT + a;
+                d = it - a * nd;
+            } else {
+                const int j = it - n1, a = j / FT;
+                d = nd - DR + a;
+                f = j - a * FT;
+            }
             const double2* dr = dat + d * LD;
-            const int sk = d & 3;
-            double re = 0.0, im = 0.0;
+            const int sk = kSkew ? (d & 3) : 0;
+            // 8 independent accumulator chains (4 terms x k parity): the dot is
+            // DFMA-latency bound otherwise
+            double acc[2][4] = {};
 #pragma unroll
             for (int kk = 0; kk < 4 * KS; ++kk) {
-                const double2 a = fr[kk ^ sk], b = dr[kk ^ sk];
-                re = fma(a.x, b.x, re);
-                re = fma(-a.y, b.y, re);
-                im = fma(a.x, b.y, im);
-                im = fma(a.y, b.x, im);
+                const double2 a = fval(f, kk ^ sk), b = dr[kk ^ sk];
+                double* c = acc[kk & 1];
+                c[0] = fma(a.x, b.x, c[0]);
+                c[1] = fma(a.y, b.y, c[1]);
+                c[2] = fma(a.x, b.y, c[2]);
+                c[3] = fma(a.y, b.x, c[3]);
             }
-            if (sa) epi(F - FR + f, d, make_double2(re, im));
-            else epi(d, F - FR + f, make_double2(re, im));
+            const double re = (acc[0][0] + acc[1][0]) - (acc[0][1] + acc[1][1]);
+            const double im = (acc[0][2] + acc[1][2]) + (acc[0][3] + acc[1][3]);
+            if (sa) epi(f, d, make_double2(re, im));
+            else epi(d, f, make_double2(re, im));
         }
     }
 };
@@ -277,20 +309,17 @@ __global__ void __launch_bounds__(kFThreads, 1) k_dd_fdm(FineGeom g, const FdmCl
         const FdmClassDev c = classes[ci];
         const int seg_end = min(wk.y, c.first + c.nsub);
         const int nx = c.nx, ny = c.ny, nux = c.nux, nuy = c.nuy;
-        double2* V1T = fac;              // [ix'][ix] = Vx[ix][ix']
-        double2* V2T = V1T + nx * LD;    // [iy'][iy] = Vy[iy][iy']
-        double2* V1U = V2T + ny * LD;    // [ixu][ix'] = Vx[ux0 + ixu][ix']
-        double2* V2U = V1U + nux * LD;   // [iyu][iy'] = Vy[uy0 + iyu][iy']
-        double2* D = V2U + nuy * LD;     // Dinv[ix'][iy']
+        constexpr int KP = 4 * KS;
+        double2* V1T = fac;            // [ix'][ix] = Vx[ix][ix'], KP rows (rows >= nx zero); the U-row
+        double2* V2T = V1T + KP * LD;  // factor Vx[ux0 + ixu][ix'] of stage 3 is V1T[ix'][ux0 + ixu]
+        double2* D = V2T + KP * LD;    // Dinv[ix'][iy']
         __syncthreads();  // previous segment finished with the factors
         const double2 z = make_double2(0.0, 0.0);
-        for (int i = tid; i < (nx + ny + nux + nuy) * LD; i += kFThreads) {
+        for (int i = tid; i < 2 * KP * LD; i += kFThreads) {
             const int a = i / LD, b = i - a * LD;
             double2 v = z;
-            if (a < nx) v = b < nx ? c.Vx[b * nx + a] : z;
-            else if (a < nx + ny) v = b < ny ? c.Vy[b * ny + (a - nx)] : z;
-            else if (a < nx + ny + nux) v = b < nx ? c.Vx[(c.ux0 + a - nx - ny) * nx + b] : z;
-            else v = b < ny ? c.Vy[(c.uy0 + a - nx - ny - nux) * ny + b] : z;
+            if (a < KP) v = (a < nx && b < nx) ? c.Vx[b * nx + a] : z;
+            else v = (a - KP < ny && b < ny) ? c.Vy[b * ny + (a - KP)] : z;
             fac[i] = v;
         }
         for (int i = tid; i < nx * ny; i += kFThreads) D[i] = c.Dinv[i];
@@ -391,7 +420,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_dd_fdm(FineGeom g, const FdmCl
             group_sync(grp);
             HTG_CLK(3);
             // 3: R[ixu][(s,iy')] = sum_ix' Vx[ux0 + ixu][ix'] Q[(s,iy')][ix']  -> W[(s,ixu)][iy']
-            Stage<LD, KS>{V1U, nux, X, nb * ny, true, q, lane}([&](int m, int n, double2 v) {
+            Stage<LD, KS, true>{V1T, nux, X, nb * ny, true, q, lane, c.ux0}([&](int m, int n, double2 v) {
                 if (m < nux && n < nb * ny) {
                     const int s = fdiv(n, inv_ny);
                     W[(s * nux + m) * LD + n - s * ny] = v;
@@ -407,7 +436,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_dd_fdm(FineGeom g, const FdmCl
             if (bi + 1 < nbatch) gather(bsize(bi + 1), par ^ 1);
             HTG_CLK(5);
             // 4: Y[(s,ixu)][iyu] = sum_iy' R[(s,ixu)][iy'] Vy[uy0 + iyu][iy']  -> staging rows
-            Stage<LD, KS>{V2U, nuy, W, nb * nux, false, q, lane}(
+            Stage<LD, KS, true>{V2T, nuy, W, nb * nux, false, q, lane, c.uy0}(
                 [&](int m, int n, double2 v) {
                     if (m < nb * nux && n < nuy) {
                         const int s = fdiv(m, inv_nux), ixu = m - s * nux;
@@ -433,6 +462,219 @@ int fdm_rows(int fac_elems) {
     return (kSmemMax / int(sizeof(double2)) - fac_elems) / (kFGroups * 2 * FdmDims<P>::LD);
 }
 
+// ---------------------------------------------------------------- team per subdomain
+// A team of NP warps (NP = 1 or 2) runs all four products of one subdomain,
+// synchronised only by a team barrier between stages, so the DMMA pipe of an
+// SM sub-partition is fed by independent teams instead of 4-warp groups
+// waiting on each other's stage tails. The tiles of a product are split
+// evenly over the team (the odd tile alternates between the warps from stage
+// to stage); factor rows 8t + FR and data rows 8t + DR with FR, DR <= 2 run
+// their last rows as DFMA dot products spread over the team's lanes (25 = 3 x
+// 8 + 1 and 17 = 2 x 8 + 1 at p = 4: 588 DMMAs per subdomain against 693 for
+// the batched 4-warp form). The U-row factors of stages 3 and 4 are read
+// transposed out of Vx^T, Vy^T (their rows are columns there), which leaves
+// shared memory for 8 teams of two 25-row buffers each at p = 4.
+#ifndef HTG_FDM_TGW
+#define HTG_FDM_TGW 3
+#endif
+constexpr int kTGW = HTG_FDM_TGW < kTG ? HTG_FDM_TGW : kTG;  // moving tiles in flight (team kernel)
+
+template <int LD, int KS, bool FTR>
+struct WStage {
+    const double2* fac;  // FTR: factor row f, k at fac[k * LD + fo + f]; else fac[f * LD + k]
+    int F, fo;
+    const double2* dat;  // data rows [0, nd), [row][k]
+    int nd;
+    bool sa;             // C[factor][data] (else C[data][factor])
+    int lane;
+    int part, np;        // this warp's share of the team's tiles and dot products
+
+    __device__ __forceinline__ double2 fval(int f, int k) const {
+        return FTR ? fac[k * LD + fo + f] : fac[f * LD + k];
+    }
+
+    template <class Epi>
+    __device__ __forceinline__ void operator()(Epi&& epi) const {
+        const Stage<LD, KS> b{fac, F, dat, nd, sa, 0, lane};
+        const int r = lane >> 2, kq = lane & 3;
+        const int FR = (F & 7) <= 2 ? (F & 7) : 0, DR = (nd & 7) <= 2 ? (nd & 7) : 0;
+        const int ST = (F - FR + 7) >> 3, OT = (nd - DR + 7) >> 3;
+        const int flim = F - FR - 1, dlim = nd - DR - 1;
+        // tiles (st, ot) flattened st-major; this warp takes [t0, t1)
+        const int T = ST * OT, t0 = T * part / np, t1 = T * (part + 1) / np;
+        for (int t = t0; t < t1;) {
+            const int st = t / OT, o_lo = t - st * OT, o_hi = min(OT, o_lo + (t1 - t));
+            double2 sf[KS];
+            double ss[KS];
+            const int fr = min(st * 8 + r, flim);
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) {
+                sf[ks] = fval(fr, ks * 4 + kq);
+                ss[ks] = sf[ks].x + sf[ks].y;
+            }
+            for (int o0 = o_lo; o0 < o_hi; o0 += kTGW) {
+                const int nt = min(kTGW, o_hi - o0);
+                int mrow[kTG], tm[kTG], tn[kTG];
+#pragma unroll
+                for (int j = 0; j < kTG; ++j) {
+                    mrow[j] = min((o0 + j) * 8 + r, dlim) * LD + kq;
+                    tm[j] = sa ? st : o0 + j;
+                    tn[j] = sa ? o0 + j : st;
+                }
+                b.template dispatch<kTGW>(nt, sf, ss, mrow, tm, tn, epi);
+            }
+            t += o_hi - o_lo;
+        }
+        // remainder rows: factor rows [F - FR, F) x all data rows, then data rows
+        // [nd - DR, nd) x the tiled factor rows; one complex dot per lane
+        const int FT = F - FR, n1 = FR * nd, n2 = DR * FT;
+        for (int it = part * 32 + lane; it < n1 + n2; it += np * 32) {
+            int f, d;
+            if (it < n1) {
+                const int a = it / nd;
+                f = FT + a;
+                d = it - a * nd;
+            } else {
+                const int j = it - n1, a = j / FT;
+                d = nd - DR + a;
+                f = j - a * FT;
+            }
+            const double2* dr = dat + d * LD;
+            const int sk = kSkew ? (d & 3) : 0;
+            double acc[2][4] = {};  // independent chains, as in Stage
+#pragma unroll
+            for (int kk = 0; kk < 4 * KS; ++kk) {
+                const double2 a = fval(f, kk ^ sk), bb = dr[kk ^ sk];
+                double* c = acc[kk & 1];
+                c[0] = fma(a.x, bb.x, c[0]);
+                c[1] = fma(a.y, bb.y, c[1]);
+                c[2] = fma(a.x, bb.y, c[2]);
+                c[3] = fma(a.y, bb.x, c[3]);
+            }
+            const double re = (acc[0][0] + acc[1][0]) - (acc[0][1] + acc[1][1]);
+            const double im = (acc[0][2] + acc[1][2]) + (acc[0][3] + acc[1][3]);
+            if (sa) epi(f, d, make_double2(re, im));
+            else epi(d, f, make_double2(re, im));
+        }
+    }
+};
+
+// CTA size the kernel is compiled for: NP = 1 at p = 4 runs 8 warps (shared
+// memory holds 8 buffer pairs), so the register budget is the full 255 per thread
+#ifndef HTG_FDM_TTHREADS
+#define HTG_FDM_TTHREADS 512
+#endif
+constexpr int kWThreads(int p, int np) { return (np == 1 && p == 4) ? 256 : (np == 2 && p == 4 ? HTG_FDM_TTHREADS : 512); }
+
+template <int NP>
+__device__ __forceinline__ void team_sync(int team) {
+    if constexpr (NP == 1) __syncwarp();
+    else asm volatile("bar.sync %0, %1;\n" ::"r"(team + 1), "r"(NP * 32) : "memory");
+}
+
+template <int P, int NP>
+__global__ void __launch_bounds__(kWThreads(P, NP), 1)
+    k_dd_fdm_w(FineGeom g, const FdmClassDev* __restrict__ classes, const int4* __restrict__ work,
+               const double2* __restrict__ r, double2* __restrict__ ystage, int nu_max, int rows, int fac_elems) {
+    constexpr int LD = FdmDims<P>::LD, KS = FdmDims<P>::KS, KP = 4 * KS;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double2* fac = reinterpret_cast<double2*>(smem_raw);
+    const int tid = threadIdx.x, nthr = blockDim.x, nteam = nthr / (32 * NP);
+    const int warp = tid >> 5, lane = tid & 31, team = warp / NP, part = warp - team * NP;
+    const int tl = part * 32 + lane;                               // lane within the team
+    double2* X = fac + fac_elems + size_t(team) * 2 * rows * LD;  // gathered tile, then Q o Dinv
+    double2* W = X + rows * LD;                                   // stage 1 / stage 3 products
+    {  // the k padding of the data buffers must be finite: zero them once
+        double2* data = fac + fac_elems;
+        for (int i = tid; i < nteam * 2 * rows * LD; i += nthr) data[i] = make_double2(0.0, 0.0);
+    }
+    double2* V1T = fac;            // [ix'][ix] = Vx[ix][ix'], KP rows (rows >= nx zero)
+    double2* V2T = V1T + KP * LD;  // [iy'][iy] = Vy[iy][iy']
+    double2* D = V2T + KP * LD;    // Dinv[ix'][iy']
+    const int4 wk = work[blockIdx.x];
+    int pos = wk.x;
+    while (pos < wk.y) {
+        int ci = 0;
+        while (classes[ci].first + classes[ci].nsub <= pos) ++ci;
+        const FdmClassDev c = classes[ci];
+        const int seg_end = min(wk.y, c.first + c.nsub);
+        const int nx = c.nx, ny = c.ny, nux = c.nux, nuy = c.nuy;
+        int* urow = reinterpret_cast<int*>(D + nx * ny);
+        int* gofs = urow + nux * nuy;
+        __syncthreads();  // previous segment finished with the factors
+        const double2 z = make_double2(0.0, 0.0);
+        for (int i = tid; i < 2 * KP * LD; i += nthr) {
+            const int a = i / LD, b = i - a * LD;
+            double2 v = z;
+            if (a < KP) v = (a < nx && b < nx) ? c.Vx[b * nx + a] : z;
+            else v = (a - KP < ny && b < ny) ? c.Vy[b * ny + (a - KP)] : z;
+            fac[i] = v;
+        }
+        for (int i = tid; i < nx * ny; i += nthr) D[i] = c.Dinv[i];
+        for (int i = tid; i < nux * nuy; i += nthr) {
+            const int ixu = i / nuy, iyu = i - ixu * nuy;
+            urow[i] = c.rowmap[dof_index(c.onx, c.ony, P, c.ux0 + ixu, c.uy0 + iyu)];
+        }
+        if (c.goff)
+            for (int i = tid; i < nx * ny; i += nthr) gofs[i] = c.goff[i];
+        __syncthreads();
+        const int nxy = nx * ny;
+        const float inv_nx = 1.0f / nx;
+        auto gather = [&](int sidx) {
+            const int so = c.sub_o[c.subs[sidx - c.first]];
+            const int ox = (so & 0xffff) * P, oy = (so >> 16) * P;
+            if (c.goff) {
+                const double2* rb = r + dof_index(g.nx, g.ny, P, ox, oy);
+                for (int l = tl; l < nxy; l += NP * 32) {
+                    const int iy = fdiv(l, inv_nx), ix = l - iy * nx;
+                    cp_async16(&X[iy * LD + ix], rb + gofs[l]);
+                }
+            } else {
+                for (int l = tl; l < nxy; l += NP * 32) {
+                    const int iy = fdiv(l, inv_nx), ix = l - iy * nx;
+                    cp_async16(&X[iy * LD + ix], r + dof_index(g.nx, g.ny, P, ox + ix, oy + iy));
+                }
+            }
+            asm volatile("cp.async.commit_group;\n" ::: "memory");
+        };
+        int cur = pos + team;
+        if (cur < seg_end) gather(cur);
+        for (; cur < seg_end; cur += nteam) {
+            const int id = c.subs[cur - c.first];
+            asm volatile("cp.async.wait_all;\n" ::: "memory");
+            team_sync<NP>(team);
+            // 1: P[ix'][iy] = sum_ix Vx[ix][ix'] G[iy][ix]  -> W[ix'][iy]
+            WStage<LD, KS, false>{V1T, nx, 0, X, ny, true, lane, part, NP}([&](int m, int n, double2 v) {
+                if (m < nx && n < ny) W[m * LD + n] = v;
+            });
+            team_sync<NP>(team);
+            // 2: Q[ix'][iy'] = (sum_iy P[ix'][iy] Vy[iy][iy']) Dinv[ix'][iy']  -> X[iy'][ix']
+            WStage<LD, KS, false>{V2T, ny, 0, W, nx, false, lane, NP - 1 - part, NP}([&](int m, int n, double2 v) {
+                if (m < nx && n < ny) {
+                    const double2 d = D[m * ny + n];
+                    X[n * LD + m] = make_double2(v.x * d.x - v.y * d.y, v.x * d.y + v.y * d.x);
+                }
+            });
+            team_sync<NP>(team);
+            // 3: R[ixu][iy'] = sum_ix' Vx[ux0 + ixu][ix'] Q[iy'][ix']  -> W[ixu][iy']
+            WStage<LD, KS, true>{V1T, nux, c.ux0, X, ny, true, lane, part, NP}([&](int m, int n, double2 v) {
+                if (m < nux && n < ny) W[m * LD + n] = v;
+            });
+            team_sync<NP>(team);
+            // the gathered tile is free: fetch the team's next subdomain under stage 4
+            if (cur + nteam < seg_end) gather(cur + nteam);
+            // 4: Y[ixu][iyu] = sum_iy' R[ixu][iy'] Vy[uy0 + iyu][iy']  -> staging row of the subdomain
+            double2* yrow = ystage + (size_t)id * nu_max;
+            WStage<LD, KS, true>{V2T, nuy, c.uy0, W, nux, false, lane, NP - 1 - part, NP}(
+                [&](int m, int n, double2 v) {
+                    if (m < nux && n < nuy) yrow[urow[m * nuy + n]] = v;
+                });
+        }
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        pos = seg_end;
+    }
+}
+
 }  // namespace
 
 // fdm_supported (fdm.cpp) admits 1-D extents up to 4 KS
@@ -444,6 +686,7 @@ void dd_fdm_launch(const FineGeom& g, const FdmLaunch& L, const double2* r, doub
                    cudaStream_t st) {
     if (L.nwork == 0) return;
     static bool attr[9] = {};
+    static bool attr_w[9] = {};
     auto go = [&](auto kern, int p) {
         if (!attr[p]) {
             HTG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
@@ -451,10 +694,26 @@ void dd_fdm_launch(const FineGeom& g, const FdmLaunch& L, const double2* r, doub
         }
         kern<<<L.nwork, kFThreads, L.smem, st>>>(g, L.classes, L.work, r, ystage, nu_max, L.rows, L.fac_elems);
     };
-    switch (g.p) {
-        case 2: go(k_dd_fdm<2>, 2); break;
-        case 4: go(k_dd_fdm<4>, 4); break;
-        default: throw InvalidArgument("FDM subdomain kernel: p must be 2 or 4");
+    auto go_w = [&](auto kern, int slot) {
+        if (!attr_w[slot]) {
+            HTG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
+            attr_w[slot] = true;
+        }
+        kern<<<L.nwork, L.nwarps * 32, L.smem, st>>>(g, L.classes, L.work, r, ystage, nu_max, L.rows, L.fac_elems);
+    };
+    if (L.nwarps > 0) {
+        const bool pair = L.team == 2;
+        switch (g.p) {
+            case 2: pair ? go_w(k_dd_fdm_w<2, 2>, 0) : go_w(k_dd_fdm_w<2, 1>, 1); break;
+            case 4: pair ? go_w(k_dd_fdm_w<4, 2>, 2) : go_w(k_dd_fdm_w<4, 1>, 3); break;
+            default: throw InvalidArgument("FDM subdomain kernel: p must be 2 or 4");
+        }
+    } else {
+        switch (g.p) {
+            case 2: go(k_dd_fdm<2>, 2); break;
+            case 4: go(k_dd_fdm<4>, 4); break;
+            default: throw InvalidArgument("FDM subdomain kernel: p must be 2 or 4");
+        }
     }
     HTG_CUDA(cudaGetLastError());
     count_launch();
@@ -469,15 +728,40 @@ std::vector<int4> fdm_plan(std::vector<FdmClassDev>& cls, int p, int nsm, FdmLau
     for (auto& c : cls) {
         c.first = total;
         total += c.nsub;
-        fac = std::max(fac, (c.nx + c.ny + c.nux + c.nuy) * LD + c.nx * c.ny +
+        fac = std::max(fac, 2 * (p == 2 ? 4 * FdmDims<2>::KS : 4 * FdmDims<4>::KS) * LD + c.nx * c.ny +
                                 (kFGroups * 32 + c.nux * c.nuy + c.nx * c.ny + 3) / 4);
         ext = std::max({ext, c.nx, c.ny});
     }
-    fac = (fac + 7) / 8 * 8;
-    L.fac_elems = fac;
-    L.rows = p == 2 ? fdm_rows<2>(fac) : fdm_rows<4>(fac);
-    if (L.rows < ext) throw RuntimeError("FDM subdomain kernel: shared memory too small for the class extents");
-    L.smem = size_t(fac + kFGroups * 2 * L.rows * LD) * sizeof(double2);
+    // team-per-subdomain kernel (default: 2-warp teams; HTG_FDM_TEAM=1 one warp per
+    // subdomain; HTG_FDM_GROUPK=1 selects the batched 4-warp-group kernel)
+    const char* gk = std::getenv("HTG_FDM_GROUPK");
+    const char* tk = std::getenv("HTG_FDM_TEAM");
+    L.nwarps = 0;
+    L.team = (tk && tk[0] == '1') ? 1 : 2;
+    if (!(gk && gk[0] == '1')) {
+        const int KP = p == 2 ? 4 * FdmDims<2>::KS : 4 * FdmDims<4>::KS;
+        int wfac = 0;
+        for (auto& c : cls)
+            wfac = std::max(wfac, 2 * KP * LD + c.nx * c.ny + (c.nux * c.nuy + c.nx * c.ny + 3) / 4);
+        wfac = (wfac + 7) / 8 * 8;
+        const int per_warp = 2 * ext * LD;
+        int nt = (kSmemMax / int(sizeof(double2)) - wfac) / per_warp;  // teams (buffer pairs)
+        nt = std::min(nt, kWThreads(p, L.team) / (32 * L.team));
+        if (nt * L.team >= 8) nt = (nt * L.team) / 4 * 4 / L.team;  // whole warps per SM sub-partition
+        if (nt >= 1) {
+            L.nwarps = nt * L.team;
+            L.fac_elems = wfac;
+            L.rows = ext;
+            L.smem = size_t(wfac + nt * per_warp) * sizeof(double2);
+        }
+    }
+    if (L.nwarps == 0) {
+        fac = (fac + 7) / 8 * 8;
+        L.fac_elems = fac;
+        L.rows = p == 2 ? fdm_rows<2>(fac) : fdm_rows<4>(fac);
+        if (L.rows < ext) throw RuntimeError("FDM subdomain kernel: shared memory too small for the class extents");
+        L.smem = size_t(fac + kFGroups * 2 * L.rows * LD) * sizeof(double2);
+    }
     std::vector<int4> work;
     if (total == 0) return work;
     const int ctas = std::min(nsm, total);

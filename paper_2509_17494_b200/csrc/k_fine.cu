@@ -1363,6 +1363,18 @@ __global__ void k_zero(double2* __restrict__ y, long long n) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
         y[i] = make_double2(0.0, 0.0);
 }
+// L2 flush helper (timing only): reads a buffer larger than L2 so the lines a
+// preceding flush write left dirty are written back before the timed region
+__global__ void k_l2_read(const double4* __restrict__ b, long long n, double* sink) {
+    double s = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        s += b[i].x;
+    if (s == 12345.678) sink[0] = s;  // never true for the flush pattern; keeps the loads
+}
+void l2_read(const void* buf, size_t bytes, double* sink, cudaStream_t st) {
+    k_l2_read<<<148 * 8, 256, 0, st>>>(static_cast<const double4*>(buf), (long long)(bytes / sizeof(double4)), sink);
+    HTG_CUDA(cudaGetLastError());
+}
 static unsigned vec_blocks(long long n) { return unsigned(std::min<long long>((n + 255) / 256, 148 * 8)); }
 void inclusion_restrict_launch(const double2* r, const int* map, long long nc, double2* rc, cudaStream_t st) {
     k_incl_restrict<<<vec_blocks(nc), 256, 0, st>>>(r, map, nc, rc);

@@ -46,6 +46,9 @@ void inclusion_prolong_launch(double2* u, const int* map, long long nc, const do
 void csr_apply_launch(const int* rp, const int* ci, const double2* v, long long n, const double2* x, double2* y,
                       cudaStream_t st);
 
+// timing only: read `bytes` of buf (evicts and writes back dirty L2 lines)
+void l2_read(const void* buf, size_t bytes, double* sink, cudaStream_t st);
+
 // vectors
 void vec_axpy(double2* y, const double2* x, double a, long long n, cudaStream_t st);  // y += a x
 void vec_copy(double2* y, const double2* x, long long n, cudaStream_t st);
@@ -100,6 +103,8 @@ struct FdmLaunch {
     int rows;                    // data rows per buffer (S = rows / max(nx, ny) subdomains per batch)
     int fac_elems;               // factor region (double2) sized for the largest class
     size_t smem;                 // dynamic shared memory per CTA
+    int nwarps = 0;              // > 0: team-per-subdomain kernel with this many warps per CTA
+    int team = 2;                // warps per subdomain of that kernel
 };
 void dd_fdm_launch(const FineGeom& g, const FdmLaunch& L, const double2* r, double2* ystage, int nu_max,
                    cudaStream_t st);

@@ -12,7 +12,7 @@ import paper_2509_17494_b200 as hb  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--wavelengths", type=float, default=160)
 ap.add_argument("--order", type=int, default=4)
-ap.add_argument("--what", default="step", choices=["sweep", "step", "coarse"])
+ap.add_argument("--what", default="step", choices=["sweep", "step", "coarse", "capply", "prolong"])
 ap.add_argument("--reps", type=int, default=2)
 a = ap.parse_args()
 prob = hb.build_problem(hb.ProblemSpec(order=a.order, wavelengths=a.wavelengths, ppw=10))
@@ -27,6 +27,10 @@ for _ in range(a.reps):
         ops.csdd_smoother(u, f)
     elif a.what == "step":
         ops.two_grid_step(u, f)
+    elif a.what == "capply":
+        ops.coarse_apply(rc, uc)
+    elif a.what == "prolong":
+        ops.prolong_add(u, rc, 1.0)
     else:
         ops.coarse_solve(rc, uc)
 torch.cuda.synchronize()
