@@ -319,6 +319,16 @@ DDDevice upload_dd_impl(const DDSetup& dd, const HostProblem& hp, std::vector<vo
                     bytes += go.size() * sizeof(int);
                     HTG_CUDA(cudaMemcpy(ptr, go.data(), go.size() * sizeof(int), cudaMemcpyHostToDevice));
                     f.goff = static_cast<const int*>(ptr);
+                    // memory order of the gather: consecutive lanes copy consecutive 16-byte dofs
+                    std::vector<int> ord(go.size());
+                    for (size_t i = 0; i < ord.size(); ++i) ord[i] = int(i);
+                    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return go[a] < go[b]; });
+                    void* po = nullptr;
+                    HTG_CUDA(cudaMalloc(&po, ord.size() * sizeof(int)));
+                    allocs.push_back(po);
+                    bytes += ord.size() * sizeof(int);
+                    HTG_CUDA(cudaMemcpy(po, ord.data(), ord.size() * sizeof(int), cudaMemcpyHostToDevice));
+                    f.gord = static_cast<const int*>(po);
                 }
             }
             fdm.push_back(f);

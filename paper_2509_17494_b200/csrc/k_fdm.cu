@@ -600,7 +600,8 @@ __global__ void __launch_bounds__(kWThreads(P, NP), 1)
         const int seg_end = min(wk.y, c.first + c.nsub);
         const int nx = c.nx, ny = c.ny, nux = c.nux, nuy = c.nuy;
         int* urow = reinterpret_cast<int*>(D + nx * ny);
-        int* gofs = urow + nux * nuy;
+        int* gofs = urow + nux * nuy;  // gather: dof offsets in memory order ...
+        int* gpos = gofs + nx * ny;    // ... and the tile slot each one lands in
         __syncthreads();  // previous segment finished with the factors
         const double2 z = make_double2(0.0, 0.0);
         for (int i = tid; i < 2 * KP * LD; i += nthr) {
@@ -616,7 +617,11 @@ __global__ void __launch_bounds__(kWThreads(P, NP), 1)
             urow[i] = c.rowmap[dof_index(c.onx, c.ony, P, c.ux0 + ixu, c.uy0 + iyu)];
         }
         if (c.goff)
-            for (int i = tid; i < nx * ny; i += nthr) gofs[i] = c.goff[i];
+            for (int i = tid; i < nx * ny; i += nthr) {
+                const int e = c.gord[i], iy = e / nx;
+                gofs[i] = c.goff[e];
+                gpos[i] = iy * LD + (e - iy * nx);
+            }
         __syncthreads();
         const int nxy = nx * ny;
         const float inv_nx = 1.0f / nx;
@@ -625,10 +630,7 @@ __global__ void __launch_bounds__(kWThreads(P, NP), 1)
             const int ox = (so & 0xffff) * P, oy = (so >> 16) * P;
             if (c.goff) {
                 const double2* rb = r + dof_index(g.nx, g.ny, P, ox, oy);
-                for (int l = tl; l < nxy; l += NP * 32) {
-                    const int iy = fdiv(l, inv_nx), ix = l - iy * nx;
-                    cp_async16(&X[iy * LD + ix], rb + gofs[l]);
-                }
+                for (int l = tl; l < nxy; l += NP * 32) cp_async16(&X[gpos[l]], rb + gofs[l]);
             } else {
                 for (int l = tl; l < nxy; l += NP * 32) {
                     const int iy = fdiv(l, inv_nx), ix = l - iy * nx;
@@ -742,7 +744,7 @@ std::vector<int4> fdm_plan(std::vector<FdmClassDev>& cls, int p, int nsm, FdmLau
         const int KP = p == 2 ? 4 * FdmDims<2>::KS : 4 * FdmDims<4>::KS;
         int wfac = 0;
         for (auto& c : cls)
-            wfac = std::max(wfac, 2 * KP * LD + c.nx * c.ny + (c.nux * c.nuy + c.nx * c.ny + 3) / 4);
+            wfac = std::max(wfac, 2 * KP * LD + c.nx * c.ny + (c.nux * c.nuy + 2 * c.nx * c.ny + 3) / 4);
         wfac = (wfac + 7) / 8 * 8;
         const int per_warp = 2 * ext * LD;
         int nt = (kSmemMax / int(sizeof(double2)) - wfac) / per_warp;  // teams (buffer pairs)

@@ -93,6 +93,7 @@ struct FdmClassDev {
     const int* sub_o;   // Omega origin per subdomain
     const int* goff;    // gather offsets: tile element iy * nx + ix -> dof offset from the
                         // subdomain's first dof (identical for every member), or null
+    const int* gord;    // tile elements in ascending goff order (memory-order gather), or null
     int nsub;
     int first;          // offset of this class in the class-sorted subdomain list
 };

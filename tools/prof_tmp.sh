@@ -1,3 +1,2 @@
 python tools/run_once.py --what sweep --reps 1 > gpurun_out/p_plain.log 2>&1
-HTG_FDM_TEAM=2 ncu --set full --clock-control none --import-source on -k regex:k_dd_fdm_w -c 1 -o gpurun_out/prof_fdm_t2 -f python tools/run_once.py --what sweep --reps 1 > gpurun_out/p1.log 2>&1
-HTG_FDM_GROUPK=1 HTG_LIB=exp/dr0.so ncu --set full --clock-control none --import-source on -k regex:k_dd_fdm -c 1 -o gpurun_out/prof_fdm_g2 -f python tools/run_once.py --what sweep --reps 1 > gpurun_out/p2.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_dd_fdm_w -c 1 -o gpurun_out/prof_fdm_t2 -f python tools/run_once.py --what sweep --reps 1 > gpurun_out/p1.log 2>&1
