@@ -69,6 +69,7 @@ def lib():
         _lib.ref_dirichlet.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int]
         for name in ("ref_bench_csdd", "ref_bench_two_grid"):
             getattr(_lib, name).argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_double)]
+        _lib.ref_add_coarse_parts.argtypes = [C.c_void_p]
         _lib.ref_set_threads.argtypes = [C.c_int]
         _lib.ref_set_threads.restype = None
     return _lib
@@ -123,6 +124,13 @@ class RefSession:
         _check(L.ref_info(h, _p(info)))
         (self.ndof, self.coarse_ndof, self.nx, self.ny, self.n_subdomains, self.n_factors,
          self.nnz_A, self.nnz_Ac, self.nnz_IP) = (int(v) for v in info)
+
+    def add_coarse_parts(self):
+        """A_c, IP, IP^H of the OptimizedFD level on a CoarseKind::None session (no coarse factor)."""
+        _check(lib().ref_add_coarse_parts(self._h))
+        info = np.zeros(9, dtype=np.int64)
+        _check(lib().ref_info(self._h, _p(info)))
+        self.coarse_ndof, self.nnz_Ac, self.nnz_IP = int(info[1]), int(info[7]), int(info[8])
 
     def __del__(self):
         if getattr(self, "_h", None) and _lib is not None:

@@ -228,6 +228,28 @@ int ref_apply(void* h, int which, const double* x, double* y) {
     });
 }
 
+// The OptimizedFD coarse level of setup_two_grid (proj/core/src/twogrid.cpp:235-243),
+// built by the reference's own coarse_mesh_for / coarsen_* / qsfem::assemble /
+// build_prolongation on a session set up with CoarseKind::None, without the
+// coarse SparseLU factorization (hours at the full-size configs): A_c, IP and
+// IP^H are then available through ref_apply, the coarse solve is not.
+int ref_add_coarse_parts(void* h) {
+    return guard([&] {
+        Session* s = S(h);
+        if (!s->ops) throw std::invalid_argument("session has no two-grid operators");
+        TwoGridOperators& o = *s->ops;
+        const FeSpace& space = *s->pr.space;
+        const int m = space.order() / 2;
+        o.coarse_mesh = std::make_unique<StructuredMesh>(coarse_mesh_for(space));
+        o.coarse_space = std::make_unique<FeSpace>(FeSpace::build_any(*o.coarse_mesh, 1));
+        const CoefficientField ccoeffs = coarsen_coefficients(s->pr.coeffs, m);
+        const BoundaryTags ctags = coarsen_tags(*o.coarse_mesh, s->pr.tags, m);
+        o.Ac = qsfem::assemble(*o.coarse_space, ccoeffs, ctags);
+        o.IP = build_prolongation(space, *o.coarse_space, space.dirichlet_dofs(s->pr.tags),
+                                  o.coarse_space->dirichlet_dofs(ctags));
+    });
+}
+
 // r = f - A u (shifted: A_s), the expression of twogrid.cpp:116 / :94
 int ref_residual(void* h, int shifted, const double* f, const double* u, double* r) {
     return guard([&] {

@@ -1183,58 +1183,63 @@ void reduce_partials(const double* partial, int n, double* out, cudaStream_t st)
 // cell the dofs with jx, jy < m (vertex and degree <= m bubbles); rows of fine
 // Dirichlet dofs and columns of coarse Dirichlet dofs are zero
 // (proj/core/src/twogrid.cpp:150-187).
+// One thread per unit cell (x, y) on a 2-D grid: it loads the (m+1)^2 coarse
+// vertices of its cell once and updates the cell's m^2 nonzero rows, so the
+// m^2 loads of u are independent (in flight together).
 template <int P>
-__global__ void k_prolong(FineGeom g, double2* __restrict__ u, const double2* __restrict__ uc, double omega) {
+__global__ void __launch_bounds__(256, P <= 4 ? 4 : 1) k_prolong(FineGeom g, double2* __restrict__ u, const double2* __restrict__ uc,
+                                                 double omega) {
     constexpr int MM = P / 2;
-    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    const int q = int(t % (MM * MM));
-    const long long cell = t / (MM * MM);
-    const int x = int(cell % (g.nx + 1)), y = int(cell / (g.nx + 1));
-    if (y > g.ny) return;
-    const int jx = q % MM, jy = q / MM;
-    if ((x == g.nx && jx) || (y == g.ny && jy)) return;
-    const int gx = x * P + jx, gy = y * P + jy;
-    if (g.has_dirichlet && fine_dir<P>(g, gx, gy)) return;
-    const int cnx1 = g.nx * MM + 1;
-    double wx[MM + 1], wy[MM + 1];
-    int nwx, nwy;
-    if (jx == 0) {
-        wx[0] = 1.0;
-        nwx = 1;
-    } else {
-        for (int i = 0; i <= MM; ++i) wx[i] = c_E[P / 2 - 1][jx + 1][i];
-        nwx = MM + 1;
-    }
-    if (jy == 0) {
-        wy[0] = 1.0;
-        nwy = 1;
-    } else {
-        for (int i = 0; i <= MM; ++i) wy[i] = c_E[P / 2 - 1][jy + 1][i];
-        nwy = MM + 1;
-    }
-    double2 s = make_double2(0.0, 0.0);
-    for (int iy = 0; iy < nwy; ++iy) {
-        const int Y = y * MM + iy;
-        for (int ix = 0; ix < nwx; ++ix) {
-            const int X = x * MM + ix;
-            if (g.has_dirichlet && coarse_dir(g, MM, X, Y)) continue;
-            s = rfma(wx[ix] * wy[iy], uc[(size_t)Y * cnx1 + X], s);
+    const int x = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 8 + threadIdx.y;
+    if (x > g.nx || y > g.ny) return;
+    const int CX = g.nx * MM, CY = g.ny * MM;
+    const size_t cnx1 = size_t(CX) + 1;
+    double2 c[MM + 1][MM + 1];
+#pragma unroll
+    for (int iy = 0; iy <= MM; ++iy)
+#pragma unroll
+        for (int ix = 0; ix <= MM; ++ix) {
+            const int X = x * MM + ix, Y = y * MM + iy;
+            const bool in = X <= CX && Y <= CY && !(g.has_dirichlet && coarse_dir(g, MM, X, Y));
+            c[iy][ix] = in ? uc[size_t(Y) * cnx1 + X] : make_double2(0.0, 0.0);
         }
+    long long dst[MM * MM];
+    double2 cur[MM * MM];
+#pragma unroll
+    for (int q = 0; q < MM * MM; ++q) {
+        const int jx = q % MM, jy = q / MM;
+        const int gx = x * P + jx, gy = y * P + jy;
+        const bool ok = !((x == g.nx && jx) || (y == g.ny && jy)) && !(g.has_dirichlet && fine_dir<P>(g, gx, gy));
+        dst[q] = ok ? dofp<P>(g.nx, g.ny, gx, gy) : -1;
+        cur[q] = ok ? u[dst[q]] : make_double2(0.0, 0.0);
     }
-    const long long d = dofp<P>(g.nx, g.ny, gx, gy);
-    u[d] = rfma(omega, s, u[d]);
+#pragma unroll
+    for (int q = 0; q < MM * MM; ++q) {
+        if (dst[q] < 0) continue;
+        const int jx = q % MM, jy = q / MM;
+        double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int iy = 0; iy <= MM; ++iy) {
+            const double wy = jy == 0 ? (iy == 0 ? 1.0 : 0.0) : c_E[P / 2 - 1][jy + 1][iy];
+            if (jy == 0 && iy > 0) continue;
+#pragma unroll
+            for (int ix = 0; ix <= MM; ++ix) {
+                if (jx == 0 && ix > 0) continue;
+                const double wx = jx == 0 ? 1.0 : c_E[P / 2 - 1][jx + 1][ix];
+                s = rfma(wx * wy, c[iy][ix], s);
+            }
+        }
+        u[dst[q]] = rfma(omega, s, cur[q]);
+    }
 }
 
 void prolong_add_launch(const FineGeom& g, double2* u, const double2* uc, double omega, cudaStream_t st) {
-    const int MM = g.p / 2;
-    const long long n = (long long)(g.nx + 1) * (g.ny + 1) * MM * MM;
-    const int bs = 256;
-    const unsigned nb = unsigned((n + bs - 1) / bs);
+    const dim3 grid(unsigned((g.nx + 1 + 31) / 32), unsigned((g.ny + 1 + 7) / 8)), blk(32, 8);
     switch (g.p) {
-        case 2: k_prolong<2><<<nb, bs, 0, st>>>(g, u, uc, omega); break;
-        case 4: k_prolong<4><<<nb, bs, 0, st>>>(g, u, uc, omega); break;
-        case 6: k_prolong<6><<<nb, bs, 0, st>>>(g, u, uc, omega); break;
-        default: k_prolong<8><<<nb, bs, 0, st>>>(g, u, uc, omega); break;
+        case 2: k_prolong<2><<<grid, blk, 0, st>>>(g, u, uc, omega); break;
+        case 4: k_prolong<4><<<grid, blk, 0, st>>>(g, u, uc, omega); break;
+        case 6: k_prolong<6><<<grid, blk, 0, st>>>(g, u, uc, omega); break;
+        default: k_prolong<8><<<grid, blk, 0, st>>>(g, u, uc, omega); break;
     }
     HTG_CUDA(cudaGetLastError());
     count_launch();
@@ -1244,56 +1249,84 @@ void prolong_add_launch(const FineGeom& g, double2* u, const double2* uc, double
 // y = A_c x: per coarse cell the QSFEM weights q_{|dx|+|dy|} minus the i eps
 // p=1 mass, minus the Robin p=1 edge mass, Dirichlet rows/cols identity
 // (proj/core/src/qsfem.cpp:118-149).
-__global__ void k_coarse_apply(FineGeom g, int m, const double4* __restrict__ qtab, const double2* __restrict__ x,
-                               double2* __restrict__ y) {
+// One thread per coarse vertex on a 2-D grid (x fastest, coalesced loads of the
+// 3 x 3 neighbourhood through L1, one coalesced store); the mass weights are
+// products with constant reciprocals (no division) and the class lookup is
+// skipped for uniform coefficients.
+__global__ void __launch_bounds__(256) k_coarse_apply(FineGeom g, int m, const double4* __restrict__ qtab,
+                                                      const double2* __restrict__ x, double2* __restrict__ y) {
     const int CX = g.nx * m, CY = g.ny * m;
-    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (t >= (long long)(CX + 1) * (CY + 1)) return;
-    const int X = int(t % (CX + 1)), Y = int(t / (CX + 1));
+    const int X = blockIdx.x * 32 + threadIdx.x, Y = blockIdx.y * 8 + threadIdx.y;
+    if (X > CX || Y > CY) return;
+    const size_t row = size_t(CX) + 1, t = size_t(Y) * row + X;
     const bool dir = g.has_dirichlet;
     if (dir && coarse_dir(g, m, X, Y)) {
         y[t] = x[t];
         return;
     }
-    auto xv = [&](int a, int b) -> double2 {
-        if (dir && coarse_dir(g, m, a, b)) return make_double2(0.0, 0.0);
-        return x[(size_t)b * (CX + 1) + a];
-    };
+    // 3 x 3 neighbourhood (zero outside the lattice and on Dirichlet vertices)
+    double2 v[3][3];
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const int xa = X + a - 1, yb = Y + b - 1;
+            const bool in = xa >= 0 && xa <= CX && yb >= 0 && yb <= CY && !(dir && coarse_dir(g, m, xa, yb));
+            v[b][a] = in ? x[size_t(yb) * row + xa] : make_double2(0.0, 0.0);
+        }
+    // mass of the p = 1 element between two vertices at Manhattan distance d: (4, 2, 1) / 36
+    constexpr double kM0 = 4.0 / 36.0, kM1 = 2.0 / 36.0, kM2 = 1.0 / 36.0;
+    const bool uni = g.cls == nullptr;
+    double4 q = qtab[0];
     double2 s = make_double2(0.0, 0.0);
-    for (int cy = Y - 1; cy <= Y; ++cy) {
-        if (cy < 0 || cy >= CY) continue;
-        for (int cx = X - 1; cx <= X; ++cx) {
-            if (cx < 0 || cx >= CX) continue;
-            const double4 q = qtab[g.cls ? g.cls[(size_t)(cy / m) * g.nx + cx / m] : 0];
-            for (int wy = cy; wy <= cy + 1; ++wy)
-                for (int wx = cx; wx <= cx + 1; ++wx) {
-                    const int dx = abs(wx - X), dy = abs(wy - Y);
-                    const double qw = (dx + dy == 0) ? q.x : (dx + dy == 1 ? q.y : q.z);
-                    const double mass = double((dx == 0 ? 2 : 1) * (dy == 0 ? 2 : 1)) / 36.0;
-                    const double2 v = xv(wx, wy);
-                    // (qw - i eps hc^2 mass) v
-                    const double em = q.w * mass;
-                    s.x += qw * v.x + em * v.y;
-                    s.y += qw * v.y - em * v.x;
+    if (uni && X > 0 && X < CX && Y > 0 && Y < CY) {
+        // interior vertex of a uniform medium: the 9-point stencil N [P2 P1 P2; P1 P0 P1; P2 P1 P2]
+        // summed over its 4 cells: 4 (q0 - i e0) centre, 2 (q1 - i e1) edge, (q2 - i e2) corner
+        const double2 ce = cadd(cadd(v[0][1], v[2][1]), cadd(v[1][0], v[1][2]));
+        const double2 co = cadd(cadd(v[0][0], v[0][2]), cadd(v[2][0], v[2][2]));
+        const double2 w0 = make_double2(4.0 * q.x, -4.0 * q.w * kM0), w1 = make_double2(2.0 * q.y, -2.0 * q.w * kM1),
+                      w2 = make_double2(q.z, -q.w * kM2);
+        y[t] = cadd(cadd(cmul(w0, v[1][1]), cmul(w1, ce)), cmul(w2, co));
+        return;
+    }
+#pragma unroll
+    for (int cb = 0; cb < 2; ++cb)
+#pragma unroll
+        for (int ca = 0; ca < 2; ++ca) {
+            const int cx = X - 1 + ca, cy = Y - 1 + cb;  // cell (cx, cy) has vertices cx..cx+1, cy..cy+1
+            if (cx < 0 || cx >= CX || cy < 0 || cy >= CY) continue;
+            if (!uni) q = qtab[g.cls[(size_t)(cy / m) * g.nx + cx / m]];
+            const double w[3] = {q.x, q.y, q.z}, e[3] = {q.w * kM0, q.w * kM1, q.w * kM2};
+#pragma unroll
+            for (int wb = 0; wb < 2; ++wb)
+#pragma unroll
+                for (int wa = 0; wa < 2; ++wa) {
+                    // vertex (cx + wa, cy + wb) = neighbourhood slot (ca + wa, cb + wb)
+                    const int d = (ca + wa == 1 ? 0 : 1) + (cb + wb == 1 ? 0 : 1);
+                    const double2 u = v[cb + wb][ca + wa];
+                    // (w_d - i e_d) u
+                    s.x = fma(w[d], u.x, fma(e[d], u.y, s.x));
+                    s.y = fma(w[d], u.y, fma(-e[d], u.x, s.y));
                 }
         }
-    }
-    // absorbing coarse edges (k hc = (k h) / m of the parent fine edge)
-    auto edge = [&](double khc, int ax, int ay, int bx, int by) {
-        // edge with endpoints (ax, ay) == (X, Y) and (bx, by)
-        const double2 vs = xv(ax, ay), vo = xv(bx, by);
-        const double2 c = make_double2(vs.x / 3.0 + vo.x / 6.0, vs.y / 3.0 + vo.y / 6.0);
-        s = cadd(s, mik(khc, c));
-    };
-    if (Y == 0 || Y == CY) {
-        const double* kh = Y == 0 ? g.kh_b : g.kh_t;
-        if (X > 0) edge(kh[(X - 1) / m] / m, X, Y, X - 1, Y);
-        if (X < CX) edge(kh[X / m] / m, X, Y, X + 1, Y);
-    }
-    if (X == 0 || X == CX) {
-        const double* kh = X == 0 ? g.kh_l : g.kh_r;
-        if (Y > 0) edge(kh[(Y - 1) / m] / m, X, Y, X, Y - 1);
-        if (Y < CY) edge(kh[Y / m] / m, X, Y, X, Y + 1);
+    // absorbing coarse edges (k hc = (k h) / m of the parent fine edge): -i k hc (u_s / 3 + u_o / 6)
+    if (Y == 0 || Y == CY || X == 0 || X == CX) {
+        constexpr double k3 = 1.0 / 3.0, k6 = 1.0 / 6.0;
+        const double rm = 1.0 / m;
+        auto edge = [&](double khc, double2 vo) {
+            const double2 vs = v[1][1];
+            s = cadd(s, mik(khc, make_double2(vs.x * k3 + vo.x * k6, vs.y * k3 + vo.y * k6)));
+        };
+        if (Y == 0 || Y == CY) {
+            const double* kh = Y == 0 ? g.kh_b : g.kh_t;
+            if (X > 0) edge(kh[(X - 1) / m] * rm, v[1][0]);
+            if (X < CX) edge(kh[X / m] * rm, v[1][2]);
+        }
+        if (X == 0 || X == CX) {
+            const double* kh = X == 0 ? g.kh_l : g.kh_r;
+            if (Y > 0) edge(kh[(Y - 1) / m] * rm, v[0][1]);
+            if (Y < CY) edge(kh[Y / m] * rm, v[2][1]);
+        }
     }
     y[t] = s;
 }
@@ -1302,8 +1335,8 @@ void coarse_apply_launch(const FineGeom& g, const double4* qtab, double hc, cons
                          cudaStream_t st) {
     (void)hc;
     const int m = g.p / 2;
-    const long long n = (long long)(g.nx * m + 1) * (g.ny * m + 1);
-    k_coarse_apply<<<unsigned((n + 255) / 256), 256, 0, st>>>(g, m, qtab, x, y);
+    const dim3 grid(unsigned((g.nx * m + 1 + 31) / 32), unsigned((g.ny * m + 1 + 7) / 8));
+    k_coarse_apply<<<grid, dim3(32, 8), 0, st>>>(g, m, qtab, x, y);
     HTG_CUDA(cudaGetLastError());
     count_launch();
 }
