@@ -91,8 +91,9 @@ int htg_destroy(htg_handle* h);
  * flops 8 |U_i| |Omega_i| summed, [12] subdomains solved by fast
  * diagonalisation, [13] CUDA graphs cached by the handle (bounded LRU),
  * [14] sum of |U_i| (values staged per sweep), [15] sum of |Omega_i| (values
- * gathered per sweep), [16] algorithmic bytes one coarse solve reads.
- * out must hold 17 entries. */
+ * gathered per sweep), [16] algorithmic bytes one coarse solve reads,
+ * [17] subdomains with their own device-factored solver (no shared factor),
+ * [18] bytes of those factors. out must hold 19 entries. */
 int htg_info(const htg_handle* h, long long* out);
 int htg_set_stream(htg_handle* h, void* stream);
 

@@ -30,7 +30,8 @@ namespace htg {
 long long launch_count();
 void reset_launch_count();
 DDDevice upload_dd_impl(const DDSetup& dd, const HostProblem& hp, std::vector<void*>& allocs, size_t& bytes,
-                        cudaStream_t st, double2*& ystage, std::vector<FdmClassDev>& fdm);
+                        cudaStream_t st, double2*& ystage, std::vector<FdmClassDev>& fdm,
+                        std::vector<BandSubdomain>& band);
 }  // namespace htg
 
 using namespace htg;
@@ -111,6 +112,8 @@ struct htg_handle {
     DDDevice dd{};
     std::vector<FdmClassDev> fdm;  // separable classes (fast diagonalisation)
     FdmLaunch fdm_launch{};
+    BandLaunch band{};            // subdomains without a shared factor (device-factored)
+    long long band_subs = 0;
     double fdm_err = 0.0;
     int nclasses = 0;
     double dd_flops = 0.0;        // algorithmic flops of one sweep's subdomain solves (path used)
@@ -245,7 +248,17 @@ void build_handle(htg_handle* H, const htg_problem& prob, const htg_config& cfg)
                 H->dd_flops += 8.0 * c.nu * c.nloc;
             }
         }
-        H->dd = upload_dd_impl(dd, hp, M.ptrs, M.bytes, st, H->ystage, H->fdm);
+        std::vector<BandSubdomain> bandsubs;
+        H->dd = upload_dd_impl(dd, hp, M.ptrs, M.bytes, st, H->ystage, H->fdm, bandsubs);
+        if (!bandsubs.empty()) {
+            clk.mark("subdomain upload");
+            std::vector<double> khtab(hp.cls_k.size());
+            for (size_t i = 0; i < khtab.size(); ++i) khtab[i] = hp.cls_k[i] * hp.h;
+            if (khtab.empty()) khtab.push_back(hp.k.empty() ? 0.0 : hp.k[0] * hp.h);
+            H->band = band_setup(H->g, bandsubs, H->basis, khtab, M.ptrs, M.bytes, st);
+            H->band_subs = H->band.nsub;
+            clk.mark("band subdomain factors (device)");
+        }
         for (const DDClass& c : dd.classes)
             if (c.fdm) H->fdm_err = std::max(H->fdm_err, c.fdm_err);
         if (!H->fdm.empty()) {
@@ -388,6 +401,7 @@ void coarse_apply(htg_handle* H, const double2* x, double2* y) {
 void subdomain_solves(htg_handle* H, const double2* gvec) {
     dd_gemm_launch(H->g, H->dd, gvec, H->ystage, H->st);
     dd_fdm_launch(H->g, H->fdm_launch, gvec, H->ystage, H->dd.nu_max, H->st);
+    band_solve_launch(H->g, H->band, gvec, H->ystage, H->dd.nu_max, H->st);
 }
 
 // out = dd_step(u, f): g = f - A_s u (skipped when u is null, i.e. zero)
@@ -656,6 +670,8 @@ int htg_info(const htg_handle* h, long long* out) {
         out[14] = h->sum_u;
         out[15] = h->sum_omega;
         out[16] = h->coarse ? (long long)h->coarse->solve_read_bytes() : 0;
+        out[17] = h->band_subs;
+        out[18] = h->band.pool_elems * (long long)sizeof(double2);
     });
 }
 

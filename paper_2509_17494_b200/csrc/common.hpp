@@ -47,7 +47,7 @@ struct FineGeom {
     int nx, ny, p;
     long long ndof;
     // per-cell coefficient class (nullptr: one class for every cell)
-    const uint16_t* cls;
+    const uint32_t* cls;
     // complex mass weight m = (k^2 (1 + i alpha) + i eps) h^2 per class, for
     // alpha = 0 (mtab0) and alpha = alpha_s (mtabS)
     const double2* mtab0;

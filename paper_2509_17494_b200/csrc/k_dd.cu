@@ -221,7 +221,8 @@ void dd_combine_launch(const FineGeom& g, const DDDevice& d, const double2* ysta
 // Host: lay the classes out for the kernels (padded B_c, local gather tables,
 // U-row maps, tile list) and upload.
 DDDevice upload_dd_impl(const DDSetup& dd, const HostProblem& hp, std::vector<void*>& allocs, size_t& bytes,
-                        cudaStream_t st, double2*& ystage, std::vector<FdmClassDev>& fdm) {
+                        cudaStream_t st, double2*& ystage, std::vector<FdmClassDev>& fdm,
+                        std::vector<BandSubdomain>& band) {
     DDDevice d;
     const int nc = int(dd.classes.size());
     d.nclass = nc;
@@ -253,8 +254,8 @@ DDDevice upload_dd_impl(const DDSetup& dd, const HostProblem& hp, std::vector<vo
         in[6] = int(locg.size());
         in[7] = int(subs[ci].size());
         const size_t b0 = Bm.size();
-        Bm.resize(b0 + size_t(rpad) * kpad, make_double2(0.0, 0.0));
-        for (int rI = 0; rI < c.nu; ++rI)
+        if (!c.band) Bm.resize(b0 + size_t(rpad) * kpad, make_double2(0.0, 0.0));
+        for (int rI = 0; rI < (c.band ? 0 : c.nu); ++rI)
             for (int l = 0; l < c.nloc; ++l) {
                 const cplx v = c.B[size_t(rI) * c.nloc + l];
                 Bm[b0 + size_t(rI) * kpad + l] = make_double2(v.real(), v.imag());
@@ -268,6 +269,10 @@ DDDevice upload_dd_impl(const DDSetup& dd, const HostProblem& hp, std::vector<vo
         rowmap.insert(rowmap.end(), rm.begin(), rm.end());
         const int off = int(class_subs.size());
         class_subs.insert(class_subs.end(), subs[ci].begin(), subs[ci].end());
+        if (c.band) {  // per-member device factors (k_band.cu)
+            for (int sI : subs[ci]) band.push_back({sI, dd.sub_ox[sI], dd.sub_oy[sI], c.onx, c.ony, &c.umem});
+            continue;
+        }
         if (c.fdm && fdm_supported(p, c.fdm_nx, c.fdm_ny)) {
             FdmClassDev f{};
             f.nx = c.fdm_nx;

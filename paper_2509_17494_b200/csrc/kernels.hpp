@@ -112,6 +112,40 @@ void dd_fdm_launch(const FineGeom& g, const FdmLaunch& L, const double2* r, doub
 std::vector<int4> fdm_plan(std::vector<FdmClassDev>& cls, int p, int nsm, FdmLaunch& L);
 // p and 1-D extents of Omega the FDM kernel takes (others use the dense path)
 bool fdm_supported(int p, int nx, int ny);
+// subdomains without a shared factor: device-factored per-subdomain solves (k_band.cu)
+struct BandGeomDev {
+    int onx, ony, NXn, NYn;  // Omega cells, lattice nodes per direction
+    int ns, bw;              // skeleton dofs, half bandwidth of the skeleton matrix
+    int ncell, cellstride;   // cells; factor elements per cell (A_II^-1 and W)
+    int nu, nucell;          // U outputs; cells with U bubbles
+    const int* node_code;    // lattice node -> skeleton index, -1 for bubbles
+    const int* skel_node;    // skeleton index -> lattice node
+    const int* cell_bnd;     // per cell, boundary slot -> skeleton index
+    const int* uout;         // (lattice node, U row) per U member
+    const int* ucells;       // cells with U bubbles
+};
+struct BandLaunch {
+    const BandGeomDev* geoms;
+    const int4* subs;        // per band subdomain: subdomain id, geometry, Omega origin (ox | oy << 16)
+    const long long* foff;   // factor offset (double2) per band subdomain
+    double2* pool;           // factors
+    const double* khtab;     // k h per coefficient class
+    const double* basis;     // 1-D M then S, (p+1)^2 each
+    long long pool_elems;
+    int nsub;
+    int warps;               // sweep: warps (subdomains in flight) per CTA
+    int warp_elems;          // sweep: shared-memory vector elements per warp
+    size_t solve_smem;
+};
+struct BandSubdomain {
+    int sid, ox, oy, onx, ony;
+    const std::vector<int>* umem;  // U members (local reference dof order = U-row order)
+};
+struct Basis1D;
+BandLaunch band_setup(const FineGeom& g, const std::vector<BandSubdomain>& subs, const Basis1D& basis,
+                      const std::vector<double>& khtab, std::vector<void*>& allocs, size_t& bytes, cudaStream_t st);
+void band_solve_launch(const FineGeom& g, const BandLaunch& L, const double2* r, double2* ystage, int nu_max,
+                       cudaStream_t st);
 // out = u + sum_i y_i / L in subdomain order (u may be null -> 0); out may alias u
 void dd_combine_launch(const FineGeom& g, const DDDevice& d, const double2* ystage, const double2* u, double2* out,
                        cudaStream_t st);

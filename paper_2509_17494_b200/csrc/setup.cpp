@@ -197,12 +197,11 @@ HostProblem make_problem(const htg_problem& pr) {
         auto key = std::make_pair(hp.k[c], hp.eps[c]);
         auto it = ids.find(key);
         if (it == ids.end()) {
-            if (ids.size() >= 65535) throw InvalidArgument("more than 65535 distinct (k, eps) cell values");
             it = ids.emplace(key, int(ids.size())).first;
             hp.cls_k.push_back(key.first);
             hp.cls_eps.push_back(key.second);
         }
-        hp.cls[c] = uint16_t(it->second);
+        hp.cls[c] = uint32_t(it->second);
     }
     hp.uniform = ids.size() == 1;
     return hp;
@@ -416,15 +415,40 @@ DDSetup build_dd(const HostProblem& hp, const Basis1D& b, double alpha_s, int l_
             dd.sub_ox[s] = ox0;
             dd.sub_oy[s] = oy0;
         }
-    // restricted inverses, one per class (threads over classes)
+    // classes without a shared factor: few members (HTG_BAND_MAX, default 8) and
+    // coefficients that vary over Omega (not separable); HTG_BAND=0 keeps every
+    // class on the dense path
     const int nc = int(dd.classes.size());
+    {
+        const char* be = std::getenv("HTG_BAND");
+        const char* bm = std::getenv("HTG_BAND_MAX");
+        const int band_max = bm ? std::atoi(bm) : 8;
+        std::vector<int> members(nc, 0);
+        for (int c : dd.sub_class) ++members[c];
+        if (!(be && be[0] == '0'))
+            for (int ci = 0; ci < nc; ++ci) {
+                const DDClass& c = dd.classes[ci];
+                const int ox = first[ci].ox, oy = first[ci].oy;
+                bool varies = false;
+                for (int y = oy; y < oy + c.ony && !varies; ++y)
+                    for (int x = ox; x < ox + c.onx; ++x)
+                        if (hp.kc(x, y) != hp.kc(ox, oy) || hp.ec(x, y) != hp.ec(ox, oy)) {
+                            varies = true;
+                            break;
+                        }
+                dd.classes[ci].band = varies && members[ci] <= band_max;
+            }
+    }
+    // restricted inverses, one per class (threads over classes)
     std::vector<std::exception_ptr> errs(nc);
     auto work = [&](int ci) {
         try {
             DDClass& c = dd.classes[ci];
             std::vector<cplx> A;
-            assemble_omega(hp, b, alpha_s, first[ci].ox, first[ci].oy, c.onx, c.ony, A, c.nloc);
-            const int n = c.nloc, p = hp.p;
+            const int p = hp.p;
+            if (c.band) c.nloc = int(dof_index(c.onx, c.ony, p, c.onx * p, c.ony * p)) + 1;
+            else assemble_omega(hp, b, alpha_s, first[ci].ox, first[ci].oy, c.onx, c.ony, A, c.nloc);
+            const int n = c.nloc;
             // U members: local dofs whose support touches a U cell (twogrid.cpp:46-62)
             const int NG_x = c.onx * p + 1, NG_y = c.ony * p + 1;
             std::vector<int> isU(n, 0);
@@ -441,6 +465,7 @@ DDSetup build_dd(const HostProblem& hp, const Basis1D& b, double alpha_s, int l_
             for (int l = 0; l < n; ++l)
                 if (isU[l]) c.umem.push_back(l);
             c.nu = int(c.umem.size());
+            if (c.band) return;  // factored per member on the device
             // B = A^-1 [U, :] = (A^-T [:, U])^T: solve A^T X = E_U
             std::vector<cplx> At(size_t(n) * n);
             for (int i = 0; i < n; ++i)

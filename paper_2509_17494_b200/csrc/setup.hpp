@@ -37,7 +37,7 @@ struct HostProblem {
     std::vector<double> khb, kht, khl, khr;  // Robin k*h (0 unless absorbing)
     bool has_dirichlet = false;
     // unique (k, eps) coefficient classes
-    std::vector<uint16_t> cls;  // per cell
+    std::vector<uint32_t> cls;  // per cell
     std::vector<double> cls_k, cls_eps;
     bool uniform = true;
     long long ndof() const { return (long long)(nx * p + 1) * (ny * p + 1); }
@@ -67,6 +67,9 @@ struct DDClass {
     std::vector<cplx> Vx, Vy;      // (nx x nx), (ny x ny) row-major, columns are eigenvectors
     std::vector<cplx> Dinv;        // nx x ny
     double fdm_err = 0.0;          // max |B_fdm - B| / max |B| over the class
+    // no shared factor (few members, coefficients varying over Omega): every
+    // member is factored on the device (k_band.cu); B stays empty
+    bool band = false;
 };
 // Build the FDM factors of a class whose first subdomain's Omega starts at
 // cell (ox, oy); false if the class is not separable or fails validation.
