@@ -214,9 +214,13 @@ __global__ void __launch_bounds__(256) k_band_factor(FineGeom g, BandLaunch L) {
             }
             __syncthreads();
             // store A_II^-1 and W; Schur complement A_BB - A_BI W into the band (lower triangle)
+            // cell block [j][o], o < NI: (A_II^-1)[o][j] (symmetric), o >= NI: W[j][o - NI]; for a
+            // fixed j the lanes of the sweep read consecutive entries (coalesced)
             double2* Fc = F + (size_t)cell * G.cellstride;
-            for (int e = tid; e < NI * NI; e += nt) Fc[e] = Ai[e];
-            for (int e = tid; e < NI * NB; e += nt) Fc[NI * NI + e] = Wm[e];
+            for (int e = tid; e < NI * (NI + NB); e += nt) {
+                const int j = e / (NI + NB), o = e % (NI + NB);
+                Fc[e] = o < NI ? Ai[o * NI + j] : Wm[j * NB + (o - NI)];
+            }
             const int* cb = G.cell_bnd + (size_t)cell * NB;
             for (int e = tid; e < NB * NB; e += nt) {
                 const int a = e / NB, b = e % NB;
@@ -257,24 +261,67 @@ __global__ void __launch_bounds__(256) k_band_factor(FineGeom g, BandLaunch L) {
 }
 
 // ------------------------------------------------------------------ sweep
-template <int P>
-__global__ void __launch_bounds__(512) k_band_solve(FineGeom g, BandLaunch L, const double2* __restrict__ r,
+// One warp per subdomain. The factor stream is what bounds it (375 KB per
+// subdomain at p = 4, the band read twice): every load is issued ahead of its
+// use -- the next cell's condensation coefficients under the current cell, the
+// band columns D = 4 columns ahead of the substitution (registers, NV entries
+// per lane with bw <= 32 NV) -- so a warp keeps several DRAM requests in flight
+// instead of one latency per column.
+template <int NV>
+__device__ __forceinline__ void band_col(double2 (&v)[NV], const double2* band, int col, int ns, int LDB, int bw,
+                                         int lane) {
+#pragma unroll
+    for (int t = 0; t < NV; ++t) {
+        const int i = 1 + lane + 32 * t;
+        v[t] = (col < ns && i <= bw) ? band[(size_t)col * LDB + i] : make_double2(0.0, 0.0);
+    }
+}
+
+#ifndef HTG_BAND_D
+#define HTG_BAND_D 12
+#endif
+#ifndef HTG_BAND_THREADS
+#define HTG_BAND_THREADS 384
+#endif
+constexpr int kBandD = HTG_BAND_D, kBandThreads = HTG_BAND_THREADS;
+
+template <int P, int NV>
+__global__ void __launch_bounds__(kBandThreads) k_band_solve(FineGeom g, BandLaunch L, const double2* __restrict__ r,
                                                     double2* __restrict__ ystage, int nu_max) {
-    constexpr int NE1 = P + 1, NB = 4 * P, NI = (P - 1) * (P - 1);
+    constexpr int NB = 4 * P, NI = (P - 1) * (P - 1), NO = NI + NB, NR = (NO + 31) / 32;
+    constexpr int D = NV <= 2 ? kBandD : 4;  // band columns in flight per lane
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     double2* vec = reinterpret_cast<double2*>(smem_raw) + (size_t)warp * L.warp_elems;
+    auto bub = [](int base, int NXn, int j) { return base + (1 + j / (P - 1)) * NXn + 1 + j % (P - 1); };
     for (int bs = blockIdx.x * nw + warp; bs < L.nsub; bs += gridDim.x * nw) {
         const int4 sd = L.subs[bs];
         const BandGeomDev G = L.geoms[sd.y];
         const int ox = sd.z & 0xffff, oy = sd.z >> 16;
         const double2* F = L.pool + L.foff[bs];
         const double2* band = F + (size_t)G.ncell * G.cellstride;
-        const int ns = G.ns, bw = G.bw, LDB = bw + 1, nn = G.NXn * G.NYn;
+        const int ns = G.ns, bw = G.bw, LDB = bw + 1, nn = G.NXn * G.NYn, NXn = G.NXn;
         double2* xs = vec + nn;  // skeleton vector
+        // condensation coefficients of the next cell in registers (p <= 4: 9 per
+        // lane at p = 4); larger cells read them in the loop
+        constexpr bool PRE = NR * NI <= 16;
+        double2 cf[PRE ? NR : 1][PRE ? NI : 1];
+        auto load_cell = [&](int cell) {
+            if constexpr (PRE) {
+                const double2* Fc = F + (size_t)cell * G.cellstride;
+#pragma unroll
+                for (int t = 0; t < NR; ++t)
+#pragma unroll
+                    for (int j = 0; j < NI; ++j) {
+                        const int o = lane + 32 * t;
+                        cf[t][j] = o < NO ? Fc[j * NO + o] : make_double2(0.0, 0.0);
+                    }
+            }
+        };
+        load_cell(0);
         // gather g = r on Omega (lattice node order)
         for (int n = lane; n < nn; n += 32) {
-            const int gx = n % G.NXn, gy = n / G.NXn;
+            const int gx = n % NXn, gy = n / NXn;
             vec[n] = r[dof_index(g.nx, g.ny, P, ox * P + gx, oy * P + gy)];
         }
         __syncwarp();
@@ -283,77 +330,96 @@ __global__ void __launch_bounds__(512) k_band_solve(FineGeom g, BandLaunch L, co
         // condensation: y_I = A_II^-1 g_I (into the bubble nodes), g_B -= W^T g_I
         for (int cell = 0; cell < G.ncell; ++cell) {
             const int cx = cell % G.onx, cy = cell / G.onx;
-            const int base = cy * P * G.NXn + cx * P;
-            const double2* Fc = F + (size_t)cell * G.cellstride;
+            const int base = cy * P * NXn + cx * P;
             const int* cb = G.cell_bnd + (size_t)cell * NB;
-            double2 out[(NI + NB + 31) / 32];
-            int slot[(NI + NB + 31) / 32];
+            const double2* Fc = F + (size_t)cell * G.cellstride;
+            double2 out[NR];
 #pragma unroll
-            for (int t = 0; t < (NI + NB + 31) / 32; ++t) {
+            for (int t = 0; t < NR; ++t) {
                 const int o = lane + 32 * t;
                 double2 s = make_double2(0.0, 0.0);
-                slot[t] = -1;
-                if (o < NI) {
-                    for (int j = 0; j < NI; ++j) {
-                        const int nj = base + (1 + j / (P - 1)) * G.NXn + 1 + j % (P - 1);
-                        cfma(s, Fc[o * NI + j], vec[nj]);
-                    }
-                    slot[t] = o;
-                } else if (o < NI + NB) {
-                    const int k = o - NI;
-                    s = xs[cb[k]];
-                    for (int j = 0; j < NI; ++j) {
-                        const int nj = base + (1 + j / (P - 1)) * G.NXn + 1 + j % (P - 1);
-                        cfms(s, Fc[NI * NI + j * NB + k], vec[nj]);
-                    }
-                    slot[t] = o;
+                if (o >= NI && o < NO) s = xs[cb[o - NI]];
+#pragma unroll 7
+                for (int j = 0; j < NI; ++j) {
+                    const double2 gj = vec[bub(base, NXn, j)];
+                    double2 c;
+                    if constexpr (PRE) c = cf[PRE ? t : 0][PRE ? j : 0];
+                    else c = o < NO ? Fc[j * NO + o] : make_double2(0.0, 0.0);
+                    if (o < NI) cfma(s, c, gj);
+                    else cfms(s, c, gj);
                 }
                 out[t] = s;
             }
+            if (cell + 1 < G.ncell) load_cell(cell + 1);
             __syncwarp();
 #pragma unroll
-            for (int t = 0; t < (NI + NB + 31) / 32; ++t) {
-                const int o = slot[t];
-                if (o < 0) continue;
-                if (o < NI) vec[base + (1 + o / (P - 1)) * G.NXn + 1 + o % (P - 1)] = out[t];
-                else xs[cb[o - NI]] = out[t];
+            for (int t = 0; t < NR; ++t) {
+                const int o = lane + 32 * t;
+                if (o < NI) vec[bub(base, NXn, o)] = out[t];
+                else if (o < NO) xs[cb[o - NI]] = out[t];
             }
             __syncwarp();
         }
-        // skeleton: L z = g (unit lower, by columns), z /= d, L^T x = z (dots)
-        for (int j = 0; j < ns; ++j) {
-            const double2 yj = xs[j];
-            const double2* cj = band + (size_t)j * LDB;
-            for (int i = 1 + lane; i <= bw && j + i < ns; i += 32) cfms(xs[j + i], cj[i], yj);
-            __syncwarp();
+        // skeleton: L z = g (unit lower, by columns), z /= d, L^T x = z (dots); band
+        // columns D ahead in registers
+        double2 bv[D][NV];
+#pragma unroll
+        for (int t = 0; t < D; ++t) band_col<NV>(bv[t], band, t, ns, LDB, bw, lane);
+        for (int j0 = 0; j0 < ns; j0 += D) {
+#pragma unroll
+            for (int t = 0; t < D; ++t) {
+                const int j = j0 + t;
+                if (j < ns) {
+                    const double2 yj = xs[j];
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) {
+                        const int i = 1 + lane + 32 * q;
+                        if (i <= bw && j + i < ns) cfms(xs[j + i], bv[t][q], yj);
+                    }
+                }
+                band_col<NV>(bv[t], band, j + D, ns, LDB, bw, lane);
+                __syncwarp();
+            }
         }
         for (int j = lane; j < ns; j += 32) xs[j] = cmulb(xs[j], band[(size_t)j * LDB]);
         __syncwarp();
-        for (int j = ns - 1; j >= 0; --j) {
-            const double2* cj = band + (size_t)j * LDB;
-            double2 s = make_double2(0.0, 0.0);
-            for (int i = 1 + lane; i <= bw && j + i < ns; i += 32) cfma(s, cj[i], xs[j + i]);
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
-                s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
+        for (int t = 0; t < D; ++t) band_col<NV>(bv[t], band, ns - 1 - t, ns, LDB, bw, lane);
+        for (int j0 = ns - 1; j0 >= 0; j0 -= D) {
+#pragma unroll
+            for (int t = 0; t < D; ++t) {
+                const int j = j0 - t;
+                if (j >= 0) {
+                    double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) {
+                        const int i = 1 + lane + 32 * q;
+                        if (i <= bw && j + i < ns) cfma(s, bv[t][q], xs[j + i]);
+                    }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
+                        s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
+                    }
+                    if (lane == 0) xs[j] = make_double2(xs[j].x - s.x, xs[j].y - s.y);
+                }
+                if (j - D >= 0) band_col<NV>(bv[t], band, j - D, ns, LDB, bw, lane);
+                __syncwarp();
             }
-            if (lane == 0) xs[j] = make_double2(xs[j].x - s.x, xs[j].y - s.y);
-            __syncwarp();
         }
         for (int s = lane; s < ns; s += 32) vec[G.skel_node[s]] = xs[s];
         __syncwarp();
-        // bubbles of the U cells: x_I = y_I - W x_B
+        // bubbles of the U cells: x_I = y_I - W x_B (W row o of the cell block: entries o * NO + NI + k)
         for (int uc = 0; uc < G.nucell; ++uc) {
             const int cell = G.ucells[uc];
             const int cx = cell % G.onx, cy = cell / G.onx;
-            const int base = cy * P * G.NXn + cx * P;
-            const double2* Wc = F + (size_t)cell * G.cellstride + NI * NI;
+            const int base = cy * P * NXn + cx * P;
+            const double2* Fc = F + (size_t)cell * G.cellstride;
             const int* cb = G.cell_bnd + (size_t)cell * NB;
             for (int o = lane; o < NI; o += 32) {
-                const int no = base + (1 + o / (P - 1)) * G.NXn + 1 + o % (P - 1);
+                const int no = bub(base, NXn, o);
                 double2 s = vec[no];
-                for (int k = 0; k < NB; ++k) cfms(s, Wc[o * NB + k], xs[cb[k]]);
+                for (int k = 0; k < NB; ++k) cfms(s, Fc[o * NO + NI + k], xs[cb[k]]);
                 vec[no] = s;
             }
         }
@@ -503,13 +569,13 @@ BandLaunch band_setup(const FineGeom& g, const std::vector<BandSubdomain>& subs,
     L.warp_elems = int((max_warp + 1) / 2 * 2);
     // sweep launch: as many warps per CTA as the per-warp vectors allow (<= 16)
     constexpr int kSmem = 232448;
-    L.warps = int(std::min<size_t>(16, kSmem / (size_t(L.warp_elems) * sizeof(double2))));
+    L.warps = int(std::min<size_t>(kBandThreads / 32, kSmem / (size_t(L.warp_elems) * sizeof(double2))));
     if (L.warps < 1) throw RuntimeError("band subdomain solver: Omega too large for shared memory");
     L.solve_smem = size_t(L.warps) * L.warp_elems * sizeof(double2);
     // setup: assemble, condense and factor every band subdomain on the device
     const int NE = (p + 1) * (p + 1);
     int ns_max = 0;
-    for (const BandGeomDev& d : gd) ns_max = std::max(ns_max, d.ns);
+    for (const BandGeomDev& d : gd) ns_max = std::max(ns_max, d.ns), L.bw_max = std::max(L.bw_max, d.bw);
     const size_t fsm = (size_t(NE) * NE + size_t(NI) * NI + size_t(NI) * NB + NI) * sizeof(double2) + size_t(ns_max) * 4;
     if (fsm > size_t(kSmem) - 4096) throw RuntimeError("band subdomain solver: element too large for shared memory");
     const int nsm = current_sm_count();
@@ -534,21 +600,32 @@ BandLaunch band_setup(const FineGeom& g, const std::vector<BandSubdomain>& subs,
 void band_solve_launch(const FineGeom& g, const BandLaunch& L, const double2* r, double2* ystage, int nu_max,
                        cudaStream_t st) {
     if (L.nsub == 0) return;
-    static bool attr[9] = {};
+    static bool attr[12] = {};
     const int nsm = current_sm_count();
     const int grid = std::min((L.nsub + L.warps - 1) / L.warps, nsm * std::max(1, 16 / L.warps));
-    auto go = [&](auto kern, int p) {
-        if (!attr[p]) {
+    auto go = [&](auto kern, int slot) {
+        if (!attr[slot]) {
             HTG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
-            attr[p] = true;
+            attr[slot] = true;
         }
         kern<<<grid, L.warps * 32, L.solve_smem, st>>>(g, L, r, ystage, nu_max);
     };
-    switch (g.p) {
-        case 2: go(k_band_solve<2>, 2); break;
-        case 4: go(k_band_solve<4>, 4); break;
-        case 6: go(k_band_solve<6>, 6); break;
-        default: go(k_band_solve<8>, 8); break;
+    // band entries per lane: bw <= 32 NV
+    const int nv = L.bw_max <= 64 ? 2 : (L.bw_max <= 128 ? 4 : 8);
+    if (L.bw_max > 256) throw RuntimeError("band subdomain solver: half bandwidth above 256");
+    switch (g.p * 10 + nv) {
+        case 22: go(k_band_solve<2, 2>, 0); break;
+        case 24: go(k_band_solve<2, 4>, 1); break;
+        case 28: go(k_band_solve<2, 8>, 2); break;
+        case 42: go(k_band_solve<4, 2>, 3); break;
+        case 44: go(k_band_solve<4, 4>, 4); break;
+        case 48: go(k_band_solve<4, 8>, 5); break;
+        case 62: go(k_band_solve<6, 2>, 6); break;
+        case 64: go(k_band_solve<6, 4>, 7); break;
+        case 68: go(k_band_solve<6, 8>, 8); break;
+        case 82: go(k_band_solve<8, 2>, 9); break;
+        case 84: go(k_band_solve<8, 4>, 10); break;
+        default: go(k_band_solve<8, 8>, 11); break;
     }
     HTG_CUDA(cudaGetLastError());
     count_launch();

@@ -135,6 +135,7 @@ struct BandLaunch {
     int nsub;
     int warps;               // sweep: warps (subdomains in flight) per CTA
     int warp_elems;          // sweep: shared-memory vector elements per warp
+    int bw_max;              // largest half bandwidth
     size_t solve_smem;
 };
 struct BandSubdomain {
