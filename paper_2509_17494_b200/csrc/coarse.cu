@@ -14,8 +14,12 @@
 #include <functional>
 #include <thread>
 
+#include <cooperative_groups.h>
+
 #include "coarse.hpp"
 #include "kernels.hpp"
+
+namespace cg = cooperative_groups;
 
 namespace htg {
 
@@ -42,6 +46,10 @@ constexpr int kCT = 256;     // threads per CTA (8 warps)
 #define HTG_ND_KU 4
 #endif
 constexpr int kWarpFMax = 128;  // warp-tier shared buffers (fronts with s + u <= g_warpF)
+#ifndef HTG_ND_MERGED
+#define HTG_ND_MERGED 0
+#endif
+constexpr bool kMergedLevels = HTG_ND_MERGED != 0;  // one launch per (branch, level) for all tiers
 static int env_int(const char* name, int dflt) {
     const char* e = std::getenv(name);
     return e ? std::atoi(e) : dflt;
@@ -181,16 +189,16 @@ __device__ void gather_front(const NDArgs& a, const NodeDev& nd, double2* sv, in
     sync();
 }
 
-// forward: y1 = (L^-1 P) v1, c = v2 - L21 y1. Warp tier: one warp per front.
-__global__ void __launch_bounds__(kCT) k_nd_fwd_warp(const NodeDev* __restrict__ list, int n, NDArgs a) {
-    __shared__ double2 sv[kCT / 32][kWarpFMax];
-    __shared__ double2 sy[kCT / 32][kWarpFMax];
+// forward: y1 = (L^-1 P) v1, c = v2 - L21 y1. Warp tier: one warp per front,
+// front item * 8 + warp of the list; ws: 2 x 8 x kWarpFMax shared entries.
+__device__ __forceinline__ void dev_fwd_warp(const NodeDev* __restrict__ list, int n, const NDArgs& a, int item,
+                                             double2* ws) {
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int id = blockIdx.x * (kCT / 32) + w;
+    const int id = item * (kCT / 32) + w;
     if (id >= n) return;
     const NodeDev nd = list[id];
-    double2* v = sv[w];
-    double2* y = sy[w];
+    double2* v = ws + w * 2 * kWarpFMax;
+    double2* y = v + kWarpFMax;
     gather_front<32>(a, nd, v, lane, [] { __syncwarp(); });
     cols_dot<1>(a.fac + nd.off_F, nd.s, nd.s, v, lane, [&](int r, double2 acc) {
         y[r] = acc;
@@ -202,11 +210,13 @@ __global__ void __launch_bounds__(kCT) k_nd_fwd_warp(const NodeDev* __restrict__
         a.contrib[nd.off_contrib + r] = make_double2(v2.x - acc.x, v2.y - acc.y);
     });
 }
+__global__ void __launch_bounds__(kCT) k_nd_fwd_warp(const NodeDev* __restrict__ list, int n, NDArgs a) {
+    __shared__ double2 ws[(kCT / 32) * 2 * kWarpFMax];
+    dev_fwd_warp(list, n, a, blockIdx.x, ws);
+}
 
 // forward, CTA tier: one CTA per front, both phases
-__global__ void __launch_bounds__(kCT) k_nd_fwd_mid(const NodeDev* __restrict__ list, NDArgs a) {
-    extern __shared__ double2 smem[];
-    const NodeDev nd = list[blockIdx.x];
+__device__ __forceinline__ void dev_fwd_mid(const NodeDev& nd, const NDArgs& a, double2* smem) {
     double2* v = smem;
     double2* y = smem + nd.s + nd.u;
     gather_front<kCT>(a, nd, v, threadIdx.x, [] { __syncthreads(); });
@@ -221,12 +231,14 @@ __global__ void __launch_bounds__(kCT) k_nd_fwd_mid(const NodeDev* __restrict__ 
         a.contrib[nd.off_contrib + r] = make_double2(v2.x - acc.x, v2.y - acc.y);
     });
 }
+__global__ void __launch_bounds__(kCT) k_nd_fwd_mid(const NodeDev* __restrict__ list, NDArgs a) {
+    extern __shared__ double2 smem[];
+    dev_fwd_mid(list[blockIdx.x], a, smem);
+}
 
 // forward, large tier phase 1: y1 rows of a task (v2 stashed by the r0 == 0 task)
-__global__ void __launch_bounds__(kCT) k_nd_fwd1(const Task* tasks, NDArgs a) {
-    extern __shared__ double2 smem[];
-    const Task tk = tasks[blockIdx.x];
-    const NodeDev nd = tk.nd;
+__device__ __forceinline__ void dev_fwd1(const Task& tk, const NDArgs& a, double2* smem) {
+    const NodeDev& nd = tk.nd;
     // rows [r0, r0 + nr) of the lower-triangular L^-1 P read v[0, r0 + nr) only; the
     // r0 == 0 task also stashes v2 for the contribution tasks
     gather_front<kCT>(a, nd, smem, threadIdx.x, [] { __syncthreads(); },
@@ -237,12 +249,14 @@ __global__ void __launch_bounds__(kCT) k_nd_fwd1(const Task* tasks, NDArgs a) {
     rows_dot<1>(a.fac + nd.off_F, nd.s, smem, tk.r0, tk.r0 + tk.nr, warp, kCT / 32, lane,
              [&](int r, double2 acc) { a.front[nd.off_front + r] = acc; });
 }
+__global__ void __launch_bounds__(kCT) k_nd_fwd1(const Task* tasks, NDArgs a) {
+    extern __shared__ double2 smem[];
+    dev_fwd1(tasks[blockIdx.x], a, smem);
+}
 
 // forward, large tier phase 2: contribution rows c = v2 - L21 y1
-__global__ void __launch_bounds__(kCT) k_nd_fwd2(const Task* tasks, NDArgs a) {
-    extern __shared__ double2 smem[];
-    const Task tk = tasks[blockIdx.x];
-    const NodeDev nd = tk.nd;
+__device__ __forceinline__ void dev_fwd2(const Task& tk, const NDArgs& a, double2* smem) {
+    const NodeDev& nd = tk.nd;
 #pragma unroll 4
     for (int i = threadIdx.x; i < nd.s; i += kCT) smem[i] = a.front[nd.off_front + i];
     __syncthreads();
@@ -251,6 +265,10 @@ __global__ void __launch_bounds__(kCT) k_nd_fwd2(const Task* tasks, NDArgs a) {
         const double2 v2 = a.front[nd.off_front + nd.s + r];
         a.contrib[nd.off_contrib + r] = make_double2(v2.x - acc.x, v2.y - acc.y);
     });
+}
+__global__ void __launch_bounds__(kCT) k_nd_fwd2(const Task* tasks, NDArgs a) {
+    extern __shared__ double2 smem[];
+    dev_fwd2(tasks[blockIdx.x], a, smem);
 }
 
 // backward: x1 = U^-1 y1 - (U^-1 U12) x2. Z rows are computed into sz first.
@@ -271,21 +289,20 @@ __device__ __forceinline__ void bwd_rows(const NDArgs& a, const NodeDev& nd, con
 }
 __device__ void sync_cta_fn() { __syncthreads(); }
 
-__global__ void __launch_bounds__(kCT) k_nd_bwd_warp(const NodeDev* __restrict__ list, int n, NDArgs a) {
-    __shared__ double2 sv[kCT / 32][kWarpFMax];
-    __shared__ double2 sz[kCT / 32][kWarpFMax];
+__device__ __forceinline__ void dev_bwd_warp(const NodeDev* __restrict__ list, int n, const NDArgs& a, int item,
+                                             double2* ws) {
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int id = blockIdx.x * (kCT / 32) + w;
+    const int id = item * (kCT / 32) + w;
     if (id >= n) return;
     const NodeDev nd = list[id];
-    double2* v = sv[w];
+    double2* v = ws + w * 2 * kWarpFMax;
 #pragma unroll 4
     for (int i = lane; i < nd.s; i += 32) v[i] = a.Y[a.idx[nd.off_var + i]];
 #pragma unroll 4
     for (int i = lane; i < nd.u; i += 32) v[nd.s + i] = a.X[a.idx[nd.off_ring + i]];
     __syncwarp();
     // x1 = U^-1 y1 - Z x2 (column-major blocks)
-    double2* z = sz[w];
+    double2* z = v + kWarpFMax;
     if (nd.u > 0) {
         cols_dot(a.fac + nd.off_Z, nd.s, nd.u, v + nd.s, lane, [&](int r, double2 acc) { z[r] = acc; });
         __syncwarp();
@@ -298,12 +315,14 @@ __global__ void __launch_bounds__(kCT) k_nd_bwd_warp(const NodeDev* __restrict__
         a.X[a.idx[nd.off_var + r]] = acc;
     });
 }
+__global__ void __launch_bounds__(kCT) k_nd_bwd_warp(const NodeDev* __restrict__ list, int n, NDArgs a) {
+    __shared__ double2 ws[(kCT / 32) * 2 * kWarpFMax];
+    dev_bwd_warp(list, n, a, blockIdx.x, ws);
+}
 
 // backward, CTA tasks (whole front for the CTA tier, row blocks for the large tier)
-__global__ void __launch_bounds__(kCT) k_nd_bwd(const Task* tasks, NDArgs a) {
-    extern __shared__ double2 smem[];
-    const Task tk = tasks[blockIdx.x];
-    const NodeDev nd = tk.nd;
+__device__ __forceinline__ void dev_bwd(const Task& tk, const NDArgs& a, double2* smem) {
+    const NodeDev& nd = tk.nd;
     double2* y1 = smem;
     double2* x2 = smem + nd.s;
     double2* sz = smem + nd.s + nd.u;
@@ -315,6 +334,60 @@ __global__ void __launch_bounds__(kCT) k_nd_bwd(const Task* tasks, NDArgs a) {
     for (int i = threadIdx.x; i < nd.u; i += kCT) x2[i] = a.X[a.idx[nd.off_ring + i]];
     __syncthreads();
     bwd_rows(a, nd, y1, x2, sz, tk.r0, tk.r0 + tk.nr, threadIdx.x >> 5, kCT / 32, threadIdx.x & 31, sync_cta_fn);
+}
+__global__ void __launch_bounds__(kCT) k_nd_bwd(const Task* tasks, NDArgs a) {
+    extern __shared__ double2 smem[];
+    dev_bwd(tasks[blockIdx.x], a, smem);
+}
+
+// ------------------------------------------------------------------ persistent solve
+// The whole solve as ONE cooperative launch: the phases (per depth, deepest
+// first: warp-tier fronts + CTA-tier fronts + large-tier y1 tasks, then the
+// large-tier contribution tasks; backward per depth, top first) are walked by
+// every CTA of a co-resident grid, items grid-strided, with a grid barrier
+// between phases. Replaces ~250 dependent launches (16 subtree branches on
+// forked streams) whose launch latencies dominated the solve.
+struct NDPhase {
+    const Task* tasks;    // fwd: y1 tasks (kind 0) or contribution tasks (kind 1); bwd: CTA / row-block tasks
+    const NodeDev* mid;   // fwd CTA-tier fronts
+    const NodeDev* warp;  // warp-tier fronts (8 per item)
+    int ntask, nmid, nwarp, kind;  // kind 0 fwd, 1 fwd contributions, 2 bwd
+};
+__device__ __forceinline__ int phase_items(const NDPhase& P) {
+    return P.ntask + P.nmid + (P.nwarp + kCT / 32 - 1) / (kCT / 32);
+}
+__device__ __forceinline__ void phase_item(const NDPhase& P, int it, const NDArgs& a, double2* smem) {
+    if (it < P.ntask) {
+        const Task tk = P.tasks[it];
+        if (P.kind == 0) dev_fwd1(tk, a, smem);
+        else if (P.kind == 1) dev_fwd2(tk, a, smem);
+        else dev_bwd(tk, a, smem);
+    } else if (it < P.ntask + P.nmid) {
+        const NodeDev nd = P.mid[it - P.ntask];
+        dev_fwd_mid(nd, a, smem);
+    } else {
+        const int wi = it - P.ntask - P.nmid;
+        if (P.kind == 2) dev_bwd_warp(P.warp, P.nwarp, a, wi, smem);
+        else dev_fwd_warp(P.warp, P.nwarp, a, wi, smem);
+    }
+}
+__global__ void __launch_bounds__(kCT) k_nd_persist(const NDPhase* __restrict__ ph, int nph, NDArgs a) {
+    extern __shared__ double2 smem[];
+    cg::grid_group grid = cg::this_grid();
+    for (int p = 0; p < nph; ++p) {
+        const NDPhase P = ph[p];
+        const int total = phase_items(P);
+        for (int it = blockIdx.x; it < total; it += gridDim.x) {
+            phase_item(P, it, a, smem);
+            __syncthreads();  // shared memory reuse by the next item
+        }
+        if (p + 1 < nph) grid.sync();
+    }
+}
+// one level of one subtree branch, every tier in ONE launch (item = block)
+__global__ void __launch_bounds__(kCT) k_nd_level(NDPhase P, NDArgs a) {
+    extern __shared__ double2 smem[];
+    phase_item(P, blockIdx.x, a, smem);
 }
 
 class NDSolver : public CoarseSolver {
@@ -350,6 +423,21 @@ class NDSolver : public CoarseSolver {
         NDArgs a = args_;
         a.rc = rc;
         a.X = uc;
+        if (nph_ > 0) {  // one cooperative launch walks every level (k_nd_persist)
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(pgrid_);
+            cfg.blockDim = dim3(kCT);
+            cfg.dynamicSmemBytes = psmem_;
+            cfg.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeCooperative;
+            at[0].val.cooperative = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            HTG_CUDA(cudaLaunchKernelEx(&cfg, k_nd_persist, static_cast<const NDPhase*>(phases_), nph_, a));
+            count_launch();
+            return;
+        }
         const int nb = int(br_.size()) - 1;  // branch 0: the top levels
 #ifdef HTG_ND_TIMING_SKIP
         static const int skip = env_int("HTG_ND_SKIP", 0);  // timing experiments only: 1 branches, 2 top
@@ -387,6 +475,21 @@ class NDSolver : public CoarseSolver {
         size_t smem_mid = 0, smem_big = 0, smem_b = 0;
     };
     static void fwd_level(const Level& lv, const NDArgs& a, cudaStream_t st) {
+        if (kMergedLevels) {  // warp + CTA + large-tier y1 items in one launch, then the contributions
+            const NDPhase p0{lv.f1, lv.mid, lv.warp, lv.nf1, lv.nmid, lv.nwarp, 0};
+            const int n0 = lv.nf1 + lv.nmid + (lv.nwarp + 7) / 8;
+            if (n0) {
+                const size_t sm = std::max({lv.nwarp ? size_t(2 * (kCT / 32) * kWarpFMax) * sizeof(double2) : size_t(0),
+                                            lv.smem_mid, lv.smem_big});
+                k_nd_level<<<n0, kCT, sm, st>>>(p0, a);
+                count_launch();
+            }
+            if (lv.nf2) {
+                k_nd_level<<<lv.nf2, kCT, lv.smem_big, st>>>(NDPhase{lv.f2, nullptr, nullptr, lv.nf2, 0, 0, 1}, a);
+                count_launch();
+            }
+            return;
+        }
         if (lv.nwarp) {
             k_nd_fwd_warp<<<(lv.nwarp + 7) / 8, kCT, 0, st>>>(lv.warp, lv.nwarp, a);
             count_launch();
@@ -405,6 +508,16 @@ class NDSolver : public CoarseSolver {
         }
     }
     static void bwd_level(const Level& lv, const NDArgs& a, cudaStream_t st) {
+        if (kMergedLevels) {
+            const int n = lv.nb + (lv.nwarp + 7) / 8;
+            if (n) {
+                const size_t sm = std::max(lv.nwarp ? size_t(2 * (kCT / 32) * kWarpFMax) * sizeof(double2) : size_t(0),
+                                           lv.smem_b);
+                k_nd_level<<<n, kCT, sm, st>>>(NDPhase{lv.b, nullptr, lv.warp, lv.nb, 0, lv.nwarp, 2}, a);
+                count_launch();
+            }
+            return;
+        }
         if (lv.nb) {
             k_nd_bwd<<<lv.nb, kCT, lv.smem_b, st>>>(lv.b, a);
             count_launch();
@@ -424,6 +537,9 @@ class NDSolver : public CoarseSolver {
     std::vector<void*> allocs_;
     size_t bytes_ = 0;
     size_t read_bytes_ = 0;
+    const NDPhase* phases_ = nullptr;  // persistent solve (HTG_ND_PERSIST, default on)
+    int nph_ = 0, pgrid_ = 0;
+    size_t psmem_ = 0;
     int nv_ = 0;
     long long delayed_ = 0;
     NDArgs args_{};
@@ -630,6 +746,44 @@ class NDSolver : public CoarseSolver {
                 max_smem = std::max({max_smem, lv.smem_mid, lv.smem_big, lv.smem_b});
                 br_[b][L] = lv;
             }
+        // persistent solve: the same work lists merged over the branches, per depth
+        if (env_int("HTG_ND_PERSIST", 0)) {
+            std::vector<NDPhase> ph;
+            auto mergedT = [&](std::vector<std::vector<Task>>& lists, int dep) {
+                std::vector<Task> out;
+                for (int b = 0; b <= nbranch; ++b) out.insert(out.end(), lists[li(b, dep)].begin(), lists[li(b, dep)].end());
+                return out;
+            };
+            auto mergedN = [&](std::vector<std::vector<NodeDev>>& lists, int dep) {
+                std::vector<NodeDev> out;
+                for (int b = 0; b <= nbranch; ++b) out.insert(out.end(), lists[li(b, dep)].begin(), lists[li(b, dep)].end());
+                return out;
+            };
+            for (int dep = D - 1; dep >= 0; --dep) {
+                auto t1 = mergedT(f1, dep), t2 = mergedT(f2, dep);
+                auto m = mergedN(md, dep), w = mergedN(wp, dep);
+                if (!t1.empty() || !m.empty() || !w.empty())
+                    ph.push_back({up(t1, st), up(m, st), up(w, st), int(t1.size()), int(m.size()), int(w.size()), 0});
+                if (!t2.empty()) ph.push_back({up(t2, st), nullptr, nullptr, int(t2.size()), 0, 0, 1});
+            }
+            for (int dep = 0; dep < D; ++dep) {
+                auto tb = mergedT(bw, dep);
+                auto w = mergedN(wp, dep);
+                if (!tb.empty() || !w.empty())
+                    ph.push_back({up(tb, st), nullptr, up(w, st), int(tb.size()), 0, int(w.size()), 2});
+            }
+            psmem_ = std::max(max_smem, size_t(2 * (kCT / 32) * kWarpFMax) * sizeof(double2));
+            if (psmem_ > 227 * 1024) throw InvalidArgument("coarse front too large for shared memory");
+            static std::once_flag pers_once;
+            std::call_once(pers_once, [] {
+                HTG_CUDA(cudaFuncSetAttribute(k_nd_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+            });
+            int per_sm = 0;
+            HTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nd_persist, kCT, psmem_));
+            pgrid_ = std::max(1, per_sm) * current_sm_count();
+            phases_ = up(ph, st);
+            nph_ = int(ph.size());
+        }
         for (int b = 0; b < nbranch; ++b) {
             cudaStream_t x;
             cudaEvent_t e;
@@ -650,6 +804,7 @@ class NDSolver : public CoarseSolver {
             HTG_CUDA(cudaFuncSetAttribute(k_nd_fwd1, cudaFuncAttributeMaxDynamicSharedMemorySize, kOptIn));
             HTG_CUDA(cudaFuncSetAttribute(k_nd_fwd2, cudaFuncAttributeMaxDynamicSharedMemorySize, kOptIn));
             HTG_CUDA(cudaFuncSetAttribute(k_nd_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kOptIn));
+            HTG_CUDA(cudaFuncSetAttribute(k_nd_level, cudaFuncAttributeMaxDynamicSharedMemorySize, kOptIn));
         });
     }
 };
