@@ -240,7 +240,14 @@ void build_handle(htg_handle* H, const htg_problem& prob, const htg_config& cfg)
             H->dd_flops_dense += 8.0 * c.nu * c.nloc;
             H->sum_u += c.nu;
             H->sum_omega += c.nloc;
-            if (c.fdm && fdm_supported(hp.p, c.fdm_nx, c.fdm_ny)) {
+            if (c.fdm && c.fdm_sym) {
+                // parity blocks: each product splits into an even and an odd half
+                // (13 / 12 eigenvectors, 9 / 8 U rows at p = 4)
+                const double n = c.fdm_nx, ne = (n + 1) / 2, no = (n - 1) / 2, u = c.fdm_nux, ue = (u + 1) / 2,
+                             uo = (u - 1) / 2;
+                H->dd_flops += 8.0 * (2 * n * (ne * ne + no * no) + n * (ue * ne + uo * no) + u * (ue * ne + uo * no));
+                H->fdm_subs += 1;
+            } else if (c.fdm && fdm_supported(hp.p, c.fdm_nx, c.fdm_ny)) {
                 const double nx = c.fdm_nx, ny = c.fdm_ny, ux = c.fdm_nux, uy = c.fdm_nuy;
                 H->dd_flops += 8.0 * (nx * nx * ny + nx * ny * ny + ux * nx * ny + ux * ny * uy);
                 H->fdm_subs += 1;

@@ -302,6 +302,26 @@ DDDevice upload_dd_impl(const DDSetup& dd, const HostProblem& hp, std::vector<vo
             f.Vx = put(vx);
             f.Vy = put(vy);
             f.Dinv = put(dv);
+            if (c.fdm_sym) {
+                auto putc = [&](const std::vector<cplx>& v) {
+                    std::vector<double2> w(v.size());
+                    for (size_t i = 0; i < v.size(); ++i) w[i] = make_double2(v[i].real(), v[i].imag());
+                    return put(w);
+                };
+                f.sym = 1;
+                f.Vxe = putc(c.Vxe);
+                f.Vxo = putc(c.Vxo);
+                f.Vye = putc(c.Vye);
+                f.Vyo = putc(c.Vyo);
+                std::vector<int> mr(c.mirror.size());
+                for (size_t i = 0; i < mr.size(); ++i) mr[i] = c.mirror[i] | ((c.msign[i] > 0 ? 1 : 0) << 16);
+                void* ptr = nullptr;
+                HTG_CUDA(cudaMalloc(&ptr, mr.size() * sizeof(int)));
+                allocs.push_back(ptr);
+                bytes += mr.size() * sizeof(int);
+                HTG_CUDA(cudaMemcpy(ptr, mr.data(), mr.size() * sizeof(int), cudaMemcpyHostToDevice));
+                f.mir = static_cast<const int*>(ptr);
+            }
             {  // relative gather offsets, shared by every member of the class (checked)
                 const int nx = f.nx, ny = f.ny;
                 std::vector<int> go(size_t(nx) * ny);

@@ -604,12 +604,53 @@ __global__ void __launch_bounds__(kWThreads(P, NP), 1)
         int* gpos = gofs + nx * ny;    // ... and the tile slot each one lands in
         __syncthreads();  // previous segment finished with the factors
         const double2 z = make_double2(0.0, 0.0);
-        for (int i = tid; i < 2 * KP * LD; i += nthr) {
-            const int a = i / LD, b = i - a * LD;
-            double2 v = z;
-            if (a < KP) v = (a < nx && b < nx) ? c.Vx[b * nx + a] : z;
-            else v = (a - KP < ny && b < ny) ? c.Vy[b * ny + (a - KP)] : z;
-            fac[i] = v;
+        const bool sym = (P == 4) && c.sym;
+        // mirror tables of a symmetric class (after the gather tables):
+        // bfn[r]: natural rows of reordered row r; ubn[n]: reordered rows of natural row n
+        int* bfn = gpos + nx * ny;
+        int* ubn = bfn + 32;
+        if (sym) {
+            // V1T: rows [0, 16) Ve^T (13 x 13), rows [16, 28) Vo^T (12 x 12); same for V2T
+            for (int i = tid; i < 2 * KP * LD; i += nthr) {
+                const int a0 = i / LD, b = i - a0 * LD, dir = a0 / KP, a = a0 - dir * KP;
+                const double2* Ve = dir ? c.Vye : c.Vxe;
+                const double2* Vo = dir ? c.Vyo : c.Vxo;
+                double2 v = z;
+                if (a < 16) v = (a < 13 && b < 13) ? Ve[b * 13 + a] : z;
+                else v = (a - 16 < 12 && b < 12) ? Vo[b * 12 + (a - 16)] : z;
+                fac[i] = v;
+            }
+            if (tid < 25) {
+                // reordered r -> natural: r < 12 pair g = r (n1 = g, n2 = R(g), +s); r = 12 centre;
+                // r >= 13 odd pair g = r - 13 (-s). packed n1 | n2 << 8 | sign bit << 16 (bit set: -)
+                const int r = tid;
+                int code;
+                if (r == 12) code = 12 | (255 << 8);
+                else {
+                    const int gg = r < 12 ? r : r - 13, m = c.mir[gg];
+                    const bool spos = (m >> 16) & 1;
+                    const bool neg = r < 12 ? !spos : spos;
+                    code = gg | ((m & 0xffff) << 8) | (neg ? 1 << 16 : 0);
+                }
+                bfn[r] = code;
+                // natural n -> (pair g, form): n < 12: (e_g + o_g)/r2; n = 12: e_c; n > 12:
+                // s_g (e_g - o_g)/r2 with R(g) = n. packed g | form << 8 (0 plus, 1 centre, 2 s>0, 3 s<0)
+                const int n = tid;
+                int ucode = 12 | (1 << 8);
+                if (n < 12) ucode = n;
+                else if (n > 12)
+                    for (int gg = 0; gg < 12; ++gg)
+                        if ((c.mir[gg] & 0xffff) == n) ucode = gg | ((((c.mir[gg] >> 16) & 1) ? 2 : 3) << 8);
+                ubn[n] = ucode;
+            }
+        } else {
+            for (int i = tid; i < 2 * KP * LD; i += nthr) {
+                const int a = i / LD, b = i - a * LD;
+                double2 v = z;
+                if (a < KP) v = (a < nx && b < nx) ? c.Vx[b * nx + a] : z;
+                else v = (a - KP < ny && b < ny) ? c.Vy[b * ny + (a - KP)] : z;
+                fac[i] = v;
+            }
         }
         for (int i = tid; i < nx * ny; i += nthr) D[i] = c.Dinv[i];
         for (int i = tid; i < nux * nuy; i += nthr) {
@@ -641,6 +682,119 @@ __global__ void __launch_bounds__(kWThreads(P, NP), 1)
         };
         int cur = pos + team;
         if (cur < seg_end) gather(cur);
+        if constexpr (P == 4) {
+            if (sym) {
+                constexpr double r2 = 0.70710678118654752440;
+                for (; cur < seg_end; cur += nteam) {
+                    const int id = c.subs[cur - c.first];
+                    asm volatile("cp.async.wait_all;\n" ::: "memory");
+                    team_sync<NP>(team);
+                    // mirror butterflies in x and y: G[iy][ix] (natural) -> W[iy_r][ix_r]
+                    for (int e = tl; e < 625; e += NP * 32) {
+                        const int ry = e / 25, rx = e - ry * 25;
+                        const int by = bfn[ry], bx = bfn[rx];
+                        const int y1 = by & 255, y2 = (by >> 8) & 255, x1 = bx & 255, x2 = (bx >> 8) & 255;
+                        const double cy2 = (by >> 16) ? -r2 : r2, cx2 = (bx >> 16) ? -r2 : r2;
+                        const double cy1 = y2 == 255 ? 1.0 : r2, cx1 = x2 == 255 ? 1.0 : r2;
+                        const double2 a = X[y1 * LD + x1];
+                        double2 s = make_double2(cy1 * cx1 * a.x, cy1 * cx1 * a.y);
+                        if (x2 != 255) {
+                            const double2 b = X[y1 * LD + x2];
+                            s.x = fma(cy1 * cx2, b.x, s.x);
+                            s.y = fma(cy1 * cx2, b.y, s.y);
+                        }
+                        if (y2 != 255) {
+                            const double2 b = X[y2 * LD + x1];
+                            s.x = fma(cy2 * cx1, b.x, s.x);
+                            s.y = fma(cy2 * cx1, b.y, s.y);
+                            if (x2 != 255) {
+                                const double2 d2 = X[y2 * LD + x2];
+                                s.x = fma(cy2 * cx2, d2.x, s.x);
+                                s.y = fma(cy2 * cx2, d2.y, s.y);
+                            }
+                        }
+                        W[ry * LD + rx] = s;
+                    }
+                    team_sync<NP>(team);
+                    // 1: per x-parity P_p[ix'][iy] = sum_{ix in p} V_p[ix][ix'] G[iy][ix] -> X[ix'_r][iy]
+                    WStage<LD, 4, false>{V1T, 13, 0, W, 25, true, lane, part, NP}([&](int m, int n, double2 v) {
+                        if (m < 13 && n < 25) X[m * LD + n] = v;
+                    });
+                    WStage<LD, 3, false>{V1T + 16 * LD, 12, 0, W + 13, 25, true, lane, NP - 1 - part, NP}(
+                        [&](int m, int n, double2 v) {
+                            if (m < 12 && n < 25) X[(m + 13) * LD + n] = v;
+                        });
+                    team_sync<NP>(team);
+                    // 2: per y-parity, times Dinv -> W[iy'_r][ix'_r]
+                    WStage<LD, 4, false>{V2T, 13, 0, X, 25, false, lane, part, NP}([&](int m, int n, double2 v) {
+                        if (m < 25 && n < 13) {
+                            const double2 d = D[m * 25 + n];
+                            W[n * LD + m] = make_double2(v.x * d.x - v.y * d.y, v.x * d.y + v.y * d.x);
+                        }
+                    });
+                    WStage<LD, 3, false>{V2T + 16 * LD, 12, 0, X + 13, 25, false, lane, NP - 1 - part, NP}(
+                        [&](int m, int n, double2 v) {
+                            if (m < 25 && n < 12) {
+                                const double2 d = D[m * 25 + n + 13];
+                                W[(n + 13) * LD + m] = make_double2(v.x * d.x - v.y * d.y, v.x * d.y + v.y * d.x);
+                            }
+                        });
+                    team_sync<NP>(team);
+                    // 3: U rows per x-parity (pairs 4..12 even, 4..11 odd) -> X[u_r][iy'_r]
+                    WStage<LD, 4, true>{V1T, 9, 4, W, 25, true, lane, part, NP}([&](int m, int n, double2 v) {
+                        if (m < 9 && n < 25) X[m * LD + n] = v;
+                    });
+                    WStage<LD, 3, true>{V1T + 16 * LD, 8, 4, W + 13, 25, true, lane, NP - 1 - part, NP}(
+                        [&](int m, int n, double2 v) {
+                            if (m < 8 && n < 25) X[(m + 9) * LD + n] = v;
+                        });
+                    team_sync<NP>(team);
+                    // 4: U columns per y-parity -> W[u_r][v_r]
+                    WStage<LD, 4, true>{V2T, 9, 4, X, 17, false, lane, part, NP}([&](int m, int n, double2 v) {
+                        if (m < 17 && n < 9) W[m * LD + n] = v;
+                    });
+                    WStage<LD, 3, true>{V2T + 16 * LD, 8, 4, X + 13, 17, false, lane, NP - 1 - part, NP}(
+                        [&](int m, int n, double2 v) {
+                            if (m < 17 && n < 8) W[m * LD + n + 9] = v;
+                        });
+                    team_sync<NP>(team);
+                    // the gathered tile is free: fetch the team's next subdomain under the unbutterfly
+                    if (cur + nteam < seg_end) gather(cur + nteam);
+                    // inverse butterflies on the U block -> staging row of the subdomain
+                    double2* yrow = ystage + (size_t)id * nu_max;
+                    for (int e = tl; e < 289; e += NP * 32) {
+                        const int ixu = e / 17, iyu = e - ixu * 17;
+                        int rx[2], ry[2];
+                        double cx[2], cy[2];
+                        auto coef = [&](int nat, int* rr, double* cc) {
+                            const int u = ubn[nat], gg = u & 255, form = u >> 8;
+                            rr[0] = gg - 4;
+                            rr[1] = 9 + gg - 4;
+                            if (form == 1) cc[0] = 1.0, cc[1] = 0.0, rr[1] = rr[0];
+                            else if (form == 0) cc[0] = r2, cc[1] = r2;
+                            else if (form == 2) cc[0] = r2, cc[1] = -r2;
+                            else cc[0] = -r2, cc[1] = r2;
+                        };
+                        coef(4 + ixu, rx, cx);
+                        coef(4 + iyu, ry, cy);
+                        double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+                        for (int a = 0; a < 2; ++a)
+#pragma unroll
+                            for (int b = 0; b < 2; ++b) {
+                                const double w = cx[a] * cy[b];
+                                const double2 v = W[rx[a] * LD + ry[b]];
+                                s.x = fma(w, v.x, s.x);
+                                s.y = fma(w, v.y, s.y);
+                            }
+                        yrow[urow[ixu * 17 + iyu]] = s;
+                    }
+                }
+                asm volatile("cp.async.wait_all;\n" ::: "memory");
+                pos = seg_end;
+                continue;
+            }
+        }
         for (; cur < seg_end; cur += nteam) {
             const int id = c.subs[cur - c.first];
             asm volatile("cp.async.wait_all;\n" ::: "memory");
@@ -744,7 +898,7 @@ std::vector<int4> fdm_plan(std::vector<FdmClassDev>& cls, int p, int nsm, FdmLau
         const int KP = p == 2 ? 4 * FdmDims<2>::KS : 4 * FdmDims<4>::KS;
         int wfac = 0;
         for (auto& c : cls)
-            wfac = std::max(wfac, 2 * KP * LD + c.nx * c.ny + (c.nux * c.nuy + 2 * c.nx * c.ny + 3) / 4);
+            wfac = std::max(wfac, 2 * KP * LD + c.nx * c.ny + (c.nux * c.nuy + 2 * c.nx * c.ny + 64 + 3) / 4);
         wfac = (wfac + 7) / 8 * 8;
         const int per_warp = 2 * ext * LD;
         int nt = (kSmemMax / int(sizeof(double2)) - wfac) / per_warp;  // teams (buffer pairs)

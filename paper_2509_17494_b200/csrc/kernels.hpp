@@ -94,6 +94,12 @@ struct FdmClassDev {
     const int* goff;    // gather offsets: tile element iy * nx + ix -> dof offset from the
                         // subdomain's first dof (identical for every member), or null
     const int* gord;    // tile elements in ascending goff order (memory-order gather), or null
+    // mirror-symmetric class (p = 4, 6 x 6-cell Omega, centred 4 x 4 U): parity blocks
+    // Ve (13 x 13), Vo (12 x 12) per direction, Vx/Vy/Dinv in [even | odd] order and
+    // mir[g] = R(g) | (s_g > 0) << 16 for g < 12 (fdm.cpp)
+    int sym;
+    const double2 *Vxe, *Vxo, *Vye, *Vyo;
+    const int* mir;
     int nsub;
     int first;          // offset of this class in the class-sorted subdomain list
 };

@@ -67,6 +67,17 @@ struct DDClass {
     std::vector<cplx> Vx, Vy;      // (nx x nx), (ny x ny) row-major, columns are eigenvectors
     std::vector<cplx> Dinv;        // nx x ny
     double fdm_err = 0.0;          // max |B_fdm - B| / max |B| over the class
+    // mirror-symmetric classes (an even number of Omega cells per direction, equal
+    // ends, U centred): the 1-D operators commute with the reflection R (a signed
+    // permutation of the hierarchical dofs), so each direction splits into an even
+    // (n+1)/2 and an odd (n-1)/2 generalised eigenproblem. Vx, Vy, Dinv then hold the
+    // full factors in that order ([even | odd] eigenvectors); the parity blocks are
+    // V_e ((n+1)/2 square) and V_o ((n-1)/2 square) in the basis
+    // e_g = (d_g + s_g d_R(g)) / sqrt 2, o_g = (d_g - s_g d_R(g)) / sqrt 2 (g < centre),
+    // e_c = d_c; mirror[g] = R(g), msign[g] = s_g for g < centre.
+    bool fdm_sym = false;
+    std::vector<cplx> Vxe, Vxo, Vye, Vyo;
+    std::vector<int> mirror, msign;
     // no shared factor (few members, coefficients varying over Omega): every
     // member is factored on the device (k_band.cu); B stays empty
     bool band = false;
