@@ -13,6 +13,7 @@
 #include <cmath>
 #include <functional>
 #include <thread>
+#include <utility>
 
 #include <cooperative_groups.h>
 
@@ -55,6 +56,22 @@ static int env_int(const char* name, int dflt) {
     return e ? std::atoi(e) : dflt;
 }
 // tier thresholds (overridable for tuning: HTG_ND_LEAF, HTG_ND_WARPF, HTG_ND_MIDDATA, HTG_ND_RPT)
+
+// programmatic dependent launch (HTG_ND_PDL=1; off: measured 1.01 vs 0.84 ms at cfg4, the
+// early-scheduled dependent CTAs hold SM slots the other branches need): a level kernel lets the
+// next one in its stream be scheduled at once and waits for its predecessor only
+// before touching solve data, so the ~30 dependent launches of a subtree branch
+// overlap their launch latency with the previous level's tail
+#ifndef HTG_ND_PDL
+#define HTG_ND_PDL 0
+#endif
+constexpr bool kPdl = HTG_ND_PDL != 0;
+__device__ __forceinline__ void pdl_begin() {
+    if constexpr (kPdl) {
+        asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+        asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    }
+}
 
 __device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {
     return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
@@ -211,6 +228,7 @@ __device__ __forceinline__ void dev_fwd_warp(const NodeDev* __restrict__ list, i
     });
 }
 __global__ void __launch_bounds__(kCT) k_nd_fwd_warp(const NodeDev* __restrict__ list, int n, NDArgs a) {
+    pdl_begin();
     __shared__ double2 ws[(kCT / 32) * 2 * kWarpFMax];
     dev_fwd_warp(list, n, a, blockIdx.x, ws);
 }
@@ -232,6 +250,7 @@ __device__ __forceinline__ void dev_fwd_mid(const NodeDev& nd, const NDArgs& a, 
     });
 }
 __global__ void __launch_bounds__(kCT) k_nd_fwd_mid(const NodeDev* __restrict__ list, NDArgs a) {
+    pdl_begin();
     extern __shared__ double2 smem[];
     dev_fwd_mid(list[blockIdx.x], a, smem);
 }
@@ -250,6 +269,7 @@ __device__ __forceinline__ void dev_fwd1(const Task& tk, const NDArgs& a, double
              [&](int r, double2 acc) { a.front[nd.off_front + r] = acc; });
 }
 __global__ void __launch_bounds__(kCT) k_nd_fwd1(const Task* tasks, NDArgs a) {
+    pdl_begin();
     extern __shared__ double2 smem[];
     dev_fwd1(tasks[blockIdx.x], a, smem);
 }
@@ -267,6 +287,7 @@ __device__ __forceinline__ void dev_fwd2(const Task& tk, const NDArgs& a, double
     });
 }
 __global__ void __launch_bounds__(kCT) k_nd_fwd2(const Task* tasks, NDArgs a) {
+    pdl_begin();
     extern __shared__ double2 smem[];
     dev_fwd2(tasks[blockIdx.x], a, smem);
 }
@@ -316,6 +337,7 @@ __device__ __forceinline__ void dev_bwd_warp(const NodeDev* __restrict__ list, i
     });
 }
 __global__ void __launch_bounds__(kCT) k_nd_bwd_warp(const NodeDev* __restrict__ list, int n, NDArgs a) {
+    pdl_begin();
     __shared__ double2 ws[(kCT / 32) * 2 * kWarpFMax];
     dev_bwd_warp(list, n, a, blockIdx.x, ws);
 }
@@ -336,6 +358,7 @@ __device__ __forceinline__ void dev_bwd(const Task& tk, const NDArgs& a, double2
     bwd_rows(a, nd, y1, x2, sz, tk.r0, tk.r0 + tk.nr, threadIdx.x >> 5, kCT / 32, threadIdx.x & 31, sync_cta_fn);
 }
 __global__ void __launch_bounds__(kCT) k_nd_bwd(const Task* tasks, NDArgs a) {
+    pdl_begin();
     extern __shared__ double2 smem[];
     dev_bwd(tasks[blockIdx.x], a, smem);
 }
@@ -474,6 +497,21 @@ class NDSolver : public CoarseSolver {
         int nwarp = 0, nmid = 0, nf1 = 0, nf2 = 0, nb = 0;
         size_t smem_mid = 0, smem_big = 0, smem_b = 0;
     };
+    template <class... KArgs, class... Args>
+    static void launch(void (*kern)(KArgs...), int grid, size_t smem, cudaStream_t st, Args&&... args) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(unsigned(grid));
+        cfg.blockDim = dim3(kCT);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = kPdl ? 1 : 0;
+        HTG_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+        count_launch();
+    }
     static void fwd_level(const Level& lv, const NDArgs& a, cudaStream_t st) {
         if (kMergedLevels) {  // warp + CTA + large-tier y1 items in one launch, then the contributions
             const NDPhase p0{lv.f1, lv.mid, lv.warp, lv.nf1, lv.nmid, lv.nwarp, 0};
@@ -490,22 +528,10 @@ class NDSolver : public CoarseSolver {
             }
             return;
         }
-        if (lv.nwarp) {
-            k_nd_fwd_warp<<<(lv.nwarp + 7) / 8, kCT, 0, st>>>(lv.warp, lv.nwarp, a);
-            count_launch();
-        }
-        if (lv.nmid) {
-            k_nd_fwd_mid<<<lv.nmid, kCT, lv.smem_mid, st>>>(lv.mid, a);
-            count_launch();
-        }
-        if (lv.nf1) {
-            k_nd_fwd1<<<lv.nf1, kCT, lv.smem_big, st>>>(lv.f1, a);
-            count_launch();
-        }
-        if (lv.nf2) {
-            k_nd_fwd2<<<lv.nf2, kCT, lv.smem_big, st>>>(lv.f2, a);
-            count_launch();
-        }
+        if (lv.nwarp) launch(k_nd_fwd_warp, (lv.nwarp + 7) / 8, 0, st, lv.warp, lv.nwarp, a);
+        if (lv.nmid) launch(k_nd_fwd_mid, lv.nmid, lv.smem_mid, st, lv.mid, a);
+        if (lv.nf1) launch(k_nd_fwd1, lv.nf1, lv.smem_big, st, lv.f1, a);
+        if (lv.nf2) launch(k_nd_fwd2, lv.nf2, lv.smem_big, st, lv.f2, a);
     }
     static void bwd_level(const Level& lv, const NDArgs& a, cudaStream_t st) {
         if (kMergedLevels) {
@@ -518,14 +544,8 @@ class NDSolver : public CoarseSolver {
             }
             return;
         }
-        if (lv.nb) {
-            k_nd_bwd<<<lv.nb, kCT, lv.smem_b, st>>>(lv.b, a);
-            count_launch();
-        }
-        if (lv.nwarp) {
-            k_nd_bwd_warp<<<(lv.nwarp + 7) / 8, kCT, 0, st>>>(lv.warp, lv.nwarp, a);
-            count_launch();
-        }
+        if (lv.nb) launch(k_nd_bwd, lv.nb, lv.smem_b, st, lv.b, a);
+        if (lv.nwarp) launch(k_nd_bwd_warp, (lv.nwarp + 7) / 8, 0, st, lv.warp, lv.nwarp, a);
     }
     // br_[0]: levels 0 .. split-1 (the top); br_[b]: the subtree of the b-th node at
     // the split depth, indexed by depth - split

@@ -247,7 +247,7 @@ struct Stage {
                 f = j - a * FT;
             }
             const double2* dr = dat + d * LD;
-            const int sk = kSkew ? (d & 3) : 0;
+            const int sk = kSkew ? ((lane >> 1) & 3) : 0;  // consecutive lanes: consecutive rows
             // 8 independent accumulator chains (4 terms x k parity): the dot is
             // DFMA-latency bound otherwise
             double acc[2][4] = {};
@@ -540,7 +540,7 @@ struct WStage {
                 f = j - a * FT;
             }
             const double2* dr = dat + d * LD;
-            const int sk = kSkew ? (d & 3) : 0;
+            const int sk = kSkew ? ((lane >> 1) & 3) : 0;  // consecutive lanes: consecutive rows
             double acc[2][4] = {};  // independent chains, as in Stage
 #pragma unroll
             for (int kk = 0; kk < 4 * KS; ++kk) {
