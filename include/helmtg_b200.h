@@ -52,7 +52,13 @@ typedef struct htg_problem {
     const int* tags_right;
     const int* tags_top;
     const int* tags_left;
+    /* element kind (appended; zero = squares): HTG_ELEM_SQUARE, or HTG_ELEM_TRIANGLE
+     * for cells split along the (0,0)-(1,1) diagonal (ElementKind::Triangle,
+     * proj/core/include/helmtg/mesh.hpp) */
+    int element_kind;
 } htg_problem;
+#define HTG_ELEM_SQUARE 0
+#define HTG_ELEM_TRIANGLE 1
 
 /* proj/core/include/helmtg/twogrid.hpp:18-30, same fields and defaults
  * (htg_config_default). */

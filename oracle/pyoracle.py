@@ -29,13 +29,13 @@ def build() -> str:
 class _Spec(C.Structure):
     _fields_ = [("order", C.c_int), ("wavelengths", C.c_double), ("ppw", C.c_double),
                 ("side", C.c_int * 4), ("layer_mask", C.c_uint),
-                ("layer_width_dofs", C.c_double), ("damping_D", C.c_double)]
+                ("layer_width_dofs", C.c_double), ("damping_D", C.c_double), ("element_kind", C.c_int)]
 
 
 class _Desc(C.Structure):
     _fields_ = [("order", C.c_int), ("nx", C.c_int), ("ny", C.c_int), ("h", C.c_double),
                 ("k_cells", C.POINTER(C.c_double)), ("eps_cells", C.POINTER(C.c_double)),
-                ("side", C.c_int * 4)]
+                ("side", C.c_int * 4), ("element_kind", C.c_int)]
 
 
 class _Cfg(C.Structure):
@@ -112,6 +112,7 @@ class ProblemSpec:
     layer_sides: tuple = ()
     layer_width_dofs: float = 40.0
     damping_D: float = 0.0
+    element_kind: int = 0  # 0 squares, 1 triangles (the reference's ElementKind; the restated oracle: squares)
 
 
 class Session:
@@ -125,18 +126,22 @@ class Session:
         cfgp = C.byref(cfg) if cfg is not None else None
         if desc is None:
             spec = spec or ProblemSpec()
+            if spec.element_kind != 0:
+                raise ValueError("the restated oracle covers square elements; use oracle.pyref for triangles")
             mask = 0
             for s in spec.layer_sides:
                 mask |= 1 << s
             cs = _Spec(spec.order, spec.wavelengths, spec.ppw, (C.c_int * 4)(*spec.side_tags), mask,
-                       spec.layer_width_dofs, spec.damping_D)
+                       spec.layer_width_dofs, spec.damping_D, 0)
             _check(L.orc_session_from_spec(C.byref(cs), cfgp, C.byref(h)))
         else:
             nx, ny = desc["nx"], desc["ny"]
             self._k = np.ascontiguousarray(np.broadcast_to(np.asarray(desc["k"], float), (ny, nx)))
             self._e = np.ascontiguousarray(np.broadcast_to(np.asarray(desc.get("eps", 0.0), float), (ny, nx)))
             d = _Desc(desc["order"], nx, ny, desc["h"], self._k.ctypes.data_as(C.POINTER(C.c_double)),
-                      self._e.ctypes.data_as(C.POINTER(C.c_double)), (C.c_int * 4)(*desc["side_tags"]))
+                      self._e.ctypes.data_as(C.POINTER(C.c_double)), (C.c_int * 4)(*desc["side_tags"]), 0)
+            if desc.get("element_kind", 0) != 0:
+                raise ValueError("the restated oracle covers square elements; use oracle.pyref for triangles")
             _check(L.orc_session_from_desc(C.byref(d), cfgp, C.byref(h)))
         self._h = h
         self.config = config

@@ -109,14 +109,15 @@ class RefSession:
             for s in spec.layer_sides:
                 mask |= 1 << s
             cs = _Spec(spec.order, spec.wavelengths, spec.ppw, (C.c_int * 4)(*spec.side_tags), mask,
-                       spec.layer_width_dofs, spec.damping_D)
+                       spec.layer_width_dofs, spec.damping_D, spec.element_kind)
             _check(L.ref_session_from_spec(C.byref(cs), cfgp, C.byref(h)))
         else:
             nx, ny = desc["nx"], desc["ny"]
             self._k = np.ascontiguousarray(np.broadcast_to(np.asarray(desc["k"], float), (ny, nx)))
             self._e = np.ascontiguousarray(np.broadcast_to(np.asarray(desc.get("eps", 0.0), float), (ny, nx)))
             d = _Desc(desc["order"], nx, ny, desc["h"], self._k.ctypes.data_as(C.POINTER(C.c_double)),
-                      self._e.ctypes.data_as(C.POINTER(C.c_double)), (C.c_int * 4)(*desc["side_tags"]))
+                      self._e.ctypes.data_as(C.POINTER(C.c_double)), (C.c_int * 4)(*desc["side_tags"]),
+                      int(desc.get("element_kind", 0)))
             _check(L.ref_session_from_desc(C.byref(d), cfgp, C.byref(h)))
         self._h = h
         self.config = config

@@ -77,6 +77,7 @@ struct ref_spec {
     int side[4];  // L, R, B, T: 0 Dirichlet, 1 Neumann, 2 Absorbing
     unsigned layer_mask;
     double layer_width_dofs, damping_D;
+    int element_kind;  // 0 Square, 1 Triangle (ElementKind)
 };
 struct ref_desc {
     int order, nx, ny;
@@ -84,6 +85,7 @@ struct ref_desc {
     const double* k_cells;    // nx*ny, (y,x) order
     const double* eps_cells;  // nx*ny
     int side[4];
+    int element_kind;
 };
 struct ref_cfg {
     double alpha_s, alpha_c;
@@ -123,7 +125,8 @@ int ref_session_from_spec(const ref_spec* s, const ref_cfg* c, void** out) {
         pr.k = 2.0 * M_PI * s->wavelengths;
         pr.n_cells = static_cast<int>(std::lround(s->wavelengths * s->ppw / s->order));
         if (pr.n_cells < 2) throw std::invalid_argument("build_problem: domain under-resolved");
-        pr.mesh = std::make_unique<StructuredMesh>(StructuredMesh::unit_square(pr.n_cells, ElementKind::Square));
+        pr.mesh = std::make_unique<StructuredMesh>(
+            StructuredMesh::unit_square(pr.n_cells, s->element_kind ? ElementKind::Triangle : ElementKind::Square));
         pr.space = std::make_unique<FeSpace>(FeSpace::build(*pr.mesh, s->order));
         std::map<Side, BoundaryTag> sides;
         for (int i = 0; i < 4; ++i) sides[kSide[i]] = kTag[s->side[i]];
@@ -157,7 +160,8 @@ int ref_session_from_desc(const ref_desc* d, const ref_cfg* c, void** out) {
     return guard([&] {
         auto ses = std::make_unique<Session>();
         Problem& pr = ses->pr;
-        pr.mesh = std::make_unique<StructuredMesh>(StructuredMesh::rectangle(d->nx, d->ny, d->h, ElementKind::Square));
+        pr.mesh = std::make_unique<StructuredMesh>(
+            StructuredMesh::rectangle(d->nx, d->ny, d->h, d->element_kind ? ElementKind::Triangle : ElementKind::Square));
         pr.space = std::make_unique<FeSpace>(FeSpace::build(*pr.mesh, d->order));
         std::map<Side, BoundaryTag> sides;
         for (int i = 0; i < 4; ++i) sides[kSide[i]] = kTag[d->side[i]];
@@ -247,6 +251,31 @@ int ref_add_coarse_parts(void* h) {
         o.Ac = qsfem::assemble(*o.coarse_space, ccoeffs, ctags);
         o.IP = build_prolongation(space, *o.coarse_space, space.dirichlet_dofs(s->pr.tags),
                                   o.coarse_space->dirichlet_dofs(ctags));
+    });
+}
+
+// The reference element of order p (shape 0 square, 1 lower / 2 upper triangle,
+// basis.cpp:147-219): stiffness and mass (n x n row-major), n returned in *n;
+// with q > 0 also the staged interpolation E (n x npts, fespace.cpp:260-378).
+int ref_element(int p, int shape, int q, double* K, double* M, double* E, int* n, int* npts) {
+    return guard([&] {
+        const ReferenceElement& r = shape == 0 ? ReferenceElement::square(p)
+                                    : shape == 1 ? ReferenceElement::triangle_lower(p)
+                                                 : ReferenceElement::triangle_upper(p);
+        const int nn = r.n_dofs();
+        *n = nn;
+        for (int i = 0; i < nn; ++i)
+            for (int j = 0; j < nn; ++j) {
+                K[i * nn + j] = r.stiffness()(i, j);
+                M[i * nn + j] = r.mass()(i, j);
+            }
+        if (q > 0) {
+            const StageInterp& si = stage_interp(p, shape == 0 ? ElementKind::Square : ElementKind::Triangle,
+                                                 shape == 2 ? 1 : 0, q);
+            *npts = int(si.points.size());
+            for (int i = 0; i < nn; ++i)
+                for (int j = 0; j < *npts; ++j) E[i * *npts + j] = si.E(i, j);
+        }
     });
 }
 

@@ -32,7 +32,11 @@ class Problem(C.Structure):
                 ("k_cells", C.POINTER(C.c_double)), ("eps_cells", C.POINTER(C.c_double)),
                 ("side_tags", C.c_int * 4),
                 ("tags_bottom", C.POINTER(C.c_int)), ("tags_right", C.POINTER(C.c_int)),
-                ("tags_top", C.POINTER(C.c_int)), ("tags_left", C.POINTER(C.c_int))]
+                ("tags_top", C.POINTER(C.c_int)), ("tags_left", C.POINTER(C.c_int)),
+                ("element_kind", C.c_int)]
+
+
+HTG_ELEM_SQUARE, HTG_ELEM_TRIANGLE = 0, 1
 
 
 class Config(C.Structure):

@@ -124,6 +124,16 @@ struct htg_handle {
     std::unique_ptr<CoarseSolver> coarse;
     // GalerkinP: inclusion map (coarse dof -> fine dof, -1 Dirichlet) and A_c (CSR)
     int* cmap = nullptr;
+    // triangle meshes: the residual operators A, A_s and the prolongation IP (and IP^T)
+    // as device CSR (assembled on the host from the triangle elements, tri.cpp)
+    struct Csr {
+        const int* rp = nullptr;
+        const int* ci = nullptr;
+        const double2* v = nullptr;
+        long long n = 0;
+    } tA, tAs, tIP, tIPT;
+    double2* tr = nullptr;    // triangle residual scratch
+    double2* tdot = nullptr;  // one complex scalar
     int *ac_rp = nullptr, *ac_ci = nullptr;
     double2* ac_v = nullptr;
     // ExactShifted smoother: direct solver of the fine shifted operator A_s
@@ -230,6 +240,49 @@ void build_handle(htg_handle* H, const htg_problem& prob, const htg_config& cfg)
     H->dscal = M.alloc<double>(64);
     HTG_CUDA(cudaMallocHost(&H->hscal, 64 * sizeof(double)));
 
+    if (hp.tri) {
+        auto up_csr = [&](const std::vector<int>& rp, const std::vector<int>& ci, const std::vector<double2>& v) {
+            htg_handle::Csr c;
+            c.rp = M.upload(rp, st);
+            c.ci = M.upload(ci, st);
+            c.v = M.upload(v, st);
+            c.n = (long long)rp.size() - 1;
+            return c;
+        };
+        auto lat = [&](double alpha) {
+            const LatticeMatrix L = fe_lattice(hp, H->basis, hp.p, alpha);
+            std::vector<double2> v(L.v.size());
+            for (size_t i = 0; i < v.size(); ++i) v[i] = make_double2(L.v[i].real(), L.v[i].imag());
+            return up_csr(L.rp, L.ci, v);
+        };
+        H->tA = lat(0.0);
+        H->tAs = lat(cfg.alpha_s);
+        H->tr = M.alloc<double2>(H->ndof);
+        H->tdot = M.alloc<double2>(1);
+        if (cfg.coarsening == HTG_COARSE_OPTIMIZED_FD) {
+            std::vector<int> rp, ci;
+            std::vector<double> v;
+            tri_prolongation(hp, rp, ci, v);
+            std::vector<double2> v2(v.size());
+            for (size_t i = 0; i < v.size(); ++i) v2[i] = make_double2(v[i], 0.0);
+            H->tIP = up_csr(rp, ci, v2);
+            // IP^T: coarse rows
+            const long long nc = H->cndof;
+            std::vector<int> trp(size_t(nc) + 1, 0), tci(ci.size());
+            std::vector<double2> tv(ci.size());
+            for (int c : ci) ++trp[size_t(c) + 1];
+            for (long long i = 0; i < nc; ++i) trp[size_t(i) + 1] += trp[size_t(i)];
+            std::vector<int> fill(trp.begin(), trp.end() - 1);
+            for (long long r = 0; r + 1 < (long long)rp.size(); ++r)
+                for (int k = rp[size_t(r)]; k < rp[size_t(r) + 1]; ++k) {
+                    const int at = fill[size_t(ci[size_t(k)])]++;
+                    tci[size_t(at)] = int(r);
+                    tv[size_t(at)] = v2[size_t(k)];
+                }
+            H->tIPT = up_csr(trp, tci, tv);
+        }
+        clk.mark("triangle operators (CSR)");
+    }
     if (cfg.smoother == HTG_SMOOTHER_CSDD) {
         clk.mark("problem, vectors");
         DDSetup dd = build_dd(hp, H->basis, cfg.alpha_s, cfg.l_dd);
@@ -370,6 +423,11 @@ K1Args k1args(htg_handle* H, const double2* f, const double2* u, int shifted) {
 }
 
 void residual(htg_handle* H, const double2* f, const double2* u, double2* r, int shifted) {
+    if (H->hp.tri) {
+        const htg_handle::Csr& A = shifted ? H->tAs : H->tA;
+        csr_launch(1, A.rp, A.ci, A.v, A.n, u, f, 0.0, r, H->st);
+        return;
+    }
     K1Args a = k1args(H, f, u, shifted);
     a.r = r;
     k1_launch(kK1Write, a, H->st);
@@ -377,6 +435,12 @@ void residual(htg_handle* H, const double2* f, const double2* u, double2* r, int
 
 // ||f - A u||^2 into H->dscal[slot] (device)
 void residual_norm2(htg_handle* H, const double2* f, const double2* u, int slot) {
+    if (H->hp.tri) {
+        residual(H, f, u, H->tr, 0);
+        vec_dot(H->tr, H->tr, H->ndof, H->partial, H->tdot, H->st);
+        HTG_CUDA(cudaMemcpyAsync(H->dscal + slot, H->tdot, sizeof(double), cudaMemcpyDeviceToDevice, H->st));
+        return;
+    }
     K1Args a = k1args(H, f, u, 0);
     const int n = k1_launch(kK1Norm, a, H->st);
     reduce_partials(H->partial, n, H->dscal + slot, H->st);
@@ -388,6 +452,11 @@ void residual_restrict(htg_handle* H, const double2* f, const double2* u, double
         inclusion_restrict_launch(H->r, H->cmap, H->cndof, rc, H->st);
         return;
     }
+    if (H->hp.tri) {
+        residual(H, f, u, H->tr, 0);
+        csr_launch(0, H->tIPT.rp, H->tIPT.ci, H->tIPT.v, H->tIPT.n, H->tr, nullptr, 0.0, rc, H->st);
+        return;
+    }
     K1Args a = k1args(H, f, u, 0);
     a.rc = rc;
     k1_launch(kK1Restrict, a, H->st);
@@ -395,6 +464,7 @@ void residual_restrict(htg_handle* H, const double2* f, const double2* u, double
 
 void prolong_add(htg_handle* H, double2* u, const double2* uc, double omega) {
     if (H->cfg.coarsening == HTG_COARSE_GALERKIN_P) inclusion_prolong_launch(u, H->cmap, H->cndof, uc, omega, H->st);
+    else if (H->hp.tri) csr_launch(2, H->tIP.rp, H->tIP.ci, H->tIP.v, H->tIP.n, uc, nullptr, omega, u, H->st);
     else prolong_add_launch(H->g, u, uc, omega, H->st);
 }
 

@@ -188,7 +188,29 @@ LatticeMatrix fe_lattice(const HostProblem& hp, const Basis1D& b, int q, double 
     std::vector<std::vector<std::pair<int, cplx>>> rows(nv);
     auto dof = [&](int cx, int cy, int a, int c) { return L.id[(cy * q + off(c)) * L.W + cx * q + off(a)]; };
     const double h2 = hp.h * hp.h;
-    for (int cy = 0; cy < hp.ny; ++cy)
+    if (hp.tri) {  // two order-q triangles per cell (tri.cpp), rows in the same lattice numbering
+        for (int sub = 0; sub < 2; ++sub) {
+            const TriElement& T = tri_element(q, sub);
+            for (int cy = 0; cy < hp.ny; ++cy)
+                for (int cx = 0; cx < hp.nx; ++cx) {
+                    const double k = hp.kc(cx, cy), e = hp.ec(cx, cy);
+                    const cplx m = cplx(k * k, k * k * alpha + e) * h2;
+                    std::vector<int> gd(T.n);
+                    for (int i = 0; i < T.n; ++i) {
+                        const auto& pl = T.place[i];
+                        gd[i] = L.id[((cy + pl[1]) * q + pl[3]) * L.W + (cx + pl[0]) * q + pl[2]];
+                    }
+                    for (int i = 0; i < T.n; ++i) {
+                        auto& row = rows[gd[i]];
+                        for (int j = 0; j < T.n; ++j) {
+                            const cplx a = T.K[size_t(i) * T.n + j] - m * T.M[size_t(i) * T.n + j];
+                            if (a != cplx(0.0)) row.push_back({gd[j], a});
+                        }
+                    }
+                }
+        }
+    }
+    for (int cy = 0; cy < (hp.tri ? 0 : hp.ny); ++cy)
         for (int cx = 0; cx < hp.nx; ++cx) {
             const double k = hp.kc(cx, cy), e = hp.ec(cx, cy);
             const cplx m = cplx(k * k, k * k * alpha + e) * h2;

@@ -211,6 +211,7 @@ bool fdm_supported(int p, int nx, int ny) {
 
 bool build_fdm(const HostProblem& hp, const Basis1D& b, double alpha_s, int ox, int oy, DDClass& c) {
     const int p = hp.p;
+    if (hp.tri) return false;  // triangle elements are not tensor products
     // separable: one (k, eps) in Omega, no Dirichlet side
     const double k0 = hp.kc(ox, oy), e0 = hp.ec(ox, oy);
     for (int y = oy; y < oy + c.ony; ++y)

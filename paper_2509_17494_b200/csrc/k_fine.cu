@@ -1365,6 +1365,42 @@ __global__ void k_incl_prolong(double2* __restrict__ u, const int* __restrict__ 
     }
 }
 // one warp-quarter (8 lanes) per row
+// complex CSR product, 8 lanes per row: MODE 0 y = A x, 1 y = f - A x (the residual
+// of an assembled operator: triangle elements), 2 y += omega A x (a CSR prolongation)
+template <int MODE>
+__global__ void k_csr(const int* __restrict__ rp, const int* __restrict__ ci, const double2* __restrict__ v,
+                      long long n, const double2* __restrict__ x, const double2* __restrict__ f, double omega,
+                      double2* __restrict__ y) {
+    const long long row = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 3;
+    const int l = threadIdx.x & 7;
+    double re = 0.0, im = 0.0;
+    if (row < n)
+        for (int k = rp[row] + l; k < rp[row + 1]; k += 8) {
+            const double2 a = v[k], b = x[ci[k]];
+            re = fma(a.x, b.x, fma(-a.y, b.y, re));
+            im = fma(a.x, b.y, fma(a.y, b.x, im));
+        }
+#pragma unroll
+    for (int o = 4; o; o >>= 1) {
+        re += __shfl_xor_sync(0xffffffffu, re, o);
+        im += __shfl_xor_sync(0xffffffffu, im, o);
+    }
+    if (row < n && l == 0) {
+        if (MODE == 0) y[row] = make_double2(re, im);
+        else if (MODE == 1) y[row] = make_double2(f[row].x - re, f[row].y - im);
+        else y[row] = make_double2(fma(omega, re, y[row].x), fma(omega, im, y[row].y));
+    }
+}
+void csr_launch(int mode, const int* rp, const int* ci, const double2* v, long long n, const double2* x,
+                const double2* f, double omega, double2* y, cudaStream_t st) {
+    const unsigned nb = unsigned((n * 8 + 255) / 256);
+    if (mode == 0) k_csr<0><<<nb, 256, 0, st>>>(rp, ci, v, n, x, f, omega, y);
+    else if (mode == 1) k_csr<1><<<nb, 256, 0, st>>>(rp, ci, v, n, x, f, omega, y);
+    else k_csr<2><<<nb, 256, 0, st>>>(rp, ci, v, n, x, f, omega, y);
+    HTG_CUDA(cudaGetLastError());
+    count_launch();
+}
+
 __global__ void k_csr_apply(const int* __restrict__ rp, const int* __restrict__ ci, const double2* __restrict__ v,
                             long long n, const double2* __restrict__ x, double2* __restrict__ y) {
     const long long row = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 3;

@@ -49,6 +49,10 @@ void csr_apply_launch(const int* rp, const int* ci, const double2* v, long long 
 // timing only: read `bytes` of buf (evicts and writes back dirty L2 lines)
 void l2_read(const void* buf, size_t bytes, double* sink, cudaStream_t st);
 
+// complex CSR: mode 0 y = A x, 1 y = f - A x, 2 y += omega A x
+void csr_launch(int mode, const int* rp, const int* ci, const double2* v, long long n, const double2* x,
+                const double2* f, double omega, double2* y, cudaStream_t st);
+
 // vectors
 void vec_axpy(double2* y, const double2* x, double a, long long n, cudaStream_t st);  // y += a x
 void vec_copy(double2* y, const double2* x, long long n, cudaStream_t st);

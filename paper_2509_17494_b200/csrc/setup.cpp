@@ -1,6 +1,7 @@
 // setup.cpp -- host setup: 1-D basis factors, problem tables, subdomain classes.
 #include "setup.hpp"
 #include "kernels.hpp"
+#include "coarse.hpp"
 
 #include <algorithm>
 #include <cmath>
@@ -150,6 +151,9 @@ HostProblem make_problem(const htg_problem& pr) {
     if (pr.nx < 1 || pr.ny < 1) throw InvalidArgument("rectangle: cell counts must be >= 1");
     if (!(pr.h > 0.0)) throw InvalidArgument("rectangle: spacing must be positive");
     hp.p = pr.order;
+    if (pr.element_kind != HTG_ELEM_SQUARE && pr.element_kind != HTG_ELEM_TRIANGLE)
+        throw InvalidArgument("unknown element kind");
+    hp.tri = pr.element_kind == HTG_ELEM_TRIANGLE;
     hp.nx = pr.nx;
     hp.ny = pr.ny;
     hp.h = pr.h;
@@ -216,6 +220,8 @@ void validate_config(const htg_config& c, const HostProblem& hp) {
     if (c.smoother != HTG_SMOOTHER_CSDD && c.smoother != HTG_SMOOTHER_EXACT_SHIFTED)
         throw InvalidArgument("unknown smoother");
     if (c.outer != HTG_OUTER_RICHARDSON && c.outer != HTG_OUTER_KRYLOV) throw InvalidArgument("unknown outer iteration");
+    if (hp.tri && c.coarsening == HTG_COARSE_GALERKIN_P)
+        throw InvalidArgument("GalerkinP coarsening is implemented for square elements only");
     if (c.coarsening == HTG_COARSE_OPTIMIZED_FD) {
         const double hc = 2.0 * hp.h / hp.p;
         for (double k : hp.cls_k) {
@@ -285,8 +291,15 @@ struct ClassKey {
 // reference numbering: element tensor products, Robin on absorbing Omega edges
 // (internal edges are absorbing, outer edges inherit; twogrid.cpp:80-86),
 // Dirichlet rows/columns -> identity (fespace.cpp:246-258).
+void assemble_omega_tri(const HostProblem& hp, const Basis1D& b, double alpha, int ox, int oy, int onx, int ony,
+                        std::vector<cplx>& A, int& n);
+
 void assemble_omega(const HostProblem& hp, const Basis1D& b, double alpha, int ox, int oy, int onx, int ony,
                     std::vector<cplx>& A, int& n) {
+    if (hp.tri) {
+        assemble_omega_tri(hp, b, alpha, ox, oy, onx, ony, A, n);
+        return;
+    }
     const int p = hp.p;
     n = int(dof_index(onx, ony, p, onx * p, ony * p)) + 1;
     A.assign(size_t(n) * n, cplx(0.0));
@@ -352,6 +365,47 @@ void assemble_omega(const HostProblem& hp, const Basis1D& b, double alpha, int o
         }
         A[size_t(i) * n + i] = 1.0;
     }
+}
+
+// Triangle meshes: A_s on Omega is the FE matrix of the Omega rectangle as a
+// problem of its own (fe_lattice, triangle branch): its cells' k and eps,
+// outer edges inheriting the global tags and k h, internal Omega edges
+// absorbing with the k of the Omega cell on them (twogrid.cpp:80-86).
+void assemble_omega_tri(const HostProblem& hp, const Basis1D& b, double alpha, int ox, int oy, int onx, int ony,
+                        std::vector<cplx>& A, int& n) {
+    HostProblem s;
+    s.p = hp.p;
+    s.tri = true;
+    s.nx = onx;
+    s.ny = ony;
+    s.h = hp.h;
+    for (int y = 0; y < ony; ++y)
+        for (int x = 0; x < onx; ++x) {
+            s.k.push_back(hp.kc(ox + x, oy + y));
+            s.eps.push_back(hp.ec(ox + x, oy + y));
+        }
+    auto side = [&](bool outer, int8_t tg, double khg, double kcell, std::vector<int8_t>& T, std::vector<double>& K) {
+        const int8_t t = outer ? tg : kAbsorbing;
+        T.push_back(t);
+        K.push_back(t == kAbsorbing ? (outer ? khg : kcell * hp.h) : 0.0);
+        s.has_dirichlet |= t == kDirichlet;
+    };
+    for (int i = 0; i < onx; ++i) {
+        side(oy == 0, oy == 0 ? hp.tb[ox + i] : kAbsorbing, oy == 0 ? hp.khb[ox + i] : 0.0, hp.kc(ox + i, oy), s.tb, s.khb);
+        const bool top = oy + ony == hp.ny;
+        side(top, top ? hp.tt[ox + i] : kAbsorbing, top ? hp.kht[ox + i] : 0.0, hp.kc(ox + i, oy + ony - 1), s.tt, s.kht);
+    }
+    for (int i = 0; i < ony; ++i) {
+        side(ox == 0, ox == 0 ? hp.tl[oy + i] : kAbsorbing, ox == 0 ? hp.khl[oy + i] : 0.0, hp.kc(ox, oy + i), s.tl, s.khl);
+        const bool right = ox + onx == hp.nx;
+        side(right, right ? hp.tr[oy + i] : kAbsorbing, right ? hp.khr[oy + i] : 0.0, hp.kc(ox + onx - 1, oy + i), s.tr,
+             s.khr);
+    }
+    const LatticeMatrix L = fe_lattice(s, b, hp.p, alpha);
+    n = int(s.ndof());
+    A.assign(size_t(n) * n, cplx(0.0));
+    for (int i = 0; i < n; ++i)
+        for (int k = L.rp[i]; k < L.rp[i + 1]; ++k) A[size_t(i) * n + L.ci[k]] = L.v[k];
 }
 
 }  // namespace
@@ -436,7 +490,7 @@ DDSetup build_dd(const HostProblem& hp, const Basis1D& b, double alpha_s, int l_
                             varies = true;
                             break;
                         }
-                dd.classes[ci].band = varies && members[ci] <= band_max;
+                dd.classes[ci].band = !hp.tri && varies && members[ci] <= band_max;  // the device assembly is for squares
             }
     }
     // restricted inverses, one per class (threads over classes)

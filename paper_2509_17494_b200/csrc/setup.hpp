@@ -1,7 +1,9 @@
 // setup.hpp -- host-side setup of the two-grid operators (runs once per handle).
 #pragma once
 
+#include <array>
 #include <complex>
+#include <map>
 #include <memory>
 #include <vector>
 
@@ -28,9 +30,29 @@ struct Basis1D {
 };
 Basis1D make_basis(int p);
 
+// Order-p triangle element of the reference's split square cell (tri.cpp):
+// sub 0 lower {y <= x}, sub 1 upper {y >= x}, dofs in the reference element
+// order (proj/core/src/fespace.cpp:85-108). place[i] = (dx, dy, jx, jy): element
+// dof i lives in unit cell (x + dx, y + dy) at the lattice offset (jx, jy) of
+// the square dof occupying the same unit-cell slot. E (n x npts) is the staged
+// interpolation from the q = p/2 coarse lattice points stage_pts (offsets in
+// coarse vertices from the cell origin), fespace.cpp:260-378.
+struct TriElement {
+    int p = 0, n = 0, npts = 0;
+    std::vector<double> K, M;  // n x n, unit-cell scale (the mass scales with h^2)
+    std::vector<std::array<int, 4>> place;
+    std::vector<double> E;
+    std::vector<std::array<int, 2>> stage_pts;
+};
+const TriElement& tri_element(int p, int sub);
+struct HostProblem;
+// IP (fine dofs x coarse vertices) of a triangle mesh as CSR (tri.cpp)
+void tri_prolongation(const HostProblem& hp, std::vector<int>& rp, std::vector<int>& ci, std::vector<double>& v);
+
 // Validated copy of the C-ABI problem plus per-cell / per-edge tables.
 struct HostProblem {
     int p = 0, nx = 0, ny = 0;
+    bool tri = false;  // triangle elements (each cell split along its (0,0)-(1,1) diagonal)
     double h = 0.0;
     std::vector<double> k, eps;           // per cell, (y, x) order
     std::vector<int8_t> tb, tt, tl, tr;   // tags per boundary edge

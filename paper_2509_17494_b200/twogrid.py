@@ -25,6 +25,7 @@ from ._lib import HtgError, check, lib
 DIRICHLET, NEUMANN, ABSORBING = 0, 1, 2
 LEFT, RIGHT, BOTTOM, TOP = 0, 1, 2, 3
 OPTIMIZED_FD, GALERKIN_P, NONE = 0, 1, 2
+SQUARE, TRIANGLE = 0, 1  # element kinds (proj/core/include/helmtg/mesh.hpp ElementKind)
 CSDD, EXACT_SHIFTED = 0, 1
 RICHARDSON, KRYLOV = 0, 1
 
@@ -58,6 +59,7 @@ class ProblemSpec:
     layer_sides: tuple = ()
     layer_width_dofs: float = 40.0
     damping_D: float = 0.0
+    element_kind: int = 0  # SQUARE (0) or TRIANGLE (1)
 
 
 @dataclass
@@ -72,6 +74,7 @@ class Problem:
     side_tags: tuple
     rhs: np.ndarray = field(repr=False)
     ny: int | None = None  # cells in y (None: n_cells, the unit square of build_problem)
+    element_kind: int = 0  # SQUARE, or TRIANGLE: cells split along the (0,0)-(1,1) diagonal
 
     @property
     def ndof(self) -> int:
@@ -134,7 +137,7 @@ def build_problem(spec: ProblemSpec) -> Problem:
     tags = tuple(spec.side_tags)
     if DIRICHLET in tags:
         rhs[dirichlet_mask(n, n, p, tags)] = 0.0
-    return Problem(p, n, h, k, kc, ec, tags, rhs)
+    return Problem(p, n, h, k, kc, ec, tags, rhs, element_kind=spec.element_kind)
 
 
 def dirichlet_mask(nx: int, ny: int, p: int, side_tags) -> np.ndarray:
@@ -198,7 +201,7 @@ class TwoGridOperators:
         cp = _lib.Problem(problem.order, n, problem.ny or n, problem.h, problem.k, 0.0,
                           self._k.ctypes.data_as(C.POINTER(C.c_double)),
                           self._e.ctypes.data_as(C.POINTER(C.c_double)),
-                          (C.c_int * 4)(*problem.side_tags), None, None, None, None)
+                          (C.c_int * 4)(*problem.side_tags), None, None, None, None, int(problem.element_kind))
         cfg = config._c()
         h = C.c_void_p()
         import torch

@@ -24,6 +24,24 @@ void matvec_sub(const std::vector<cplx>& M, int rows, int cols, const cplx* x, c
 
 extern "C" {
 
+// The product's triangle element (csrc/tri.cpp): K, M (n x n), E (n x npts) and
+// the lattice placement (4 ints per dof).
+int nd_tri_element(int p, int sub, double* K, double* M, double* E, int* place, int* n, int* npts) {
+    try {
+        const htg::TriElement& T = htg::tri_element(p, sub);
+        *n = T.n;
+        *npts = T.npts;
+        std::memcpy(K, T.K.data(), T.K.size() * sizeof(double));
+        std::memcpy(M, T.M.data(), T.M.size() * sizeof(double));
+        std::memcpy(E, T.E.data(), T.E.size() * sizeof(double));
+        for (int i = 0; i < T.n; ++i)
+            for (int c = 0; c < 4; ++c) place[4 * i + c] = T.place[i][c];
+        return 0;
+    } catch (const std::exception&) {
+        return 1;
+    }
+}
+
 // A9 stencil rows of the coarse matrix (nv * 9 complex = 18 doubles per vertex).
 int nd_stencil(const htg_problem* prob, double* a9, long long cap) {
     try {

@@ -22,8 +22,9 @@ def _cproblem(problem):
     k = np.ascontiguousarray(problem.k_cells, dtype=np.float64)
     e = np.ascontiguousarray(problem.eps_cells, dtype=np.float64)
     n = problem.n_cells
-    cp = hl.Problem(problem.order, n, n, problem.h, problem.k, 0.0, k.ctypes.data_as(C.POINTER(C.c_double)),
-                    e.ctypes.data_as(C.POINTER(C.c_double)), (C.c_int * 4)(*problem.side_tags), None, None, None, None)
+    cp = hl.Problem(problem.order, n, problem.ny or n, problem.h, problem.k, 0.0,
+                    k.ctypes.data_as(C.POINTER(C.c_double)), e.ctypes.data_as(C.POINTER(C.c_double)),
+                    (C.c_int * 4)(*problem.side_tags), None, None, None, None, int(problem.element_kind))
     return cp, (k, e)
 
 
