@@ -134,6 +134,8 @@ struct htg_handle {
     } tA, tAs, tIP, tIPT;
     double2* tr = nullptr;    // triangle residual scratch
     double2* tdot = nullptr;  // one complex scalar
+    const double* tKM = nullptr;  // combined cell operator [K_c | M_c] (matrix-free triangle residual)
+    bool tri_csr = false;         // HTG_TRI_CSR=1: residual from the assembled CSR instead
     int *ac_rp = nullptr, *ac_ci = nullptr;
     double2* ac_v = nullptr;
     // ExactShifted smoother: direct solver of the fine shifted operator A_s
@@ -255,8 +257,29 @@ void build_handle(htg_handle* H, const htg_problem& prob, const htg_config& cfg)
             for (size_t i = 0; i < v.size(); ++i) v[i] = make_double2(L.v[i].real(), L.v[i].imag());
             return up_csr(L.rp, L.ci, v);
         };
-        H->tA = lat(0.0);
-        H->tAs = lat(cfg.alpha_s);
+        {  // the two triangles of a cell as one (p+1)^2 operator over the cell's lattice nodes
+            const int B = hp.p + 1, NB = B * B;
+            std::vector<double> km(size_t(2) * NB * NB, 0.0);
+            for (int sub = 0; sub < 2; ++sub) {
+                const TriElement& T = tri_element(hp.p, sub);
+                auto lc = [&](int i) {
+                    const auto& pl = T.place[i];
+                    return (pl[1] * hp.p + pl[3]) * B + pl[0] * hp.p + pl[2];
+                };
+                for (int i = 0; i < T.n; ++i)
+                    for (int j = 0; j < T.n; ++j) {
+                        km[size_t(lc(i)) * NB + lc(j)] += T.K[size_t(i) * T.n + j];
+                        km[size_t(NB) * NB + size_t(lc(i)) * NB + lc(j)] += T.M[size_t(i) * T.n + j];
+                    }
+            }
+            H->tKM = M.upload(km, st);
+        }
+        const char* tc = std::getenv("HTG_TRI_CSR");
+        H->tri_csr = tc && tc[0] == '1';
+        if (H->tri_csr) {
+            H->tA = lat(0.0);
+            H->tAs = lat(cfg.alpha_s);
+        }
         H->tr = M.alloc<double2>(H->ndof);
         H->tdot = M.alloc<double2>(1);
         if (cfg.coarsening == HTG_COARSE_OPTIMIZED_FD) {
@@ -424,8 +447,12 @@ K1Args k1args(htg_handle* H, const double2* f, const double2* u, int shifted) {
 
 void residual(htg_handle* H, const double2* f, const double2* u, double2* r, int shifted) {
     if (H->hp.tri) {
-        const htg_handle::Csr& A = shifted ? H->tAs : H->tA;
-        csr_launch(1, A.rp, A.ci, A.v, A.n, u, f, 0.0, r, H->st);
+        if (H->tri_csr) {
+            const htg_handle::Csr& A = shifted ? H->tAs : H->tA;
+            csr_launch(1, A.rp, A.ci, A.v, A.n, u, f, 0.0, r, H->st);
+        } else {
+            tri_residual_launch(H->g, H->tKM, u, f, r, shifted, H->st);
+        }
         return;
     }
     K1Args a = k1args(H, f, u, shifted);

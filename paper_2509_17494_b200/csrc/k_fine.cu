@@ -1178,6 +1178,143 @@ void reduce_partials(const double* partial, int n, double* out, cudaStream_t st)
     count_launch();
 }
 
+// ---------------------------------------------------------------- K1 (triangles)
+// Matrix-free residual on triangle meshes: the two P_p triangles of a cell
+// combine into one (p+1)^2 x (p+1)^2 cell operator K_c - m M_c over the cell's
+// lattice nodes (tri.cpp places every triangle dof on the lattice), so a CTA
+// stages the u values of a tile of cells plus a one-cell halo in shared memory
+// and every thread gathers the rows of the lattice nodes it owns from the 1, 2
+// or 4 cells containing the node. Robin rows: -i k h times the 1-D edge mass
+// (fespace.cpp:198-203); Dirichlet rows r = f - u, Dirichlet columns dropped
+// (fespace.cpp:246-258). K_c, M_c (basis-independent, unit-cell scale) come from
+// tri.cpp via the handle.
+constexpr int kTriTile = 8;  // cells per tile side
+template <int P>
+__global__ void __launch_bounds__(256) k_tri_residual(FineGeom g, const double* __restrict__ KMc,
+                                                      const double2* __restrict__ u, const double2* __restrict__ f,
+                                                      double2* __restrict__ r, int shifted) {
+    constexpr int B = P + 1, NB = B * B, T = kTriTile, SW = (T + 2) * P + 1;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* sK = reinterpret_cast<double*>(smem_raw);  // NB x NB
+    double* sM = sK + NB * NB;
+    double2* su = reinterpret_cast<double2*>(sM + NB * NB);  // SW x SW lattice nodes (zero outside / Dirichlet)
+    double2* sm = su + SW * SW;                              // (T + 2)^2 cell weights m
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int cx0 = blockIdx.x * T, cy0 = blockIdx.y * T;
+    const int gx0 = (cx0 - 1) * P, gy0 = (cy0 - 1) * P;  // lattice origin of the staged window
+    const int NGx = g.nx * P, NGy = g.ny * P;
+    for (int i = tid; i < NB * NB; i += nt) {
+        sK[i] = KMc[i];
+        sM[i] = KMc[NB * NB + i];
+    }
+    const double2* mt = shifted ? g.mtabS : g.mtab0;
+    for (int i = tid; i < (T + 2) * (T + 2); i += nt) {
+        const int cx = cx0 - 1 + i % (T + 2), cy = cy0 - 1 + i / (T + 2);
+        sm[i] = (cx >= 0 && cx < g.nx && cy >= 0 && cy < g.ny) ? mt[g.cls ? g.cls[(size_t)cy * g.nx + cx] : 0]
+                                                                 : make_double2(0.0, 0.0);
+    }
+    for (int i = tid; i < SW * SW; i += nt) {
+        const int gx = gx0 + i % SW, gy = gy0 + i / SW;
+        double2 v = make_double2(0.0, 0.0);
+        if (gx >= 0 && gx <= NGx && gy >= 0 && gy <= NGy && !(g.has_dirichlet && fine_dir<P>(g, gx, gy)))
+            v = u[dofp<P>(g.nx, g.ny, gx, gy)];
+        su[i] = v;
+    }
+    __syncthreads();
+    // owned nodes: lattice lines [cx0 P, (cx0 + T) P) (+ the last line on the mesh edge)
+    const int ox1 = min((cx0 + T) * P, NGx) + ((cx0 + T) * P >= NGx ? 1 : 0);
+    const int oy1 = min((cy0 + T) * P, NGy) + ((cy0 + T) * P >= NGy ? 1 : 0);
+    const int OW = ox1 - cx0 * P, OH = oy1 - cy0 * P;
+    for (int e = tid; e < OW * OH; e += nt) {
+        const int gx = cx0 * P + e % OW, gy = cy0 * P + e / OW;
+        const long long d = dofp<P>(g.nx, g.ny, gx, gy);
+        if (g.has_dirichlet && fine_dir<P>(g, gx, gy)) {  // identity row
+            const double2 uv = u[d], fv = f[d];
+            r[d] = make_double2(fv.x - uv.x, fv.y - uv.y);
+            continue;
+        }
+        const int x = gx / P, jx = gx - x * P, y = gy / P, jy = gy - y * P;
+        double2 acc = make_double2(0.0, 0.0);
+        for (int cy = (jy ? y : y - 1); cy <= y; ++cy) {
+            if (cy < 0 || cy >= g.ny) continue;
+            for (int cx = (jx ? x : x - 1); cx <= x; ++cx) {
+                if (cx < 0 || cx >= g.nx) continue;
+                const int lx = gx - cx * P, ly = gy - cy * P, lc = ly * B + lx;
+                const double* Kr = sK + lc * NB;
+                const double* Mr = sM + lc * NB;
+                const double2* ub = su + (cy * P - gy0) * SW + (cx * P - gx0);
+                double2 ku = make_double2(0.0, 0.0), mu = ku;
+#pragma unroll 5
+                for (int j = 0; j < NB; ++j) {
+                    const double2 uv = ub[(j / B) * SW + j % B];
+                    ku.x = fma(Kr[j], uv.x, ku.x);
+                    ku.y = fma(Kr[j], uv.y, ku.y);
+                    mu.x = fma(Mr[j], uv.x, mu.x);
+                    mu.y = fma(Mr[j], uv.y, mu.y);
+                }
+                const double2 m = sm[(cy - cy0 + 1) * (T + 2) + (cx - cx0 + 1)];
+                acc.x += ku.x - (m.x * mu.x - m.y * mu.y);
+                acc.y += ku.y - (m.x * mu.y + m.y * mu.x);
+            }
+        }
+        // Robin: -i k h M1 along absorbing boundary edges containing the node
+        auto edge = [&](double kh, bool horiz, int c, int line) {
+            if (kh == 0.0) return;
+            const int l = (horiz ? gx : gy) - c * P;  // 1-D position in the edge
+            const int bl = l == 0 ? 0 : (l == P ? 1 : l + 1);
+            double2 s = make_double2(0.0, 0.0);
+            for (int t = 0; t <= P; ++t) {
+                const int bt = t == 0 ? 0 : (t == P ? 1 : t + 1);
+                const double mv = c_M[P / 2 - 1][bl][bt];
+                if (mv == 0.0) continue;
+                const int nx_ = horiz ? c * P + t : line, ny_ = horiz ? line : c * P + t;
+                const double2 uv = su[(ny_ - gy0) * SW + (nx_ - gx0)];
+                s.x = fma(mv, uv.x, s.x);
+                s.y = fma(mv, uv.y, s.y);
+            }
+            acc = cadd(acc, mik(kh, s));
+        };
+        if (gy == 0 || gy == NGy) {
+            const double* kh = gy == 0 ? g.kh_b : g.kh_t;
+            for (int c = (jx ? x : x - 1); c <= x; ++c)
+                if (c >= 0 && c < g.nx) edge(kh[c], true, c, gy);
+        }
+        if (gx == 0 || gx == NGx) {
+            const double* kh = gx == 0 ? g.kh_l : g.kh_r;
+            for (int c = (jy ? y : y - 1); c <= y; ++c)
+                if (c >= 0 && c < g.ny) edge(kh[c], false, c, gx);
+        }
+        const double2 fv = f[d];
+        r[d] = make_double2(fv.x - acc.x, fv.y - acc.y);
+    }
+}
+
+size_t tri_residual_smem(int p) {
+    const int B = p + 1, NB = B * B, SW = (kTriTile + 2) * p + 1;
+    return size_t(2 * NB * NB) * sizeof(double) + size_t(SW * SW + (kTriTile + 2) * (kTriTile + 2)) * sizeof(double2);
+}
+void tri_residual_launch(const FineGeom& g, const double* KMc, const double2* u, const double2* f, double2* r,
+                         int shifted, cudaStream_t st) {
+    const dim3 grid(unsigned((g.nx + kTriTile - 1) / kTriTile), unsigned((g.ny + kTriTile - 1) / kTriTile));
+    const size_t sm = tri_residual_smem(g.p);
+    static bool attr[9] = {};
+    auto go = [&](auto kern, int p) {
+        if (!attr[p]) {
+            HTG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
+            attr[p] = true;
+        }
+        kern<<<grid, 256, sm, st>>>(g, KMc, u, f, r, shifted);
+    };
+    switch (g.p) {
+        case 2: go(k_tri_residual<2>, 2); break;
+        case 4: go(k_tri_residual<4>, 4); break;
+        case 6: go(k_tri_residual<6>, 6); break;
+        default: go(k_tri_residual<8>, 8); break;
+    }
+    HTG_CUDA(cudaGetLastError());
+    count_launch();
+}
+
 // ---------------------------------------------------------------- K3b
 // u += omega IP uc, IP = (P1 (x) P1) restricted to the nonzero rows: per unit
 // cell the dofs with jx, jy < m (vertex and degree <= m bubbles); rows of fine

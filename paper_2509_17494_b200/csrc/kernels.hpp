@@ -32,6 +32,12 @@ int k1_launch(int mode, const K1Args& a, cudaStream_t st);
 int k1_partials(const FineGeom& g, int rows);
 void reduce_partials(const double* partial, int n, double* out, cudaStream_t st);
 
+// K1 on triangle meshes: r = f - A u (A_s when shifted) from the combined cell
+// operator KMc = [K_c | M_c] ((p+1)^2 x (p+1)^2 each, lattice-node order)
+void tri_residual_launch(const FineGeom& g, const double* KMc, const double2* u, const double2* f, double2* r,
+                         int shifted, cudaStream_t st);
+size_t tri_residual_smem(int p);
+
 // K3b: u += omega IP uc
 void prolong_add_launch(const FineGeom& g, double2* u, const double2* uc, double omega, cudaStream_t st);
 // K4: y = A_c x (QSFEM)
