@@ -364,9 +364,26 @@ void build_handle(htg_handle* H, const htg_problem& prob, const htg_config& cfg)
         std::vector<int> map(size_t(H->cndof), -1);
         const std::vector<char> fdir = fe_dirichlet(hp, hp.p), cdir = fe_dirichlet(hp, q);
         const int Wf = hp.nx * hp.p + 1;
+        // triangles: a unit-cell slot of the order-q lattice -> the slot of the same
+        // function in the order-p unit (diagonal-edge and degree-major bubble offsets
+        // carry over, twogrid.cpp:205-210), then its order-p lattice position
+        auto tri_slot = [&](int jx, int jy, int& fx, int& fy) {
+            if (jx == 0 || jy == 0) {
+                fx = jx;
+                fy = jy;
+                return;
+            }
+            const int i = (jx - 1) * (q - 1) + (jy - 1), niq = (q - 1) * (q - 2) / 2,
+                      nip = (hp.p - 1) * (hp.p - 2) / 2;
+            const int fi = i < q - 1 ? i : (i < q - 1 + niq ? (hp.p - 1) + (i - (q - 1)) : (hp.p - 1) + nip + (i - (q - 1) - niq));
+            fx = 1 + fi / (hp.p - 1);
+            fy = 1 + fi % (hp.p - 1);
+        };
         for (int Y = 0; Y < Ac.H; ++Y)
             for (int X = 0; X < Ac.W; ++X) {
-                const int gx = X / q * hp.p + X % q, gy = Y / q * hp.p + Y % q;  // same function, order-p index
+                int jx = X % q, jy = Y % q;
+                if (hp.tri) tri_slot(X % q, Y % q, jx, jy);
+                const int gx = X / q * hp.p + jx, gy = Y / q * hp.p + jy;  // same function, order-p index
                 if (cdir[Y * Ac.W + X] || fdir[size_t(gy) * Wf + gx]) continue;
                 map[Ac.id[Y * Ac.W + X]] = int(dof_index(hp.nx, hp.ny, hp.p, gx, gy));
             }

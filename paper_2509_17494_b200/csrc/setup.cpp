@@ -220,8 +220,6 @@ void validate_config(const htg_config& c, const HostProblem& hp) {
     if (c.smoother != HTG_SMOOTHER_CSDD && c.smoother != HTG_SMOOTHER_EXACT_SHIFTED)
         throw InvalidArgument("unknown smoother");
     if (c.outer != HTG_OUTER_RICHARDSON && c.outer != HTG_OUTER_KRYLOV) throw InvalidArgument("unknown outer iteration");
-    if (hp.tri && c.coarsening == HTG_COARSE_GALERKIN_P)
-        throw InvalidArgument("GalerkinP coarsening is implemented for square elements only");
     if (c.coarsening == HTG_COARSE_OPTIMIZED_FD) {
         const double hc = 2.0 * hp.h / hp.p;
         for (double k : hp.cls_k) {

@@ -24,6 +24,10 @@ CASES = {
     "p6_abs_krylov": (dict(order=6, wavelengths=3, ppw=8), dict(outer=1)),
     "p8_dir": (dict(order=8, wavelengths=2, ppw=8, side_tags=(A_, D_, A_, D_)), dict()),
     "p4_exact_krylov": (dict(order=4, wavelengths=3, ppw=10), dict(smoother=1, outer=1)),
+    "p4_galerkin_dir": (dict(order=4, wavelengths=3, ppw=10, side_tags=(D_, A_, A_, A_)),
+                        dict(coarsening=1, alpha_s=0.02, alpha_c=0.02)),
+    "p6_galerkin_exact": (dict(order=6, wavelengths=2, ppw=8), dict(coarsening=1, alpha_c=0.05, smoother=1, outer=1)),
+    "p8_galerkin": (dict(order=8, wavelengths=2, ppw=8, side_tags=(A_, N_, D_, A_)), dict(coarsening=1, alpha_c=0.1)),
 }
 
 
@@ -115,14 +119,3 @@ def test_triangles_rectangle_heterogeneous(ref_lib):
     ops.two_grid_step(ud, d(f))
     assert rel(ud.cpu().numpy(), ref.two_grid_step(u, f)) <= TOL
     ops.close()
-
-
-def test_triangles_reject_galerkin():
-    torch = pytest.importorskip("torch")
-    if not torch.cuda.is_available():
-        pytest.skip("no CUDA device")
-    import paper_2509_17494_b200 as hb
-    prob = hb.build_problem(hb.ProblemSpec(order=4, wavelengths=2, ppw=8, element_kind=1))
-    with pytest.raises(hb.HtgError) as e:
-        hb.setup_two_grid(prob, hb.SolverConfig(coarsening=1))
-    assert e.value.code == 2
