@@ -99,7 +99,8 @@ int htg_destroy(htg_handle* h);
  * [14] sum of |U_i| (values staged per sweep), [15] sum of |Omega_i| (values
  * gathered per sweep), [16] algorithmic bytes one coarse solve reads,
  * [17] subdomains with their own device-factored solver (no shared factor),
- * [18] bytes of those factors. out must hold 19 entries. */
+ * [18] bytes of those factors, [19] dense-path subdomain classes whose explicit
+ * restricted inverse was computed on the device. out must hold 20 entries. */
 int htg_info(const htg_handle* h, long long* out);
 int htg_set_stream(htg_handle* h, void* stream);
 

@@ -31,7 +31,7 @@ long long launch_count();
 void reset_launch_count();
 DDDevice upload_dd_impl(const DDSetup& dd, const HostProblem& hp, std::vector<void*>& allocs, size_t& bytes,
                         cudaStream_t st, double2*& ystage, std::vector<FdmClassDev>& fdm,
-                        std::vector<BandSubdomain>& band);
+                        std::vector<BandSubdomain>& band, std::vector<BandInvJob>& jobs);
 }  // namespace htg
 
 using namespace htg;
@@ -114,6 +114,7 @@ struct htg_handle {
     FdmLaunch fdm_launch{};
     BandLaunch band{};            // subdomains without a shared factor (device-factored)
     long long band_subs = 0;
+    int devb_classes = 0;         // dense-path classes whose B_c was computed on the device
     double fdm_err = 0.0;
     int nclasses = 0;
     double dd_flops = 0.0;        // algorithmic flops of one sweep's subdomain solves (path used)
@@ -332,13 +333,16 @@ void build_handle(htg_handle* H, const htg_problem& prob, const htg_config& cfg)
             }
         }
         std::vector<BandSubdomain> bandsubs;
-        H->dd = upload_dd_impl(dd, hp, M.ptrs, M.bytes, st, H->ystage, H->fdm, bandsubs);
-        if (!bandsubs.empty()) {
+        std::vector<BandInvJob> invjobs;
+        H->dd = upload_dd_impl(dd, hp, M.ptrs, M.bytes, st, H->ystage, H->fdm, bandsubs, invjobs);
+        if (!bandsubs.empty() || !invjobs.empty()) {
             clk.mark("subdomain upload");
             std::vector<double> khtab(hp.cls_k.size());
             for (size_t i = 0; i < khtab.size(); ++i) khtab[i] = hp.cls_k[i] * hp.h;
             if (khtab.empty()) khtab.push_back(hp.k.empty() ? 0.0 : hp.k[0] * hp.h);
-            H->band = band_setup(H->g, bandsubs, H->basis, khtab, M.ptrs, M.bytes, st);
+            H->band = band_setup(H->g, bandsubs, invjobs, const_cast<double2*>(H->dd.Bmat), H->basis, khtab, M.ptrs,
+                                 M.bytes, st);
+            H->devb_classes = int(invjobs.size());
             H->band_subs = H->band.nsub;
             clk.mark("band subdomain factors (device)");
         }
@@ -793,6 +797,7 @@ int htg_info(const htg_handle* h, long long* out) {
         out[16] = h->coarse ? (long long)h->coarse->solve_read_bytes() : 0;
         out[17] = h->band_subs;
         out[18] = h->band.pool_elems * (long long)sizeof(double2);
+        out[19] = h->devb_classes;
     });
 }
 

@@ -209,6 +209,32 @@ bool fdm_supported(int p, int nx, int ny) {
     return lim > 0 && nx <= lim && ny <= lim;
 }
 
+bool fdm_candidate(const HostProblem& hp, int ox, int oy, const DDClass& c) {
+    const int p = hp.p;
+    if (hp.tri || !fdm_supported(p, c.onx * p + 1, c.ony * p + 1)) return false;
+    const double k0 = hp.kc(ox, oy), e0 = hp.ec(ox, oy);
+    for (int y = oy; y < oy + c.ony; ++y)
+        for (int x = ox; x < ox + c.onx; ++x)
+            if (hp.kc(x, y) != k0 || hp.ec(x, y) != e0) return false;
+    auto tag = [&](char s, int i) -> int8_t {
+        switch (s) {
+            case 'b': return oy == 0 ? hp.tb[ox + i] : kAbsorbing;
+            case 't': return oy + c.ony == hp.ny ? hp.tt[ox + i] : kAbsorbing;
+            case 'l': return ox == 0 ? hp.tl[oy + i] : kAbsorbing;
+            default: return ox + c.onx == hp.nx ? hp.tr[oy + i] : kAbsorbing;
+        }
+    };
+    const char names[4] = {'l', 'r', 'b', 't'};
+    for (int s = 0; s < 4; ++s) {
+        const int cnt = s < 2 ? c.ony : c.onx;
+        const int8_t t0 = tag(names[s], 0);
+        if (t0 == kDirichlet) return false;
+        for (int i = 1; i < cnt; ++i)
+            if (tag(names[s], i) != t0) return false;
+    }
+    return true;
+}
+
 bool build_fdm(const HostProblem& hp, const Basis1D& b, double alpha_s, int ox, int oy, DDClass& c) {
     const int p = hp.p;
     if (hp.tri) return false;  // triangle elements are not tensor products

@@ -116,11 +116,11 @@ __global__ void __launch_bounds__(256) k_band_factor(FineGeom g, BandLaunch L) {
         Ms[i / NE1][i % NE1] = L.basis[i];
         Ss[i / NE1][i % NE1] = L.basis[NE1 * NE1 + i];
     }
-    for (int bs = blockIdx.x; bs < L.nsub; bs += gridDim.x) {
-        const int4 sd = L.subs[bs];
+    for (int bs = blockIdx.x; bs < L.nfac; bs += gridDim.x) {
+        const int4 sd = L.fsubs[bs];
         const BandGeomDev G = L.geoms[sd.y];
         const int ox = sd.z & 0xffff, oy = sd.z >> 16;
-        double2* F = L.pool + L.foff[bs];
+        double2* F = L.pool + L.ffoff[bs];
         double2* band = F + (size_t)G.ncell * G.cellstride;
         const int ns = G.ns, bw = G.bw, LDB = bw + 1;
         for (size_t i = tid; i < (size_t)ns * LDB; i += nt) band[i] = make_double2(0.0, 0.0);
@@ -285,7 +285,10 @@ __device__ __forceinline__ void band_col(double2 (&v)[NV], const double2* band, 
 #endif
 constexpr int kBandD = HTG_BAND_D, kBandThreads = HTG_BAND_THREADS;
 
-template <int P, int NV>
+// INV: the same solve with a unit right-hand side e_{U_u} per item, every cell's
+// bubbles back-substituted, writing row u of B_c = A^-1[U, :] (A_s is complex
+// symmetric, so A^-1 e_{U_u} is that row) for the dense-path classes
+template <int P, int NV, bool INV = false>
 __global__ void __launch_bounds__(kBandThreads) k_band_solve(FineGeom g, BandLaunch L, const double2* __restrict__ r,
                                                     double2* __restrict__ ystage, int nu_max) {
     constexpr int NB = 4 * P, NI = (P - 1) * (P - 1), NO = NI + NB, NR = (NO + 31) / 32;
@@ -294,11 +297,12 @@ __global__ void __launch_bounds__(kBandThreads) k_band_solve(FineGeom g, BandLau
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     double2* vec = reinterpret_cast<double2*>(smem_raw) + (size_t)warp * L.warp_elems;
     auto bub = [](int base, int NXn, int j) { return base + (1 + j / (P - 1)) * NXn + 1 + j % (P - 1); };
-    for (int bs = blockIdx.x * nw + warp; bs < L.nsub; bs += gridDim.x * nw) {
-        const int4 sd = L.subs[bs];
+    const int nitems = INV ? L.ninv : L.nsub;
+    for (int bs = blockIdx.x * nw + warp; bs < nitems; bs += gridDim.x * nw) {
+        const int4 sd = INV ? L.inv_rows[bs] : L.subs[bs];  // INV: (factor unit, geometry, U row, kpad)
         const BandGeomDev G = L.geoms[sd.y];
         const int ox = sd.z & 0xffff, oy = sd.z >> 16;
-        const double2* F = L.pool + L.foff[bs];
+        const double2* F = L.pool + (INV ? L.ffoff[sd.x] : L.foff[bs]);
         const double2* band = F + (size_t)G.ncell * G.cellstride;
         const int ns = G.ns, bw = G.bw, LDB = bw + 1, nn = G.NXn * G.NYn, NXn = G.NXn;
         double2* xs = vec + nn;  // skeleton vector
@@ -319,10 +323,15 @@ __global__ void __launch_bounds__(kBandThreads) k_band_solve(FineGeom g, BandLau
             }
         };
         load_cell(0);
-        // gather g = r on Omega (lattice node order)
-        for (int n = lane; n < nn; n += 32) {
-            const int gx = n % NXn, gy = n / NXn;
-            vec[n] = r[dof_index(g.nx, g.ny, P, ox * P + gx, oy * P + gy)];
+        // gather g = r on Omega (lattice node order); INV: the unit vector of U row sd.z
+        if constexpr (INV) {
+            const int hot = G.uout[2 * sd.z];
+            for (int n = lane; n < nn; n += 32) vec[n] = make_double2(n == hot ? 1.0 : 0.0, 0.0);
+        } else {
+            for (int n = lane; n < nn; n += 32) {
+                const int gx = n % NXn, gy = n / NXn;
+                vec[n] = r[dof_index(g.nx, g.ny, P, ox * P + gx, oy * P + gy)];
+            }
         }
         __syncwarp();
         for (int s = lane; s < ns; s += 32) xs[s] = vec[G.skel_node[s]];
@@ -409,9 +418,10 @@ __global__ void __launch_bounds__(kBandThreads) k_band_solve(FineGeom g, BandLau
         }
         for (int s = lane; s < ns; s += 32) vec[G.skel_node[s]] = xs[s];
         __syncwarp();
-        // bubbles of the U cells: x_I = y_I - W x_B (W row o of the cell block: entries o * NO + NI + k)
-        for (int uc = 0; uc < G.nucell; ++uc) {
-            const int cell = G.ucells[uc];
+        // bubbles of the U cells (INV: of every cell): x_I = y_I - W x_B (W row o of the
+        // cell block: entries o * NO + NI + k)
+        for (int uc = 0; uc < (INV ? G.ncell : G.nucell); ++uc) {
+            const int cell = INV ? uc : G.ucells[uc];
             const int cx = cell % G.onx, cy = cell / G.onx;
             const int base = cy * P * NXn + cx * P;
             const double2* Fc = F + (size_t)cell * G.cellstride;
@@ -424,8 +434,13 @@ __global__ void __launch_bounds__(kBandThreads) k_band_solve(FineGeom g, BandLau
             }
         }
         __syncwarp();
-        double2* yrow = ystage + (size_t)sd.x * nu_max;
-        for (int e = lane; e < G.nu; e += 32) yrow[G.uout[2 * e + 1]] = vec[G.uout[2 * e]];
+        if constexpr (INV) {
+            double2* brow = L.Bmat + L.inv_off[bs];
+            for (int l = lane; l < G.nloc; l += 32) brow[l] = vec[G.lnode[l]];
+        } else {
+            double2* yrow = ystage + (size_t)sd.x * nu_max;
+            for (int e = lane; e < G.nu; e += 32) yrow[G.uout[2 * e + 1]] = vec[G.uout[2 * e]];
+        }
         __syncwarp();
     }
 }
@@ -439,7 +454,7 @@ __global__ void __launch_bounds__(kBandThreads) k_band_solve(FineGeom g, BandLau
 // U-row order of the class (local reference dof order, as the combine table).
 struct BandGeomHost {
     int onx, ony, ns = 0, bw = 0, nu = 0;
-    std::vector<int> node_code, skel_node, cell_bnd, uout, ucells;
+    std::vector<int> node_code, skel_node, cell_bnd, uout, ucells, lnode;
 };
 
 static BandGeomHost make_band_geom(int p, int onx, int ony, const std::vector<int>& umem) {
@@ -488,21 +503,24 @@ static BandGeomHost make_band_geom(int p, int onx, int ony, const std::vector<in
         if (gx % p && gy % p) ucell[size_t(gy / p) * onx + gx / p] = 1;  // a bubble of this cell is a U member
     }
     G.nu = int(umem.size());
+    G.lnode = node_of;
     for (int c = 0; c < onx * ony; ++c)
         if (ucell[c]) G.ucells.push_back(c);
     return G;
 }
 
-BandLaunch band_setup(const FineGeom& g, const std::vector<BandSubdomain>& subs, const Basis1D& basis,
-                      const std::vector<double>& khtab, std::vector<void*>& allocs, size_t& bytes, cudaStream_t st) {
+BandLaunch band_setup(const FineGeom& g, const std::vector<BandSubdomain>& subs, const std::vector<BandInvJob>& jobs,
+                      double2* Bmat, const Basis1D& basis, const std::vector<double>& khtab,
+                      std::vector<void*>& allocs, size_t& bytes, cudaStream_t st) {
     BandLaunch L{};
-    if (subs.empty()) return L;
+    if (subs.empty() && jobs.empty()) return L;
     const int p = g.p;
     const int NI = (p - 1) * (p - 1), NB = 4 * p;
     std::map<std::vector<int>, int> gid;
     std::vector<BandGeomHost> geoms;
-    std::vector<int4> sd;
-    std::vector<long long> foff;
+    std::vector<int4> sd, fsd;
+    std::vector<long long> foff, ffoff;
+    std::map<int, long long> cls_off;  // class -> its factor
     long long pool = 0;
     for (const BandSubdomain& s : subs) {
         std::vector<int> key{s.onx, s.ony};
@@ -513,9 +531,37 @@ BandLaunch band_setup(const FineGeom& g, const std::vector<BandSubdomain>& subs,
             geoms.push_back(make_band_geom(p, s.onx, s.ony, *s.umem));
         }
         const BandGeomHost& G = geoms[it->second];
-        sd.push_back(make_int4(s.sid, it->second, s.ox | (s.oy << 16), 0));
-        foff.push_back(pool);
+        const int4 e = make_int4(s.sid, it->second, s.ox | (s.oy << 16), 0);
+        auto ct = cls_off.find(s.cls);
+        if (ct == cls_off.end()) {  // first member: the class's factor unit
+            ct = cls_off.emplace(s.cls, pool).first;
+            fsd.push_back(e);
+            ffoff.push_back(pool);
+            pool += (long long)G.onx * G.ony * (NI * NI + NI * NB) + (long long)G.ns * (G.bw + 1);
+        }
+        sd.push_back(e);
+        foff.push_back(ct->second);
+    }
+    // dense-path classes: their factor unit (the first member) and one item per U row
+    std::vector<int4> inv_rows;
+    std::vector<long long> inv_off;
+    for (const BandInvJob& j : jobs) {
+        std::vector<int> key{j.onx, j.ony};
+        key.insert(key.end(), j.umem->begin(), j.umem->end());
+        auto it = gid.find(key);
+        if (it == gid.end()) {
+            it = gid.emplace(key, int(geoms.size())).first;
+            geoms.push_back(make_band_geom(p, j.onx, j.ony, *j.umem));
+        }
+        const BandGeomHost& G = geoms[it->second];
+        const int unit = int(fsd.size());
+        fsd.push_back(make_int4(j.sid, it->second, j.ox | (j.oy << 16), 0));
+        ffoff.push_back(pool);
         pool += (long long)G.onx * G.ony * (NI * NI + NI * NB) + (long long)G.ns * (G.bw + 1);
+        for (int u = 0; u < G.nu; ++u) {
+            inv_rows.push_back(make_int4(unit, it->second, u, j.kpad));
+            inv_off.push_back(j.boff + (long long)u * j.kpad);
+        }
     }
     auto up = [&](const auto& v) {
         using T = typename std::decay_t<decltype(v)>::value_type;
@@ -545,12 +591,21 @@ BandLaunch band_setup(const FineGeom& g, const std::vector<BandSubdomain>& subs,
         d.cell_bnd = up(G.cell_bnd);
         d.uout = up(G.uout);
         d.ucells = up(G.ucells);
+        d.lnode = up(G.lnode);
+        d.nloc = int(G.lnode.size());
         gd.push_back(d);
         max_warp = std::max(max_warp, size_t(d.NXn) * d.NYn + size_t(d.ns));
     }
     L.geoms = up(gd);
     L.subs = up(sd);
     L.foff = up(foff);
+    L.fsubs = up(fsd);
+    L.ffoff = up(ffoff);
+    L.nfac = int(fsd.size());
+    L.inv_rows = up(inv_rows);
+    L.inv_off = up(inv_off);
+    L.ninv = int(inv_rows.size());
+    L.Bmat = Bmat;
     L.khtab = up(khtab);
     std::vector<double> bt(2 * size_t(p + 1) * (p + 1));
     for (int a = 0; a <= p; ++a)
@@ -579,7 +634,7 @@ BandLaunch band_setup(const FineGeom& g, const std::vector<BandSubdomain>& subs,
     const size_t fsm = (size_t(NE) * NE + size_t(NI) * NI + size_t(NI) * NB + NI) * sizeof(double2) + size_t(ns_max) * 4;
     if (fsm > size_t(kSmem) - 4096) throw RuntimeError("band subdomain solver: element too large for shared memory");
     const int nsm = current_sm_count();
-    const int fgrid = std::min(L.nsub, nsm * std::max(1, std::min(8, int((kSmem - 4096) / fsm))));
+    const int fgrid = std::min(L.nfac, nsm * std::max(1, std::min(8, int((kSmem - 4096) / fsm))));
     auto go = [&](auto kern) {
         // (the kernel also holds ~1.6 KB of static shared memory)
         HTG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem - 4096));
@@ -593,6 +648,30 @@ BandLaunch band_setup(const FineGeom& g, const std::vector<BandSubdomain>& subs,
     }
     HTG_CUDA(cudaGetLastError());
     count_launch();
+    if (L.ninv > 0) {  // explicit restricted inverses of the dense-path classes
+        const int nv = L.bw_max <= 64 ? 2 : (L.bw_max <= 128 ? 4 : 8);
+        const int grid = (L.ninv + L.warps - 1) / L.warps;
+        auto gi = [&](auto kern) {
+            HTG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
+            kern<<<grid, L.warps * 32, L.solve_smem, st>>>(g, L, nullptr, nullptr, 0);
+        };
+        switch (p * 10 + nv) {
+            case 22: gi(k_band_solve<2, 2, true>); break;
+            case 24: gi(k_band_solve<2, 4, true>); break;
+            case 28: gi(k_band_solve<2, 8, true>); break;
+            case 42: gi(k_band_solve<4, 2, true>); break;
+            case 44: gi(k_band_solve<4, 4, true>); break;
+            case 48: gi(k_band_solve<4, 8, true>); break;
+            case 62: gi(k_band_solve<6, 2, true>); break;
+            case 64: gi(k_band_solve<6, 4, true>); break;
+            case 68: gi(k_band_solve<6, 8, true>); break;
+            case 82: gi(k_band_solve<8, 2, true>); break;
+            case 84: gi(k_band_solve<8, 4, true>); break;
+            default: gi(k_band_solve<8, 8, true>); break;
+        }
+        HTG_CUDA(cudaGetLastError());
+        count_launch();
+    }
     HTG_CUDA(cudaStreamSynchronize(st));
     return L;
 }

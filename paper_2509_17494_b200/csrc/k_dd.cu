@@ -222,7 +222,7 @@ void dd_combine_launch(const FineGeom& g, const DDDevice& d, const double2* ysta
 // U-row maps, tile list) and upload.
 DDDevice upload_dd_impl(const DDSetup& dd, const HostProblem& hp, std::vector<void*>& allocs, size_t& bytes,
                         cudaStream_t st, double2*& ystage, std::vector<FdmClassDev>& fdm,
-                        std::vector<BandSubdomain>& band) {
+                        std::vector<BandSubdomain>& band, std::vector<BandInvJob>& jobs) {
     DDDevice d;
     const int nc = int(dd.classes.size());
     d.nclass = nc;
@@ -255,7 +255,11 @@ DDDevice upload_dd_impl(const DDSetup& dd, const HostProblem& hp, std::vector<vo
         in[7] = int(subs[ci].size());
         const size_t b0 = Bm.size();
         if (!c.band) Bm.resize(b0 + size_t(rpad) * kpad, make_double2(0.0, 0.0));
-        for (int rI = 0; rI < (c.band ? 0 : c.nu); ++rI)
+        if (c.devB && !subs[ci].empty()) {  // B_c filled on the device (k_band.cu) from a band factor
+            const int s0 = subs[ci][0];
+            jobs.push_back({s0, dd.sub_ox[s0], dd.sub_oy[s0], c.onx, c.ony, &c.umem, ci, (long long)b0, kpad});
+        }
+        for (int rI = 0; rI < (c.band || c.devB ? 0 : c.nu); ++rI)
             for (int l = 0; l < c.nloc; ++l) {
                 const cplx v = c.B[size_t(rI) * c.nloc + l];
                 Bm[b0 + size_t(rI) * kpad + l] = make_double2(v.real(), v.imag());
@@ -270,7 +274,7 @@ DDDevice upload_dd_impl(const DDSetup& dd, const HostProblem& hp, std::vector<vo
         const int off = int(class_subs.size());
         class_subs.insert(class_subs.end(), subs[ci].begin(), subs[ci].end());
         if (c.band) {  // per-member device factors (k_band.cu)
-            for (int sI : subs[ci]) band.push_back({sI, dd.sub_ox[sI], dd.sub_oy[sI], c.onx, c.ony, &c.umem});
+            for (int sI : subs[ci]) band.push_back({sI, dd.sub_ox[sI], dd.sub_oy[sI], c.onx, c.ony, &c.umem, ci});
             continue;
         }
         if (c.fdm && fdm_supported(p, c.fdm_nx, c.fdm_ny)) {

@@ -478,6 +478,13 @@ int fdm_rows(int fac_elems) {
 #define HTG_FDM_TGW 3
 #endif
 constexpr int kTGW = HTG_FDM_TGW < kTG ? HTG_FDM_TGW : kTG;  // moving tiles in flight (team kernel)
+#ifndef HTG_FDM_PADF
+#define HTG_FDM_PADF 0
+#endif
+#ifndef HTG_FDM_PADD
+#define HTG_FDM_PADD 0
+#endif
+constexpr bool kPadF = HTG_FDM_PADF != 0, kPadD = HTG_FDM_PADD != 0;
 
 template <int LD, int KS, bool FTR>
 struct WStage {
@@ -497,7 +504,10 @@ struct WStage {
     __device__ __forceinline__ void operator()(Epi&& epi) const {
         const Stage<LD, KS> b{fac, F, dat, nd, sa, 0, lane};
         const int r = lane >> 2, kq = lane & 3;
-        const int FR = (F & 7) <= 2 ? (F & 7) : 0, DR = (nd & 7) <= 2 ? (nd & 7) : 0;
+        // remainder rows of 8t + 1 / 8t + 2 extents run as DFMA dots unless padded
+        // into a tile (HTG_FDM_PADF / HTG_FDM_PADD: padded rows repeat the last row,
+        // so their fragment loads are broadcasts, and their outputs are dropped)
+        const int FR = (!kPadF && (F & 7) <= 2) ? (F & 7) : 0, DR = (!kPadD && (nd & 7) <= 2) ? (nd & 7) : 0;
         const int ST = (F - FR + 7) >> 3, OT = (nd - DR + 7) >> 3;
         const int flim = F - FR - 1, dlim = nd - DR - 1;
         // tiles (st, ot) flattened st-major; this warp takes [t0, t1)

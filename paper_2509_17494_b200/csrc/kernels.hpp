@@ -139,6 +139,8 @@ struct BandGeomDev {
     const int* cell_bnd;     // per cell, boundary slot -> skeleton index
     const int* uout;         // (lattice node, U row) per U member
     const int* ucells;       // cells with U bubbles
+    const int* lnode;        // local reference dof -> lattice node (nloc entries)
+    int nloc;
 };
 struct BandLaunch {
     const BandGeomDev* geoms;
@@ -149,6 +151,16 @@ struct BandLaunch {
     const double* basis;     // 1-D M then S, (p+1)^2 each
     long long pool_elems;
     int nsub;
+    // factor units (one per class, factored from its first member)
+    const int4* fsubs;
+    const long long* ffoff;
+    int nfac;
+    // explicit restricted inverses B_c = A^-1[U, :] of dense-path classes, one row per
+    // item: (factor unit, geometry, U row, kpad) and the row's offset into Bmat
+    const int4* inv_rows;
+    const long long* inv_off;
+    int ninv;
+    double2* Bmat;
     int warps;               // sweep: warps (subdomains in flight) per CTA
     int warp_elems;          // sweep: shared-memory vector elements per warp
     int bw_max;              // largest half bandwidth
@@ -157,10 +169,20 @@ struct BandLaunch {
 struct BandSubdomain {
     int sid, ox, oy, onx, ony;
     const std::vector<int>* umem;  // U members (local reference dof order = U-row order)
+    int cls;                       // subdomain class: members of a class share one factor
+};
+// a dense-path class whose B_c is computed on the device from its band factor
+struct BandInvJob {
+    int sid, ox, oy, onx, ony;      // first member
+    const std::vector<int>* umem;
+    int cls;
+    long long boff;                 // B_c in the dense-path Bmat ([rpad][kpad])
+    int kpad;
 };
 struct Basis1D;
-BandLaunch band_setup(const FineGeom& g, const std::vector<BandSubdomain>& subs, const Basis1D& basis,
-                      const std::vector<double>& khtab, std::vector<void*>& allocs, size_t& bytes, cudaStream_t st);
+BandLaunch band_setup(const FineGeom& g, const std::vector<BandSubdomain>& subs, const std::vector<BandInvJob>& jobs,
+                      double2* Bmat, const Basis1D& basis, const std::vector<double>& khtab,
+                      std::vector<void*>& allocs, size_t& bytes, cudaStream_t st);
 void band_solve_launch(const FineGeom& g, const BandLaunch& L, const double2* r, double2* ystage, int nu_max,
                        cudaStream_t st);
 // out = u + sum_i y_i / L in subdomain order (u may be null -> 0); out may alias u

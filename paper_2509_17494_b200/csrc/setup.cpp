@@ -488,7 +488,15 @@ DDSetup build_dd(const HostProblem& hp, const Basis1D& b, double alpha_s, int l_
                             varies = true;
                             break;
                         }
-                dd.classes[ci].band = !hp.tri && varies && members[ci] <= band_max;  // the device assembly is for squares
+                // device factors (square cells): unique coefficient patterns, and every
+                // class at p >= 6, where a host dense inverse of |Omega| = 1369..2401 dofs
+                // costs seconds and the shared class factor stays L2-resident
+                dd.classes[ci].band = !hp.tri && varies && members[ci] <= band_max;
+                // the other square-cell classes the fast diagonalisation cannot take get
+                // their B_c from a device band factor (HTG_DEVB=0: host dense inverse)
+                const char* db = std::getenv("HTG_DEVB");
+                dd.classes[ci].devB = !(db && db[0] == '0') && !hp.tri && !dd.classes[ci].band &&
+                                      !fdm_candidate(hp, ox, oy, c);
             }
     }
     // restricted inverses, one per class (threads over classes)
@@ -498,7 +506,7 @@ DDSetup build_dd(const HostProblem& hp, const Basis1D& b, double alpha_s, int l_
             DDClass& c = dd.classes[ci];
             std::vector<cplx> A;
             const int p = hp.p;
-            if (c.band) c.nloc = int(dof_index(c.onx, c.ony, p, c.onx * p, c.ony * p)) + 1;
+            if (c.band || c.devB) c.nloc = int(dof_index(c.onx, c.ony, p, c.onx * p, c.ony * p)) + 1;
             else assemble_omega(hp, b, alpha_s, first[ci].ox, first[ci].oy, c.onx, c.ony, A, c.nloc);
             const int n = c.nloc;
             // U members: local dofs whose support touches a U cell (twogrid.cpp:46-62)
@@ -517,7 +525,7 @@ DDSetup build_dd(const HostProblem& hp, const Basis1D& b, double alpha_s, int l_
             for (int l = 0; l < n; ++l)
                 if (isU[l]) c.umem.push_back(l);
             c.nu = int(c.umem.size());
-            if (c.band) return;  // factored per member on the device
+            if (c.band || c.devB) return;  // factored on the device
             // B = A^-1 [U, :] = (A^-T [:, U])^T: solve A^T X = E_U
             std::vector<cplx> At(size_t(n) * n);
             for (int i = 0; i < n; ++i)

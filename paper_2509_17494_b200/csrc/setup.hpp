@@ -103,7 +103,13 @@ struct DDClass {
     // no shared factor (few members, coefficients varying over Omega): every
     // member is factored on the device (k_band.cu); B stays empty
     bool band = false;
+    // dense path with B computed on the device from a band factor (square cells,
+    // classes the fast diagonalisation cannot take): no host inverse
+    bool devB = false;
 };
+// cheap pre-check of build_fdm's separability conditions (uniform (k, eps) over
+// Omega, one non-Dirichlet tag per Omega side, p and extents the FDM kernel takes)
+bool fdm_candidate(const HostProblem& hp, int ox, int oy, const DDClass& c);
 // Build the FDM factors of a class whose first subdomain's Omega starts at
 // cell (ox, oy); false if the class is not separable or fails validation.
 bool build_fdm(const HostProblem& hp, const Basis1D& b, double alpha_s, int ox, int oy, DDClass& c);

@@ -211,7 +211,7 @@ class TwoGridOperators:
         st = C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
         check(L.htg_create(C.byref(cp), C.byref(cfg), st, C.byref(h)))
         self._h = h
-        info = (C.c_longlong * 19)()
+        info = (C.c_longlong * 20)()
         check(L.htg_info(h, info))
         (self.ndof, self.coarse_ndof, self.n_subdomains, self.n_classes, self.device_bytes,
          self.coarse_factor_bytes) = (int(v) for v in info[:6])
@@ -221,6 +221,7 @@ class TwoGridOperators:
         self.fdm_subdomains = int(info[12])
         self.sum_u, self.sum_omega, self.coarse_read_bytes = int(info[14]), int(info[15]), int(info[16])
         self.band_subdomains, self.band_factor_bytes = int(info[17]), int(info[18])
+        self.device_inverse_classes = int(info[19])
 
     def _f(self, t):  # fine-space device vector
         return _dptr(t, self.ndof, self.device)
@@ -230,7 +231,7 @@ class TwoGridOperators:
 
     @property
     def cached_graphs(self) -> int:
-        info = (C.c_longlong * 19)()
+        info = (C.c_longlong * 20)()
         check(lib().htg_info(self._h, info))
         return int(info[13])
 
