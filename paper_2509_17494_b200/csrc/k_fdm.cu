@@ -50,6 +50,16 @@ template <int P> struct FdmDims;
 template <> struct FdmDims<2> { static constexpr int LD = HTG_FDM_ODD_LD ? 17 : 20, KS = 4; };  // extents <= 16
 template <> struct FdmDims<4> { static constexpr int LD = HTG_FDM_ODD_LD ? 29 : 28, KS = 7; };  // extents <= 28
 constexpr bool kSkew = !HTG_FDM_ODD_LD;  // xor-skew the k of remainder dots (even pitch only)
+// Fragment row r of every tile maps to tile row pi(r) = (r >> 1) | (r & 1) << 2: a
+// 128-bit fragment load's quarter-warp (rows 2p, 2p+1 x 4 k) then covers all 8
+// bank groups with the odd pitch (pi(2p+1) - pi(2p) = 4, 5 * 4 = 4 mod 8), and so
+// do the row-major and transposed epilogue stores; without it every fragment
+// load is two-way conflicted (8 wavefronts instead of 4, 31% of the kernel's
+// shared-memory traffic)
+#ifndef HTG_FDM_PERM
+#define HTG_FDM_PERM 1
+#endif
+__device__ __forceinline__ int frow_perm(int r) { return HTG_FDM_PERM ? ((r >> 1) | ((r & 1) << 2)) : r; }
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -118,7 +128,7 @@ struct Stage {
                     a2 += t2[h][j][i];
                     a3 += t3[h][j][i];
                 }
-                epi(tm[j] * 8 + r, tn[j] * 8 + 2 * kq + i, make_double2(a1 - a2, a3 - a1 - a2));
+                epi(tm[j] * 8 + frow_perm(r), tn[j] * 8 + frow_perm(2 * kq + i), make_double2(a1 - a2, a3 - a1 - a2));
             }
     }
     template <int NTL>
@@ -215,7 +225,7 @@ struct Stage {
         for (int st = st0; st < ST; st += sstep) {
             double2 sf[KS];
             double ss[KS];
-            const int frow = min(st * 8 + r, flim);
+            const int frow = min(st * 8 + frow_perm(r), flim);
 #pragma unroll
             for (int ks = 0; ks < KS; ++ks) {
                 sf[ks] = fval(frow, ks * 4 + kq);
@@ -226,7 +236,7 @@ struct Stage {
                 int mrow[kTG], tm[kTG], tn[kTG];
 #pragma unroll
                 for (int j = 0; j < kTG; ++j) {
-                    mrow[j] = min((o0 + j) * 8 + r, dlim) * LD + kq;
+                    mrow[j] = min((o0 + j) * 8 + frow_perm(r), dlim) * LD + kq;
                     tm[j] = sa ? st : o0 + j;
                     tn[j] = sa ? o0 + j : st;
                 }
@@ -516,7 +526,7 @@ struct WStage {
             const int st = t / OT, o_lo = t - st * OT, o_hi = min(OT, o_lo + (t1 - t));
             double2 sf[KS];
             double ss[KS];
-            const int fr = min(st * 8 + r, flim);
+            const int fr = min(st * 8 + frow_perm(r), flim);
 #pragma unroll
             for (int ks = 0; ks < KS; ++ks) {
                 sf[ks] = fval(fr, ks * 4 + kq);
@@ -527,7 +537,7 @@ struct WStage {
                 int mrow[kTG], tm[kTG], tn[kTG];
 #pragma unroll
                 for (int j = 0; j < kTG; ++j) {
-                    mrow[j] = min((o0 + j) * 8 + r, dlim) * LD + kq;
+                    mrow[j] = min((o0 + j) * 8 + frow_perm(r), dlim) * LD + kq;
                     tm[j] = sa ? st : o0 + j;
                     tn[j] = sa ? o0 + j : st;
                 }
