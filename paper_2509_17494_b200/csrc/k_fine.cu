@@ -521,7 +521,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_residual(K1Args a) {
 // TMA tensor loads of a 3-D map [row][sub-row][16-byte chunk] (sub-rows of 128
 // bytes for p = 4, 64 bytes for p = 2) with the matching shared-memory
 // swizzle: one instruction per row, and the per-lane unit reads hit distinct
-// banks (p = 2) or two-way (p = 4). The x = nx column unit (p dofs) and the top
+// banks (p = 2; p = 4 with the half-major box, see kc_idx). The x = nx column unit (p dofs) and the top
 // lattice row (p dofs per unit) are 1-D bulk copies; r is written back from
 // shared memory with coalesced stores.
 #ifndef HTG_KC_CELLS
@@ -585,10 +585,22 @@ struct __align__(1024) KCSmem {
 // double2 index of element k of staged unit u (rows below the top): the
 // tensor-map box layout with its 16-byte-chunk swizzle (128B: chunk ^= sub-row
 // & 7; 64B: chunk ^= (sub-row >> 1) & 3)
+//
+// Units of two sub-rows (p = 4) are staged half-major ([half][unit][chunk], a 4-D
+// map whose unit and half strides are swapped): the lanes of a warp read the
+// same element k of consecutive units, i.e. consecutive sub-rows, so the
+// swizzle spreads every eight lanes over all eight 16-byte bank groups. In
+// unit-major order ([unit][half][chunk]) consecutive units are two sub-rows
+// apart and only four of the eight swizzle phases occur: a two-way conflict on
+// every unit read.
+#ifndef HTG_KC_HMAJOR
+#define HTG_KC_HMAJOR 1
+#endif
 template <int P>
 __device__ __forceinline__ int kc_idx(int u, int k) {
     using C = KCCfg<P>;
-    const int r = u * C::RPU + k / C::CPR, c = k % C::CPR;
+    const int r = (HTG_KC_HMAJOR && C::RPU == 2) ? (k / C::CPR) * C::NU + u : u * C::RPU + k / C::CPR;
+    const int c = k % C::CPR;
     const int sw = C::RB == 128 ? (r & 7) : ((r >> 1) & 3);
     return r * C::CPR + (c ^ sw);
 }
@@ -605,6 +617,15 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
         "[%5];\n" ::"r"(smem_u32(dst)),
         "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+        "[%6];\n" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
         : "memory");
 }
 
@@ -658,7 +679,8 @@ __device__ __forceinline__ void k1c_body(const K1Args& a, const CUtensorMap* tmu
         if (yy < ny) {
             const bool with_edge = xb == nx;
             mbar_expect_tx(bar, unsigned(Cf::BOX + (with_edge ? P * 16 : 0)));
-            tma_load_3d(dst, map, 0, xa * Cf::RPU, yy, bar);
+            if (HTG_KC_HMAJOR && Cf::RPU == 2) tma_load_4d(dst, map, 0, xa, 0, yy, bar);
+            else tma_load_3d(dst, map, 0, xa * Cf::RPU, yy, bar);
             if (with_edge) tma_load_1d(dst + EDGE, src + unit_off<P>(nx, ny, nx, yy), P * 16, bar);
         } else {
             const long long lo = unit_off<P>(nx, ny, xa, ny);
@@ -1088,8 +1110,20 @@ static CUtensorMap kc_tensor_map(const FineGeom& g, const double2* base) {
         if (!encode || q != cudaDriverEntryPointSuccess) throw RuntimeError("cuTensorMapEncodeTiled unavailable");
     }
     CUtensorMap m;
+    const cuuint64_t rowb = cuuint64_t(g.nx * P * P + P) * 16;
+    if (HTG_KC_HMAJOR && C::RPU == 2) {  // [row][half][unit][chunk]: half-major box (see kc_idx)
+        const cuuint64_t dims[4] = {cuuint64_t(C::RB / 8), cuuint64_t(g.nx), 2, cuuint64_t(g.ny)};
+        const cuuint64_t strides[3] = {cuuint64_t(C::UB), cuuint64_t(C::RB), rowb};
+        const cuuint32_t box[4] = {cuuint32_t(C::RB / 8), cuuint32_t(C::NU), 2, 1};
+        const cuuint32_t estr[4] = {1, 1, 1, 1};
+        const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double2*>(base), dims, strides,
+                                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) throw RuntimeError("cuTensorMapEncodeTiled (4-D) failed (" + std::to_string(int(r)) + ")");
+        return m;
+    }
     const cuuint64_t dims[3] = {cuuint64_t(C::RB / 8), cuuint64_t(g.nx) * C::RPU, cuuint64_t(g.ny)};
-    const cuuint64_t strides[2] = {cuuint64_t(C::RB), cuuint64_t(g.nx * P * P + P) * 16};
+    const cuuint64_t strides[2] = {cuuint64_t(C::RB), rowb};
     const cuuint32_t box[3] = {cuuint32_t(C::RB / 8), cuuint32_t(C::NU * C::RPU), 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double2*>(base), dims, strides, box,

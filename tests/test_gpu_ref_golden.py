@@ -1,5 +1,6 @@
 """The CUDA path against the REFERENCE's own outputs (tests/golden/ref_*.npz, made by
-tools/make_ref_golden.py from the reference's unmodified hot-path sources), with no
+tools/make_ref_golden.py from the reference's unmodified hot-path sources; reftri_*
+are triangle meshes), with no
 oracle at run time. North-star tolerances: relative l2 <= 1e-10 for each residual,
 smoother sweep and transfer application; two-grid iteration counts equal within
 +-1 (asserted equal here, with the history to 1e-6 relative)."""
@@ -11,7 +12,7 @@ import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
-GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "ref_*.npz")))
+GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "ref*.npz")))
 TOL = 1e-10
 
 
@@ -28,7 +29,8 @@ def problem_of(hb, g):
     return hb.twogrid.Problem(order=d["order"], n_cells=d["nx"], h=d["h"], k=float(g["k_cells"].mean()),
                               k_cells=np.ascontiguousarray(g["k_cells"].ravel()),
                               eps_cells=np.ascontiguousarray(g["eps_cells"].ravel()),
-                              side_tags=d["side_tags"], rhs=g["f"], ny=d["ny"])
+                              side_tags=d["side_tags"], rhs=g["f"], ny=d["ny"],
+                              element_kind=d.get("element_kind", 0))
 
 
 @pytest.mark.parametrize("path", GOLDEN, ids=[os.path.basename(p)[:-4] for p in GOLDEN])

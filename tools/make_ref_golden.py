@@ -51,6 +51,21 @@ DESC_CASES = {
     "ref_rect_p6_hetero_exact": (dict(order=6, nx=5, ny=4, h=0.1, side_tags=(N_, A_, A_, A_), kr=(6.0, 9.0), er=1.0,
                                       seed=5), dict(smoother=1, outer=1)),
 }
+# triangle meshes (ElementKind::Triangle): the restated oracle covers squares only,
+# so these pin the product's host assembly (tests/test_tri_cpu.py) and its CUDA path
+# (tests/test_gpu_ref_golden.py) to the reference's outputs
+TRI_SPEC_CASES = {
+    "reftri_p2_abs_ns2": (dict(order=2, wavelengths=3, ppw=8, element_kind=1), dict(n_s=2)),
+    "reftri_p4_dir_neu": (dict(order=4, wavelengths=4, ppw=10, side_tags=(D_, A_, N_, A_), element_kind=1), dict()),
+    "reftri_p4_galerkin_exact": (dict(order=4, wavelengths=3, ppw=10, side_tags=(A_, A_, D_, A_), element_kind=1),
+                                 dict(coarsening=1, alpha_c=0.05, smoother=1, outer=1)),
+    "reftri_p6_layer_krylov": (dict(order=6, wavelengths=3, ppw=8, side_tags=(N_, A_, A_, A_), layer_sides=(L_,),
+                                    layer_width_dofs=8, element_kind=1), dict(outer=1)),
+    "reftri_p8_abs": (dict(order=8, wavelengths=2, ppw=8, element_kind=1), dict()),
+}
+SPEC_CASES.update(TRI_SPEC_CASES)
+DESC_CASES["reftri_rect_p4_hetero"] = (dict(order=4, nx=11, ny=7, h=0.07, side_tags=(A_, D_, N_, A_), kr=(8.0, 12.0),
+                                            er=0.5, seed=6, element_kind=1), dict())
 
 
 def desc_arrays(d):
@@ -69,7 +84,8 @@ def make(name):
         d, cfg = DESC_CASES[name]
         k, eps = desc_arrays(d)
         ses = pyref.RefSession(desc=dict(order=d["order"], nx=d["nx"], ny=d["ny"], h=d["h"], k=k, eps=eps,
-                                         side_tags=d["side_tags"]), config=po.SolverConfig(**cfg))
+                                         side_tags=d["side_tags"], element_kind=d.get("element_kind", 0)),
+                               config=po.SolverConfig(**cfg))
         extra = dict(desc=np.array(repr(d)), k_cells=k, eps_cells=eps)
     n, nc = ses.ndof, ses.coarse_ndof
     f, u = po.random_vector(n, 11), po.random_vector(n, 12)
