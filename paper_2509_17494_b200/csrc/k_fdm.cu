@@ -101,6 +101,22 @@ constexpr int kTG = HTG_FDM_TG;  // moving tiles in flight per warp (one station
 #endif
 constexpr bool kDataRem = HTG_FDM_DR != 0;  // data-row remainders on the CUDA cores (group kernel)
 
+// Complex products on the real DMMA: 3M (default: t1 = Re a Re b, t2 = Im a Im b,
+// t3 = (Re a + Im a)(Re b + Im b); re = t1 - t2, im = t3 - t1 - t2) or, with
+// HTG_FDM_4M, four products into two accumulators (re += Re a Re b + (-Im a) Im b,
+// im += Re a Im b + Im a Re b): a third more DMMAs, but no pre-sum of the moving
+// operand in front of every third DMMA and no post-combination.
+#ifndef HTG_FDM_4M
+#define HTG_FDM_4M 0
+#endif
+constexpr bool kF4M = HTG_FDM_4M != 0;
+// the stationary operand's auxiliary value: Re + Im (3M) or -Im (4M, a sign flip
+// on the integer pipe)
+__device__ __forceinline__ double stat_aux(double2 v) {
+    if constexpr (kF4M) return __longlong_as_double(__double_as_longlong(v.y) ^ (1ll << 63));
+    else return v.x + v.y;
+}
+
 template <int LD, int KS, bool FTR = false>
 struct Stage {
     const double2* fac;  // factor operand [F][LD] (zero k padding)
@@ -146,6 +162,46 @@ struct Stage {
                                              const int* mrow, const int* tm, const int* tn, Epi& epi) const {
         Acc t1, t2, t3;
         zero<NTL>(t1, t2, t3);
+        if constexpr (kF4M) {  // t1: re, t2: im (ss = -Im of the stationary fragment)
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) {
+                const int h = ks % kKP;
+                double2 v[kTG];
+#pragma unroll
+                for (int j = 0; j < NTL; ++j) v[j] = mv[mrow[j] + ks * 4];
+#pragma unroll
+                for (int j = 0; j < NTL; ++j) {
+                    if (SA) dmma(t1[h][j][0], t1[h][j][1], sf[ks].x, v[j].x);
+                    else dmma(t1[h][j][0], t1[h][j][1], v[j].x, sf[ks].x);
+                }
+#pragma unroll
+                for (int j = 0; j < NTL; ++j) {
+                    if (SA) dmma(t2[h][j][0], t2[h][j][1], sf[ks].x, v[j].y);
+                    else dmma(t2[h][j][0], t2[h][j][1], v[j].x, sf[ks].y);
+                }
+#pragma unroll
+                for (int j = 0; j < NTL; ++j) {
+                    if (SA) dmma(t1[h][j][0], t1[h][j][1], ss[ks], v[j].y);
+                    else dmma(t1[h][j][0], t1[h][j][1], v[j].y, ss[ks]);
+                }
+#pragma unroll
+                for (int j = 0; j < NTL; ++j) {
+                    if (SA) dmma(t2[h][j][0], t2[h][j][1], sf[ks].y, v[j].x);
+                    else dmma(t2[h][j][0], t2[h][j][1], v[j].y, sf[ks].x);
+                }
+            }
+            const int r = lane >> 2, kq = lane & 3;
+#pragma unroll
+            for (int j = 0; j < NTL; ++j)
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    double re = t1[0][j][i], im = t2[0][j][i];
+#pragma unroll
+                    for (int hh = 1; hh < kKP; ++hh) re += t1[hh][j][i], im += t2[hh][j][i];
+                    epi(tm[j] * 8 + frow_perm(r), tn[j] * 8 + frow_perm(2 * kq + i), make_double2(re, im));
+                }
+            return;
+        }
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
             const int h = ks % kKP;
@@ -229,7 +285,7 @@ struct Stage {
 #pragma unroll
             for (int ks = 0; ks < KS; ++ks) {
                 sf[ks] = fval(frow, ks * 4 + kq);
-                ss[ks] = sf[ks].x + sf[ks].y;
+                ss[ks] = stat_aux(sf[ks]);
             }
             for (int o0 = o_lo; o0 < o_hi; o0 += kTG) {
                 const int nt = min(kTG, o_hi - o0);
@@ -530,7 +586,7 @@ struct WStage {
 #pragma unroll
             for (int ks = 0; ks < KS; ++ks) {
                 sf[ks] = fval(fr, ks * 4 + kq);
-                ss[ks] = sf[ks].x + sf[ks].y;
+                ss[ks] = stat_aux(sf[ks]);
             }
             for (int o0 = o_lo; o0 < o_hi; o0 += kTGW) {
                 const int nt = min(kTGW, o_hi - o0);
@@ -586,6 +642,14 @@ struct WStage {
 #endif
 constexpr int kWThreads(int p, int np) { return (np == 1 && p == 4) ? 256 : (np == 2 && p == 4 ? HTG_FDM_TTHREADS : 512); }
 
+#ifndef HTG_FDM_SYM_CODE
+#define HTG_FDM_SYM_CODE 1  // 0: compile the team kernel without the mirror-symmetric path
+#endif
+#ifndef HTG_FDM_TEAM4_BELOW
+#define HTG_FDM_TEAM4_BELOW 40
+#endif
+constexpr int kFdmTeam4Below = HTG_FDM_TEAM4_BELOW;  // subdomains per SM below which teams are 4 warps
+
 template <int NP>
 __device__ __forceinline__ void team_sync(int team) {
     if constexpr (NP == 1) __syncwarp();
@@ -624,7 +688,7 @@ __global__ void __launch_bounds__(kWThreads(P, NP), 1)
         int* gpos = gofs + nx * ny;    // ... and the tile slot each one lands in
         __syncthreads();  // previous segment finished with the factors
         const double2 z = make_double2(0.0, 0.0);
-        const bool sym = (P == 4) && c.sym;
+        const bool sym = HTG_FDM_SYM_CODE && (P == 4) && c.sym;
         // mirror tables of a symmetric class (after the gather tables):
         // bfn[r]: natural rows of reordered row r; ubn[n]: reordered rows of natural row n
         int* bfn = gpos + nx * ny;
@@ -878,10 +942,13 @@ void dd_fdm_launch(const FineGeom& g, const FdmLaunch& L, const double2* r, doub
         kern<<<L.nwork, L.nwarps * 32, L.smem, st>>>(g, L.classes, L.work, r, ystage, nu_max, L.rows, L.fac_elems);
     };
     if (L.nwarps > 0) {
-        const bool pair = L.team == 2;
-        switch (g.p) {
-            case 2: pair ? go_w(k_dd_fdm_w<2, 2>, 0) : go_w(k_dd_fdm_w<2, 1>, 1); break;
-            case 4: pair ? go_w(k_dd_fdm_w<4, 2>, 2) : go_w(k_dd_fdm_w<4, 1>, 3); break;
+        switch (g.p * 8 + L.team) {
+            case 17: go_w(k_dd_fdm_w<2, 1>, 1); break;
+            case 18: go_w(k_dd_fdm_w<2, 2>, 0); break;
+            case 20: go_w(k_dd_fdm_w<2, 4>, 4); break;
+            case 33: go_w(k_dd_fdm_w<4, 1>, 3); break;
+            case 34: go_w(k_dd_fdm_w<4, 2>, 2); break;
+            case 36: go_w(k_dd_fdm_w<4, 4>, 5); break;
             default: throw InvalidArgument("FDM subdomain kernel: p must be 2 or 4");
         }
     } else {
@@ -913,7 +980,12 @@ std::vector<int4> fdm_plan(std::vector<FdmClassDev>& cls, int p, int nsm, FdmLau
     const char* gk = std::getenv("HTG_FDM_GROUPK");
     const char* tk = std::getenv("HTG_FDM_TEAM");
     L.nwarps = 0;
-    L.team = (tk && tk[0] == '1') ? 1 : 2;
+    // team size: 2 warps; 4 when an SM gets few subdomains (cfg3: 17 per SM), where
+    // the time is the latency of a team's last subdomains, not the DMMA pipe
+    // (HTG_FDM_TEAM=1/2/4 forces it)
+    const int per_sm = (total + std::max(nsm, 1) - 1) / std::max(nsm, 1);
+    L.team = per_sm < kFdmTeam4Below ? 4 : 2;
+    if (tk && (tk[0] == '1' || tk[0] == '2' || tk[0] == '4')) L.team = tk[0] - '0';
     if (!(gk && gk[0] == '1')) {
         const int KP = p == 2 ? 4 * FdmDims<2>::KS : 4 * FdmDims<4>::KS;
         int wfac = 0;
