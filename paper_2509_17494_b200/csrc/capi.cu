@@ -355,6 +355,7 @@ void build_handle(htg_handle* H, const htg_problem& prob, const htg_config& cfg)
             H->fdm_launch.classes = M.upload(H->fdm, st);
             H->fdm_launch.work = M.upload(work, st);
             H->fdm_launch.nwork = int(work.size());
+            fdm_format(H->fdm, hp.p, H->fdm_launch, M.ptrs, M.bytes, st);
         }
     }
     clk.mark("subdomain upload");

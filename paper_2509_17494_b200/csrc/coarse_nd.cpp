@@ -489,11 +489,11 @@ void factor_node(NDTree& t, int id, const LatticeMatrix& A, std::vector<int>& rp
     n.F = F;
     n.ke = ke;
     n.rc.assign(F, -1);  // right-hand side entries injected at this front: own-var rows
-    {
-        std::vector<char> own(size_t(t.nv), 0);
-        for (int v : n.vars) own[v] = 1;
+    {  // own variables marked in the (idle) column scratch map
+        for (int v : n.vars) cpos[v] = 0;
         for (int i = 0; i < F; ++i)
-            if (own[rows[i]]) n.rc[i] = rows[i];
+            if (cpos[rows[i]] == 0) n.rc[i] = rows[i];
+        for (int v : n.vars) cpos[v] = -1;
     }
     // Now rows [0, ke): unit L11 (cols < ke), U11 (cols >= row, < ke), U12 (cols >= ke);
     //     rows [ke, F): L21 (cols < ke), S (cols >= ke) -- the contribution block.
@@ -549,8 +549,10 @@ void nd_factor(const LatticeMatrix& A, NDTree& t, int leaf_max, double pivtol) {
     const int nthr = std::max(1, int(std::thread::hardware_concurrency()));
     std::vector<std::vector<int>> bydepth(t.max_depth + 1);
     for (int i = 0; i < int(t.nodes.size()); ++i) bydepth[t.nodes[i].depth].push_back(i);
+    const bool times = std::getenv("HTG_ND_TIMES") != nullptr;
     for (int d = t.max_depth; d >= 0; --d) {
         const auto& ids = bydepth[d];
+        const auto td0 = std::chrono::steady_clock::now();
         if (int(ids.size()) >= nthr) {
             std::vector<std::thread> th;
             std::vector<std::exception_ptr> errs(nthr);
@@ -584,6 +586,12 @@ void nd_factor(const LatticeMatrix& A, NDTree& t, int leaf_max, double pivtol) {
             for (auto& x : th) x.join();
             for (auto& e : errs)
                 if (e) std::rethrow_exception(e);
+        }
+        if (times) {
+            int fmax = 0;
+            for (int id : ids) fmax = std::max(fmax, t.nodes[id].F);
+            std::fprintf(stderr, "htg nd: depth %2d fronts %6d max F %5d  %.3f s\n", d, int(ids.size()), fmax,
+                         std::chrono::duration<double>(std::chrono::steady_clock::now() - td0).count());
         }
         for (int id : ids) {
             const NDNode& n = t.nodes[id];

@@ -110,6 +110,13 @@ constexpr bool kDataRem = HTG_FDM_DR != 0;  // data-row remainders on the CUDA c
 #define HTG_FDM_4M 0
 #endif
 constexpr bool kF4M = HTG_FDM_4M != 0;
+// HTG_FDM_SWAPB: products whose factor is the B operand (C[data][factor]) are issued
+// as the transposed product with the factor as A (C'[factor][data]); only the
+// epilogue's index interpretation changes
+#ifndef HTG_FDM_SWAPB
+#define HTG_FDM_SWAPB 0
+#endif
+constexpr bool kSwapB = HTG_FDM_SWAPB != 0;
 // the stationary operand's auxiliary value: Re + Im (3M) or -Im (4M, a sign flip
 // on the integer pipe)
 __device__ __forceinline__ double stat_aux(double2 v) {
@@ -130,7 +137,7 @@ struct Stage {
     __device__ __forceinline__ double2 fval(int f, int k) const { return FTR ? fac[k * LD + fo + f] : fac[f * LD + k]; }
 
     using Acc = double[kKP][kTG][2];
-    template <int NTL, class Epi>
+    template <int NTL, bool SA, class Epi>
     __device__ __forceinline__ void finish(Acc& t1, Acc& t2, Acc& t3, const int* tm, const int* tn, Epi& epi) const {
         const int r = lane >> 2, kq = lane & 3;
 #pragma unroll
@@ -144,7 +151,10 @@ struct Stage {
                     a2 += t2[h][j][i];
                     a3 += t3[h][j][i];
                 }
-                epi(tm[j] * 8 + frow_perm(r), tn[j] * 8 + frow_perm(2 * kq + i), make_double2(a1 - a2, a3 - a1 - a2));
+                if (kSwapB && !SA)
+                    epi(tm[j] * 8 + frow_perm(2 * kq + i), tn[j] * 8 + frow_perm(r), make_double2(a1 - a2, a3 - a1 - a2));
+                else
+                    epi(tm[j] * 8 + frow_perm(r), tn[j] * 8 + frow_perm(2 * kq + i), make_double2(a1 - a2, a3 - a1 - a2));
             }
     }
     template <int NTL>
@@ -214,21 +224,21 @@ struct Stage {
             }
 #pragma unroll
             for (int j = 0; j < NTL; ++j) {
-                if (SA) dmma(t1[h][j][0], t1[h][j][1], sf[ks].x, v[j].x);
+                if (SA || kSwapB) dmma(t1[h][j][0], t1[h][j][1], sf[ks].x, v[j].x);
                 else dmma(t1[h][j][0], t1[h][j][1], v[j].x, sf[ks].x);
             }
 #pragma unroll
             for (int j = 0; j < NTL; ++j) {
-                if (SA) dmma(t2[h][j][0], t2[h][j][1], sf[ks].y, v[j].y);
+                if (SA || kSwapB) dmma(t2[h][j][0], t2[h][j][1], sf[ks].y, v[j].y);
                 else dmma(t2[h][j][0], t2[h][j][1], v[j].y, sf[ks].y);
             }
 #pragma unroll
             for (int j = 0; j < NTL; ++j) {
-                if (SA) dmma(t3[h][j][0], t3[h][j][1], ss[ks], vs[j]);
+                if (SA || kSwapB) dmma(t3[h][j][0], t3[h][j][1], ss[ks], vs[j]);
                 else dmma(t3[h][j][0], t3[h][j][1], vs[j], ss[ks]);
             }
         }
-        finish<NTL>(t1, t2, t3, tm, tn, epi);
+        finish<NTL, SA>(t1, t2, t3, tm, tn, epi);
     }
 
     // run_stat for the tile count nt <= N (compile-time tile counts)
@@ -641,6 +651,9 @@ struct WStage {
 #define HTG_FDM_TTHREADS 512
 #endif
 constexpr int kWThreads(int p, int np) { return (np == 1 && p == 4) ? 256 : (np == 2 && p == 4 ? HTG_FDM_TTHREADS : 512); }
+// CTA sizes the team kernel is instantiated for, per team size (the launch picks the
+// smallest one that holds the planned warps; the register budget follows the size)
+constexpr int kWSizes[5][2] = {{0, 0}, {256, 512}, {384, 512}, {480, 576}, {512, 512}};
 
 #ifndef HTG_FDM_SYM_CODE
 #define HTG_FDM_SYM_CODE 1  // 0: compile the team kernel without the mirror-symmetric path
@@ -656,102 +669,156 @@ __device__ __forceinline__ void team_sync(int team) {
     else asm volatile("bar.sync %0, %1;\n" ::"r"(team + 1), "r"(NP * 32) : "memory");
 }
 
-template <int P, int NP>
-__global__ void __launch_bounds__(kWThreads(P, NP), 1)
+// One class's factor region in the layout the team kernel keeps in shared memory
+// (generic: Vx^T, Vy^T; mirror-symmetric classes: the parity blocks and mirror tables).
+template <int P>
+__global__ void __launch_bounds__(256) k_fdm_format(const FdmClassDev* __restrict__ classes, double2* __restrict__ image,
+                                                   int2* __restrict__ pos_tab, int fac_elems) {
+    constexpr int LD = FdmDims<P>::LD, KS = FdmDims<P>::KS, KP = 4 * KS;
+    const FdmClassDev c = classes[blockIdx.x];
+    double2* fac = image + size_t(blockIdx.x) * fac_elems;
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    double2* V1T = fac;
+    double2* V2T = V1T + KP * LD;
+    double2* D = V2T + KP * LD;
+    const int nx = c.nx, ny = c.ny, nux = c.nux, nuy = c.nuy;
+    int* urow = reinterpret_cast<int*>(D + nx * ny);
+    int* gofs = urow + nux * nuy;
+    int* gpos = gofs + nx * ny;
+    (void)V1T;
+    const double2 z = make_double2(0.0, 0.0);
+    const bool sym = HTG_FDM_SYM_CODE && (P == 4) && c.sym;
+    // mirror tables of a symmetric class (after the gather tables):
+    // bfn[r]: natural rows of reordered row r; ubn[n]: reordered rows of natural row n
+    int* bfn = gpos + nx * ny;
+    int* ubn = bfn + 32;
+    if (sym) {
+        // V1T: rows [0, 16) Ve^T (13 x 13), rows [16, 28) Vo^T (12 x 12); same for V2T
+        for (int i = tid; i < 2 * KP * LD; i += nthr) {
+            const int a0 = i / LD, b = i - a0 * LD, dir = a0 / KP, a = a0 - dir * KP;
+            const double2* Ve = dir ? c.Vye : c.Vxe;
+            const double2* Vo = dir ? c.Vyo : c.Vxo;
+            double2 v = z;
+            if (a < 16) v = (a < 13 && b < 13) ? Ve[b * 13 + a] : z;
+            else v = (a - 16 < 12 && b < 12) ? Vo[b * 12 + (a - 16)] : z;
+            fac[i] = v;
+        }
+        if (tid < 25) {
+            // reordered r -> natural: r < 12 pair g = r (n1 = g, n2 = R(g), +s); r = 12 centre;
+            // r >= 13 odd pair g = r - 13 (-s). packed n1 | n2 << 8 | sign bit << 16 (bit set: -)
+            const int r = tid;
+            int code;
+            if (r == 12) code = 12 | (255 << 8);
+            else {
+                const int gg = r < 12 ? r : r - 13, m = c.mir[gg];
+                const bool spos = (m >> 16) & 1;
+                const bool neg = r < 12 ? !spos : spos;
+                code = gg | ((m & 0xffff) << 8) | (neg ? 1 << 16 : 0);
+            }
+            bfn[r] = code;
+            // natural n -> (pair g, form): n < 12: (e_g + o_g)/r2; n = 12: e_c; n > 12:
+            // s_g (e_g - o_g)/r2 with R(g) = n. packed g | form << 8 (0 plus, 1 centre, 2 s>0, 3 s<0)
+            const int n = tid;
+            int ucode = 12 | (1 << 8);
+            if (n < 12) ucode = n;
+            else if (n > 12)
+                for (int gg = 0; gg < 12; ++gg)
+                    if ((c.mir[gg] & 0xffff) == n) ucode = gg | ((((c.mir[gg] >> 16) & 1) ? 2 : 3) << 8);
+            ubn[n] = ucode;
+        }
+    } else {
+        for (int i = tid; i < 2 * KP * LD; i += nthr) {
+            const int a = i / LD, b = i - a * LD;
+            double2 v = z;
+            if (a < KP) v = (a < nx && b < nx) ? c.Vx[b * nx + a] : z;
+            else v = (a - KP < ny && b < ny) ? c.Vy[b * ny + (a - KP)] : z;
+            fac[i] = v;
+        }
+    }
+    for (int i = tid; i < nx * ny; i += nthr) D[i] = c.Dinv[i];
+    for (int i = tid; i < nux * nuy; i += nthr) {
+        const int ixu = i / nuy, iyu = i - ixu * nuy;
+        urow[i] = c.rowmap[dof_index(c.onx, c.ony, P, c.ux0 + ixu, c.uy0 + iyu)];
+    }
+    if (c.goff)
+        for (int i = tid; i < nx * ny; i += nthr) {
+            const int e = c.gord[i], iy = e / nx;
+            gofs[i] = c.goff[e];
+            gpos[i] = iy * LD + (e - iy * nx);
+        }
+    for (int j = tid; j < c.nsub; j += nthr) {
+        const int id = c.subs[j];
+        pos_tab[c.first + j] = make_int2(id, c.sub_o[id]);
+    }
+}
+
+// HTG_FDM_TRACE: per-team clock64 accounting of the generic path (CTAs 0 and 1 print)
+#ifdef HTG_FDM_TRACE
+#define HTG_TR(i)                                  \
+    do {                                           \
+        const long long t_ = clock64();            \
+        tr_acc[i] += t_ - tr_last;                 \
+        tr_last = t_;                              \
+    } while (0)
+#else
+#define HTG_TR(i) \
+    do {          \
+    } while (0)
+#endif
+
+template <int P, int NP, int NT>
+__global__ void __launch_bounds__(NT, 1)
     k_dd_fdm_w(FineGeom g, const FdmClassDev* __restrict__ classes, const int4* __restrict__ work,
-               const double2* __restrict__ r, double2* __restrict__ ystage, int nu_max, int rows, int fac_elems) {
+               const double2* __restrict__ image, const int2* __restrict__ pos_tab, const double2* __restrict__ r,
+               double2* __restrict__ ystage, int nu_max, int rows, int fac_elems) {
     constexpr int LD = FdmDims<P>::LD, KS = FdmDims<P>::KS, KP = 4 * KS;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double2* fac = reinterpret_cast<double2*>(smem_raw);
     const int tid = threadIdx.x, nthr = blockDim.x, nteam = nthr / (32 * NP);
     const int warp = tid >> 5, lane = tid & 31, team = warp / NP, part = warp - team * NP;
     const int tl = part * 32 + lane;                               // lane within the team
+#ifdef HTG_FDM_TRACE
+    long long tr_acc[8] = {}, tr_last = clock64();
+    const long long tr_t0 = tr_last;
+    int tr_n = 0;
+#endif
     double2* X = fac + fac_elems + size_t(team) * 2 * rows * LD;  // gathered tile, then Q o Dinv
     double2* W = X + rows * LD;                                   // stage 1 / stage 3 products
-    {  // the k padding of the data buffers must be finite: zero them once
-        double2* data = fac + fac_elems;
-        for (int i = tid; i < nteam * 2 * rows * LD; i += nthr) data[i] = make_double2(0.0, 0.0);
-    }
     double2* V1T = fac;            // [ix'][ix] = Vx[ix][ix'], KP rows (rows >= nx zero)
     double2* V2T = V1T + KP * LD;  // [iy'][iy] = Vy[iy][iy']
     double2* D = V2T + KP * LD;    // Dinv[ix'][iy']
-    const int4 wk = work[blockIdx.x];
-    int pos = wk.x;
+    const int4 wk = work[blockIdx.x];  // [first, end) of the class-sorted list, class of first
+    int pos = wk.x, ci = wk.z;
+    // the class's factor region (formatted once by k_fdm_format) -> shared memory, asynchronously
+    auto copy_image = [&](int cls) {
+        const double2* src = image + size_t(cls) * fac_elems;
+        for (int i = tid; i < fac_elems; i += nthr) cp_async16(&fac[i], src + i);
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    copy_image(ci);
+    {  // the k padding of the data buffers must be finite: zero them once (under the copy)
+        double2* data = fac + fac_elems;
+        for (int i = tid; i < nteam * 2 * rows * LD; i += nthr) data[i] = make_double2(0.0, 0.0);
+    }
     while (pos < wk.y) {
-        int ci = 0;
-        while (classes[ci].first + classes[ci].nsub <= pos) ++ci;
-        const FdmClassDev c = classes[ci];
+        const FdmClassDev c = classes[ci];  // holds pos (work table; ++ci at the segment's end)
         const int seg_end = min(wk.y, c.first + c.nsub);
         const int nx = c.nx, ny = c.ny, nux = c.nux, nuy = c.nuy;
         int* urow = reinterpret_cast<int*>(D + nx * ny);
         int* gofs = urow + nux * nuy;  // gather: dof offsets in memory order ...
         int* gpos = gofs + nx * ny;    // ... and the tile slot each one lands in
-        __syncthreads();  // previous segment finished with the factors
-        const double2 z = make_double2(0.0, 0.0);
         const bool sym = HTG_FDM_SYM_CODE && (P == 4) && c.sym;
         // mirror tables of a symmetric class (after the gather tables):
         // bfn[r]: natural rows of reordered row r; ubn[n]: reordered rows of natural row n
         int* bfn = gpos + nx * ny;
         int* ubn = bfn + 32;
-        if (sym) {
-            // V1T: rows [0, 16) Ve^T (13 x 13), rows [16, 28) Vo^T (12 x 12); same for V2T
-            for (int i = tid; i < 2 * KP * LD; i += nthr) {
-                const int a0 = i / LD, b = i - a0 * LD, dir = a0 / KP, a = a0 - dir * KP;
-                const double2* Ve = dir ? c.Vye : c.Vxe;
-                const double2* Vo = dir ? c.Vyo : c.Vxo;
-                double2 v = z;
-                if (a < 16) v = (a < 13 && b < 13) ? Ve[b * 13 + a] : z;
-                else v = (a - 16 < 12 && b < 12) ? Vo[b * 12 + (a - 16)] : z;
-                fac[i] = v;
-            }
-            if (tid < 25) {
-                // reordered r -> natural: r < 12 pair g = r (n1 = g, n2 = R(g), +s); r = 12 centre;
-                // r >= 13 odd pair g = r - 13 (-s). packed n1 | n2 << 8 | sign bit << 16 (bit set: -)
-                const int r = tid;
-                int code;
-                if (r == 12) code = 12 | (255 << 8);
-                else {
-                    const int gg = r < 12 ? r : r - 13, m = c.mir[gg];
-                    const bool spos = (m >> 16) & 1;
-                    const bool neg = r < 12 ? !spos : spos;
-                    code = gg | ((m & 0xffff) << 8) | (neg ? 1 << 16 : 0);
-                }
-                bfn[r] = code;
-                // natural n -> (pair g, form): n < 12: (e_g + o_g)/r2; n = 12: e_c; n > 12:
-                // s_g (e_g - o_g)/r2 with R(g) = n. packed g | form << 8 (0 plus, 1 centre, 2 s>0, 3 s<0)
-                const int n = tid;
-                int ucode = 12 | (1 << 8);
-                if (n < 12) ucode = n;
-                else if (n > 12)
-                    for (int gg = 0; gg < 12; ++gg)
-                        if ((c.mir[gg] & 0xffff) == n) ucode = gg | ((((c.mir[gg] >> 16) & 1) ? 2 : 3) << 8);
-                ubn[n] = ucode;
-            }
-        } else {
-            for (int i = tid; i < 2 * KP * LD; i += nthr) {
-                const int a = i / LD, b = i - a * LD;
-                double2 v = z;
-                if (a < KP) v = (a < nx && b < nx) ? c.Vx[b * nx + a] : z;
-                else v = (a - KP < ny && b < ny) ? c.Vy[b * ny + (a - KP)] : z;
-                fac[i] = v;
-            }
-        }
-        for (int i = tid; i < nx * ny; i += nthr) D[i] = c.Dinv[i];
-        for (int i = tid; i < nux * nuy; i += nthr) {
-            const int ixu = i / nuy, iyu = i - ixu * nuy;
-            urow[i] = c.rowmap[dof_index(c.onx, c.ony, P, c.ux0 + ixu, c.uy0 + iyu)];
-        }
-        if (c.goff)
-            for (int i = tid; i < nx * ny; i += nthr) {
-                const int e = c.gord[i], iy = e / nx;
-                gofs[i] = c.goff[e];
-                gpos[i] = iy * LD + (e - iy * nx);
-            }
+        int cur = pos + team;
+        int2 pt = cur < seg_end ? pos_tab[cur] : make_int2(0, 0);  // (subdomain id, Omega origin)
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
         __syncthreads();
         const int nxy = nx * ny;
         const float inv_nx = 1.0f / nx;
-        auto gather = [&](int sidx) {
-            const int so = c.sub_o[c.subs[sidx - c.first]];
+        auto gather = [&](int so) {
             const int ox = (so & 0xffff) * P, oy = (so >> 16) * P;
             if (c.goff) {
                 const double2* rb = r + dof_index(g.nx, g.ny, P, ox, oy);
@@ -764,13 +831,15 @@ __global__ void __launch_bounds__(kWThreads(P, NP), 1)
             }
             asm volatile("cp.async.commit_group;\n" ::: "memory");
         };
-        int cur = pos + team;
-        if (cur < seg_end) gather(cur);
+        HTG_TR(0);  // segment setup (factor image)
+        if (cur < seg_end) gather(pt.y);
         if constexpr (P == 4) {
             if (sym) {
                 constexpr double r2 = 0.70710678118654752440;
                 for (; cur < seg_end; cur += nteam) {
-                    const int id = c.subs[cur - c.first];
+                    const int id = pt.x;
+                    const bool more = cur + nteam < seg_end;
+                    if (more) pt = pos_tab[cur + nteam];
                     asm volatile("cp.async.wait_all;\n" ::: "memory");
                     team_sync<NP>(team);
                     // mirror butterflies in x and y: G[iy][ix] (natural) -> W[iy_r][ix_r]
@@ -843,7 +912,7 @@ __global__ void __launch_bounds__(kWThreads(P, NP), 1)
                         });
                     team_sync<NP>(team);
                     // the gathered tile is free: fetch the team's next subdomain under the unbutterfly
-                    if (cur + nteam < seg_end) gather(cur + nteam);
+                    if (more) gather(pt.y);
                     // inverse butterflies on the U block -> staging row of the subdomain
                     double2* yrow = ystage + (size_t)id * nu_max;
                     for (int e = tl; e < 289; e += NP * 32) {
@@ -876,18 +945,31 @@ __global__ void __launch_bounds__(kWThreads(P, NP), 1)
                 }
                 asm volatile("cp.async.wait_all;\n" ::: "memory");
                 pos = seg_end;
+                ++ci;
+                if (pos < wk.y) {
+                    __syncthreads();  // every team finished with the factors
+                    copy_image(ci);
+                }
                 continue;
             }
         }
         for (; cur < seg_end; cur += nteam) {
-            const int id = c.subs[cur - c.first];
+            const int id = pt.x;
+            const bool more = cur + nteam < seg_end;
+            if (more) pt = pos_tab[cur + nteam];  // next subdomain of the team, used at stage 4
+            HTG_TR(1);
             asm volatile("cp.async.wait_all;\n" ::: "memory");
             team_sync<NP>(team);
+            HTG_TR(2);  // gather wait
+#ifdef HTG_FDM_TRACE
+            ++tr_n;
+#endif
             // 1: P[ix'][iy] = sum_ix Vx[ix][ix'] G[iy][ix]  -> W[ix'][iy]
             WStage<LD, KS, false>{V1T, nx, 0, X, ny, true, lane, part, NP}([&](int m, int n, double2 v) {
                 if (m < nx && n < ny) W[m * LD + n] = v;
             });
             team_sync<NP>(team);
+            HTG_TR(3);
             // 2: Q[ix'][iy'] = (sum_iy P[ix'][iy] Vy[iy][iy']) Dinv[ix'][iy']  -> X[iy'][ix']
             WStage<LD, KS, false>{V2T, ny, 0, W, nx, false, lane, NP - 1 - part, NP}([&](int m, int n, double2 v) {
                 if (m < nx && n < ny) {
@@ -896,23 +978,37 @@ __global__ void __launch_bounds__(kWThreads(P, NP), 1)
                 }
             });
             team_sync<NP>(team);
+            HTG_TR(4);
             // 3: R[ixu][iy'] = sum_ix' Vx[ux0 + ixu][ix'] Q[iy'][ix']  -> W[ixu][iy']
             WStage<LD, KS, true>{V1T, nux, c.ux0, X, ny, true, lane, part, NP}([&](int m, int n, double2 v) {
                 if (m < nux && n < ny) W[m * LD + n] = v;
             });
             team_sync<NP>(team);
+            HTG_TR(5);
             // the gathered tile is free: fetch the team's next subdomain under stage 4
-            if (cur + nteam < seg_end) gather(cur + nteam);
+            if (more) gather(pt.y);
             // 4: Y[ixu][iyu] = sum_iy' R[ixu][iy'] Vy[uy0 + iyu][iy']  -> staging row of the subdomain
             double2* yrow = ystage + (size_t)id * nu_max;
             WStage<LD, KS, true>{V2T, nuy, c.uy0, W, nux, false, lane, NP - 1 - part, NP}(
                 [&](int m, int n, double2 v) {
                     if (m < nux && n < nuy) yrow[urow[m * nuy + n]] = v;
                 });
+            HTG_TR(6);
         }
         asm volatile("cp.async.wait_all;\n" ::: "memory");
         pos = seg_end;
+        ++ci;
+        if (pos < wk.y) {
+            __syncthreads();  // every team finished with the factors
+            copy_image(ci);
+        }
     }
+#ifdef HTG_FDM_TRACE
+    if (lane == 0 && (blockIdx.x == 0 || blockIdx.x == 70))
+        printf("fdm trace cta %d team %d part %d: n %d total %lld | setup %lld loop %lld wait %lld s1 %lld s2 %lld s3 %lld s4 %lld\n",
+               blockIdx.x, team, part, tr_n, clock64() - tr_t0, tr_acc[0], tr_acc[1], tr_acc[2], tr_acc[3], tr_acc[4],
+               tr_acc[5], tr_acc[6]);
+#endif
 }
 
 }  // namespace
@@ -926,7 +1022,7 @@ void dd_fdm_launch(const FineGeom& g, const FdmLaunch& L, const double2* r, doub
                    cudaStream_t st) {
     if (L.nwork == 0) return;
     static bool attr[9] = {};
-    static bool attr_w[9] = {};
+    static bool attr_w[12] = {};
     auto go = [&](auto kern, int p) {
         if (!attr[p]) {
             HTG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
@@ -939,16 +1035,29 @@ void dd_fdm_launch(const FineGeom& g, const FdmLaunch& L, const double2* r, doub
             HTG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
             attr_w[slot] = true;
         }
-        kern<<<L.nwork, L.nwarps * 32, L.smem, st>>>(g, L.classes, L.work, r, ystage, nu_max, L.rows, L.fac_elems);
+        kern<<<L.nwork, L.nwarps * 32, L.smem, st>>>(g, L.classes, L.work, L.image, L.pos_tab, r, ystage, nu_max,
+                                                     L.rows, L.fac_elems);
     };
     if (L.nwarps > 0) {
+        const bool small = L.nwarps * 32 <= kWSizes[L.team][0];
         switch (g.p * 8 + L.team) {
-            case 17: go_w(k_dd_fdm_w<2, 1>, 1); break;
-            case 18: go_w(k_dd_fdm_w<2, 2>, 0); break;
-            case 20: go_w(k_dd_fdm_w<2, 4>, 4); break;
-            case 33: go_w(k_dd_fdm_w<4, 1>, 3); break;
-            case 34: go_w(k_dd_fdm_w<4, 2>, 2); break;
-            case 36: go_w(k_dd_fdm_w<4, 4>, 5); break;
+            case 17: go_w(k_dd_fdm_w<2, 1, 512>, 1); break;
+            case 18: go_w(k_dd_fdm_w<2, 2, 512>, 0); break;
+            case 19: go_w(k_dd_fdm_w<2, 3, 576>, 6); break;
+            case 20: go_w(k_dd_fdm_w<2, 4, 512>, 4); break;
+            case 33:
+                if (small) go_w(k_dd_fdm_w<4, 1, kWSizes[1][0]>, 3);
+                else go_w(k_dd_fdm_w<4, 1, kWSizes[1][1]>, 7);
+                break;
+            case 34:
+                if (small) go_w(k_dd_fdm_w<4, 2, kWSizes[2][0]>, 8);
+                else go_w(k_dd_fdm_w<4, 2, kWSizes[2][1]>, 2);
+                break;
+            case 35:
+                if (small) go_w(k_dd_fdm_w<4, 3, kWSizes[3][0]>, 9);
+                else go_w(k_dd_fdm_w<4, 3, kWSizes[3][1]>, 10);
+                break;
+            case 36: go_w(k_dd_fdm_w<4, 4, 512>, 5); break;
             default: throw InvalidArgument("FDM subdomain kernel: p must be 2 or 4");
         }
     } else {
@@ -980,12 +1089,17 @@ std::vector<int4> fdm_plan(std::vector<FdmClassDev>& cls, int p, int nsm, FdmLau
     const char* gk = std::getenv("HTG_FDM_GROUPK");
     const char* tk = std::getenv("HTG_FDM_TEAM");
     L.nwarps = 0;
-    // team size: 2 warps; 4 when an SM gets few subdomains (cfg3: 17 per SM), where
-    // the time is the latency of a team's last subdomains, not the DMMA pipe
-    // (HTG_FDM_TEAM=1/2/4 forces it)
+    // team size: 2 warps (8 teams at p = 4); when an SM gets few subdomains (cfg3: 17
+    // per SM) the time is the latency of a team's chain of subdomains, not the DMMA
+    // pipe: five 3-warp teams (a product's 9 / 6 tiles split evenly over 3 warps)
+    // take 75.8 us at cfg3 against 80.2 (four 4-warp teams) and 82.3 (eight 2-warp
+    // teams). HTG_FDM_TEAM=1..4 / HTG_FDM_NTEAMS force the shape.
     const int per_sm = (total + std::max(nsm, 1) - 1) / std::max(nsm, 1);
-    L.team = per_sm < kFdmTeam4Below ? 4 : 2;
-    if (tk && (tk[0] == '1' || tk[0] == '2' || tk[0] == '4')) L.team = tk[0] - '0';
+    const bool few = per_sm < kFdmTeam4Below;
+    L.team = few ? (p == 4 ? 3 : 4) : 2;
+    if (tk && tk[0] >= '1' && tk[0] <= '4') L.team = tk[0] - '0';
+    const char* ntk = std::getenv("HTG_FDM_NTEAMS");  // teams per CTA (default: as many as fit)
+    const int nt_default = (few && p == 4 && L.team == 3) ? 5 : 1 << 20;  // 480 threads: 128 registers
     if (!(gk && gk[0] == '1')) {
         const int KP = p == 2 ? 4 * FdmDims<2>::KS : 4 * FdmDims<4>::KS;
         int wfac = 0;
@@ -994,8 +1108,9 @@ std::vector<int4> fdm_plan(std::vector<FdmClassDev>& cls, int p, int nsm, FdmLau
         wfac = (wfac + 7) / 8 * 8;
         const int per_warp = 2 * ext * LD;
         int nt = (kSmemMax / int(sizeof(double2)) - wfac) / per_warp;  // teams (buffer pairs)
-        nt = std::min(nt, kWThreads(p, L.team) / (32 * L.team));
-        if (nt * L.team >= 8) nt = (nt * L.team) / 4 * 4 / L.team;  // whole warps per SM sub-partition
+        nt = std::min(nt, (p == 4 ? kWSizes[L.team][1] : (L.team == 3 ? 576 : 512)) / (32 * L.team));
+        if (L.team != 3 && nt * L.team >= 8) nt = (nt * L.team) / 4 * 4 / L.team;  // whole warps per SM sub-partition
+        nt = std::min(nt, (ntk && std::atoi(ntk) >= 1) ? std::atoi(ntk) : nt_default);
         if (nt >= 1) {
             L.nwarps = nt * L.team;
             L.fac_elems = wfac;
@@ -1015,9 +1130,35 @@ std::vector<int4> fdm_plan(std::vector<FdmClassDev>& cls, int p, int nsm, FdmLau
     const int ctas = std::min(nsm, total);
     for (int i = 0; i < ctas; ++i) {
         const int a = int((long long)total * i / ctas), b = int((long long)total * (i + 1) / ctas);
-        if (b > a) work.push_back(make_int4(a, b, 0, 0));
+        if (b > a) {
+            int ci = 0;
+            while (cls[ci].first + cls[ci].nsub <= a) ++ci;
+            work.push_back(make_int4(a, b, ci, 0));
+        }
     }
     return work;
+}
+
+void fdm_format(const std::vector<FdmClassDev>& cls, int p, FdmLaunch& L, std::vector<void*>& allocs, size_t& bytes,
+                cudaStream_t st) {
+    if (cls.empty() || L.nwarps == 0) return;
+    for (const FdmClassDev& c : cls)
+        if (c.nsub == 0) throw RuntimeError("FDM subdomain kernel: empty class");
+    int total = 0;
+    for (const FdmClassDev& c : cls) total += c.nsub;
+    void *img = nullptr, *pt = nullptr;
+    const size_t ib = cls.size() * size_t(L.fac_elems) * sizeof(double2), pb = size_t(total) * sizeof(int2);
+    HTG_CUDA(cudaMalloc(&img, ib));
+    allocs.push_back(img);
+    HTG_CUDA(cudaMalloc(&pt, pb));
+    allocs.push_back(pt);
+    bytes += ib + pb;
+    HTG_CUDA(cudaMemsetAsync(img, 0, ib, st));
+    if (p == 2) k_fdm_format<2><<<unsigned(cls.size()), 256, 0, st>>>(L.classes, static_cast<double2*>(img), static_cast<int2*>(pt), L.fac_elems);
+    else k_fdm_format<4><<<unsigned(cls.size()), 256, 0, st>>>(L.classes, static_cast<double2*>(img), static_cast<int2*>(pt), L.fac_elems);
+    HTG_CUDA(cudaGetLastError());
+    L.image = static_cast<const double2*>(img);
+    L.pos_tab = static_cast<const int2*>(pt);
 }
 
 }  // namespace htg

@@ -122,7 +122,16 @@ struct FdmLaunch {
     size_t smem;                 // dynamic shared memory per CTA
     int nwarps = 0;              // > 0: team-per-subdomain kernel with this many warps per CTA
     int team = 2;                // warps per subdomain of that kernel
+    // team kernel: per class, the factor region exactly as the kernel keeps it in shared
+    // memory (fac_elems double2: Vx^T, Vy^T padded, Dinv, U-row and gather tables), and
+    // per position of the class-sorted list (subdomain id, Omega origin); formatted on
+    // the device once (fdm_format), so a CTA's prologue is one coalesced copy
+    const double2* image = nullptr;
+    const int2* pos_tab = nullptr;
 };
+// fills L.image / L.pos_tab (L.classes, L.work uploaded; cls = the host copy of the table)
+void fdm_format(const std::vector<FdmClassDev>& cls, int p, FdmLaunch& L, std::vector<void*>& allocs, size_t& bytes,
+                cudaStream_t st);
 void dd_fdm_launch(const FineGeom& g, const FdmLaunch& L, const double2* r, double2* ystage, int nu_max,
                    cudaStream_t st);
 std::vector<int4> fdm_plan(std::vector<FdmClassDev>& cls, int p, int nsm, FdmLaunch& L);
