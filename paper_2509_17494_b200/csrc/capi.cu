@@ -5,6 +5,7 @@
 // consumes is built once on the host and uploaded to HBM; every call after
 // that is a sequence of stream-ordered kernel launches with no allocation.
 #include <cuda_runtime.h>
+#include <thread>
 
 #include <chrono>
 #include <cstdio>
@@ -307,6 +308,32 @@ void build_handle(htg_handle* H, const htg_problem& prob, const htg_config& cfg)
         }
         clk.mark("triangle operators (CSR)");
     }
+    // The coarse factorization (host threads + its own upload stream) runs beside the
+    // subdomain setup; joined where the coarse solver is first needed.
+    std::thread coarse_thread;
+    std::exception_ptr coarse_err;
+    if (cfg.coarsening == HTG_COARSE_OPTIMIZED_FD) {
+        int dev = 0;
+        HTG_CUDA(cudaGetDevice(&dev));
+        coarse_thread = std::thread([H, &hp, &coarse_err, dev] {
+            try {
+                HTG_CUDA(cudaSetDevice(dev));
+                cudaStream_t cs = nullptr;
+                HTG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+                H->coarse = make_coarse_solver(hp, cs);
+                HTG_CUDA(cudaStreamSynchronize(cs));
+                cudaStreamDestroy(cs);
+            } catch (...) {
+                coarse_err = std::current_exception();
+            }
+        });
+    }
+    struct Joiner {  // an exception in the subdomain setup must not leave the thread running
+        std::thread& t;
+        ~Joiner() {
+            if (t.joinable()) t.join();
+        }
+    } coarse_join{coarse_thread};
     if (cfg.smoother == HTG_SMOOTHER_CSDD) {
         clk.mark("problem, vectors");
         DDSetup dd = build_dd(hp, H->basis, cfg.alpha_s, cfg.l_dd);
@@ -359,8 +386,9 @@ void build_handle(htg_handle* H, const htg_problem& prob, const htg_config& cfg)
         }
     }
     clk.mark("subdomain upload");
-    if (cfg.coarsening == HTG_COARSE_OPTIMIZED_FD) H->coarse = make_coarse_solver(hp, st);
-    clk.mark("coarse factor + upload");
+    if (coarse_thread.joinable()) coarse_thread.join();
+    if (coarse_err) std::rethrow_exception(coarse_err);
+    clk.mark("coarse factor + upload (wait)");
     if (cfg.coarsening == HTG_COARSE_GALERKIN_P) {
         // proj/core/src/twogrid.cpp:189-219: order-p/2 space on the same mesh, A_c with
         // alpha_c, IP = inclusion of the hierarchical order-p/2 functions

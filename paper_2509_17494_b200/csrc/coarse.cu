@@ -426,7 +426,11 @@ class NDSolver : public CoarseSolver {
                          int(t.nodes.size()), t.max_front);
         nv_ = t.nv;
         delayed_ = t.delayed;
+        const auto t1 = std::chrono::steady_clock::now();
         upload(t, st);
+        if (std::getenv("HTG_SETUP_TIMES"))
+            std::fprintf(stderr, "htg setup:   factor upload + solve plan %8.3f s\n",
+                         std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count());
     }
     ~NDSolver() override {
         for (void* p : allocs_) cudaFree(p);
@@ -633,58 +637,74 @@ class NDSolver : public CoarseSolver {
         HTG_CUDA(cudaMalloc(&facp, std::max<long long>(1, fac_total) * sizeof(double2)));
         allocs_.push_back(facp);
         bytes_ += fac_total * sizeof(double2);
-        // all factor blocks go through one pinned staging buffer in large chunks
-        // (one cudaMemcpy per block took seconds at cfg4: 4 blocks x 68k fronts)
-        const size_t chunk = size_t(64) << 20;  // bytes
-        cplx* stage = nullptr;
-        HTG_CUDA(cudaMallocHost(&stage, chunk));
-        size_t fill = 0;        // bytes staged
-        long long dst0 = 0;     // factor offset (double2) of the staged run
-        auto flush = [&]() {
-            if (!fill) return;
-            HTG_CUDA(cudaMemcpy(static_cast<double2*>(facp) + dst0, stage, fill, cudaMemcpyHostToDevice));
-            dst0 += (long long)(fill / sizeof(cplx));
-            fill = 0;
-        };
-        for (int i = 0; i < nn; ++i) {
-            NDNode& n = t.nodes[i];
-            const NodeDev& d = nd[i];
-            // blocks are laid out back to back in node order (off_F, off_L, off_U, off_Z)
-            auto put = [&](std::vector<cplx>& v, long long off) {
-                if (dst0 + (long long)(fill / sizeof(cplx)) != off) {  // keep the staged run contiguous
-                    flush();
-                    dst0 = off;
-                }
-                size_t done = 0;
-                while (done < v.size()) {
-                    const size_t room = (chunk - fill) / sizeof(cplx);
-                    const size_t nput = std::min(room, v.size() - done);
-                    std::memcpy(reinterpret_cast<char*>(stage) + fill, v.data() + done, nput * sizeof(cplx));
-                    fill += nput * sizeof(cplx);
-                    done += nput;
-                    if (fill == chunk) flush();
-                }
-                std::vector<cplx>().swap(v);
-            };
-            if (d.s + d.u <= warpF) {  // warp tier: column-major blocks (cols_dot)
-                auto tr = [](std::vector<cplx>& M, int rows, int cols) {
-                    std::vector<cplx> T(M.size());
-                    for (int i = 0; i < rows; ++i)
-                        for (int k = 0; k < cols; ++k) T[size_t(k) * rows + i] = M[size_t(i) * cols + k];
-                    M.swap(T);
-                };
-                tr(n.Finv, d.s, d.s);
-                tr(n.L21, d.u, d.s);
-                tr(n.Uinv, d.s, d.s);
-                tr(n.Z, d.s, d.u);
+        // The factor blocks are laid out back to back in node order (off_F, off_L, off_U,
+        // off_Z). Runs of nodes of up to 64 MB are packed by all host threads into one of
+        // two pinned staging buffers (warp-tier blocks transposed on the way: column-major
+        // for cols_dot) and copied asynchronously, so packing overlaps the transfer
+        // (one cudaMemcpy per block took seconds at cfg4: 4 blocks x 68k fronts; one
+        // thread packing through one buffer 0.5 s).
+        {
+            const auto tp0 = std::chrono::steady_clock::now();
+            const size_t chunk = size_t(64) << 20;  // bytes
+            cplx* stage[2] = {nullptr, nullptr};
+            cudaEvent_t done[2];
+            for (int b = 0; b < 2; ++b) {
+                HTG_CUDA(cudaMallocHost(&stage[b], chunk));
+                HTG_CUDA(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming));
             }
-            put(n.Finv, d.off_F);
-            put(n.L21, d.off_L);
-            put(n.Uinv, d.off_U);
-            put(n.Z, d.off_Z);
+            auto node_end = [&](int i) { return nd[i].off_Z + (long long)nd[i].s * nd[i].u; };
+            const int nthr = std::max(1, int(std::thread::hardware_concurrency()));
+            int buf = 0;
+            for (int i0 = 0; i0 < nn;) {
+                const long long base = nd[i0].off_F;
+                int i1 = i0 + 1;
+                while (i1 < nn && size_t(node_end(i1) - base) * sizeof(cplx) <= chunk) ++i1;
+                const size_t bytes = size_t(node_end(i1 - 1) - base) * sizeof(cplx);
+                if (bytes > chunk) throw RuntimeError("coarse solve: a front's factors exceed the staging buffer");
+                HTG_CUDA(cudaEventSynchronize(done[buf]));  // the buffer's previous copy
+                cplx* dst = stage[buf];
+                std::atomic<int> next{i0};
+                auto pack = [&]() {
+                    for (int i; (i = next++) < i1;) {
+                        NDNode& n = t.nodes[i];
+                        const NodeDev& d = nd[i];
+                        const bool colmajor = d.s + d.u <= warpF;
+                        auto put = [&](std::vector<cplx>& v, long long off, int rows, int cols) {
+                            cplx* o = dst + (off - base);
+                            if (colmajor) {
+                                for (int r = 0; r < rows; ++r)
+                                    for (int k = 0; k < cols; ++k) o[size_t(k) * rows + r] = v[size_t(r) * cols + k];
+                            } else if (!v.empty()) {
+                                std::memcpy(o, v.data(), v.size() * sizeof(cplx));
+                            }
+                            std::vector<cplx>().swap(v);
+                        };
+                        put(n.Finv, d.off_F, d.s, d.s);
+                        put(n.L21, d.off_L, d.u, d.s);
+                        put(n.Uinv, d.off_U, d.s, d.s);
+                        put(n.Z, d.off_Z, d.s, d.u);
+                    }
+                };
+                const int nt = std::min(nthr, i1 - i0);
+                std::vector<std::thread> th;
+                for (int w = 1; w < nt; ++w) th.emplace_back(pack);
+                pack();
+                for (auto& x : th) x.join();
+                if (bytes)
+                    HTG_CUDA(cudaMemcpyAsync(static_cast<double2*>(facp) + base, dst, bytes, cudaMemcpyHostToDevice, st));
+                HTG_CUDA(cudaEventRecord(done[buf], st));
+                buf ^= 1;
+                i0 = i1;
+            }
+            for (int b = 0; b < 2; ++b) {
+                HTG_CUDA(cudaEventSynchronize(done[b]));
+                HTG_CUDA(cudaEventDestroy(done[b]));
+                HTG_CUDA(cudaFreeHost(stage[b]));
+            }
+            if (std::getenv("HTG_SETUP_TIMES"))
+                std::fprintf(stderr, "htg setup:     factor pack + copy       %8.3f s\n",
+                             std::chrono::duration<double>(std::chrono::steady_clock::now() - tp0).count());
         }
-        flush();
-        HTG_CUDA(cudaFreeHost(stage));
         args_.fac = static_cast<const double2*>(facp);
         args_.idx = up(idx, st);
         args_.gsrc = up(gsrc, st);
@@ -836,7 +856,12 @@ std::unique_ptr<CoarseSolver> make_nd_solver(const LatticeMatrix& A, cudaStream_
 }
 
 std::unique_ptr<CoarseSolver> make_coarse_solver(const HostProblem& hp, cudaStream_t st) {
-    return make_nd_solver(qsfem_lattice(hp), st);
+    const auto t0 = std::chrono::steady_clock::now();
+    const LatticeMatrix A = qsfem_lattice(hp);
+    if (std::getenv("HTG_SETUP_TIMES"))
+        std::fprintf(stderr, "htg setup:   coarse stencil matrix      %8.3f s\n",
+                     std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+    return make_nd_solver(A, st);
 }
 
 }  // namespace htg

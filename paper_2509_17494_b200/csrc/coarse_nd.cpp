@@ -58,7 +58,8 @@ std::vector<cplx> coarse_stencil(const HostProblem& hp) {
         }
         return d;
     };
-    for (int Y = 0; Y <= CY; ++Y)
+    auto rows_of = [&](int Y0, int Y1) {
+    for (int Y = Y0; Y < Y1; ++Y)
         for (int X = 0; X <= CX; ++X) {
             cplx* row = &A9[(size_t(Y) * (CX + 1) + X) * 9];
             if (cdir(X, Y)) {
@@ -97,6 +98,16 @@ std::vector<cplx> coarse_stencil(const HostProblem& hp) {
                     row[(dy + 1) * 3 + (dx + 1)] = s;
                 }
         }
+    };
+    // lattice rows are independent: split them over the host threads
+    const int nthr = nv < 100000 ? 1 : std::max(1, std::min(int(std::thread::hardware_concurrency()), CY + 1));
+    if (nthr == 1) {
+        rows_of(0, CY + 1);
+    } else {
+        std::vector<std::thread> th;
+        for (int w = 0; w < nthr; ++w) th.emplace_back(rows_of, (CY + 1) * w / nthr, (CY + 1) * (w + 1) / nthr);
+        for (auto& x : th) x.join();
+    }
     return A9;
 }
 
@@ -141,17 +152,24 @@ LatticeMatrix qsfem_lattice(const HostProblem& hp) {
     L.id.resize(nv);
     for (int i = 0; i < nv; ++i) L.id[i] = i;
     const std::vector<cplx> A9 = coarse_stencil(hp);
-    std::vector<std::vector<std::pair<int, cplx>>> rows(nv);
+    // CSR straight from the stencil: (dy, dx) ascending is column-ascending
+    L.rp.assign(size_t(nv) + 1, 0);
+    L.ci.reserve(size_t(nv) * 9);
+    L.v.reserve(size_t(nv) * 9);
     for (int Y = 0; Y < L.H; ++Y)
-        for (int X = 0; X < L.W; ++X)
+        for (int X = 0; X < L.W; ++X) {
             for (int dy = -1; dy <= 1; ++dy)
                 for (int dx = -1; dx <= 1; ++dx) {
                     const int WX = X + dx, WY = Y + dy;
                     if (WX < 0 || WX >= L.W || WY < 0 || WY >= L.H) continue;
                     const cplx a = A9[(size_t(Y) * L.W + X) * 9 + (dy + 1) * 3 + (dx + 1)];
-                    if (a != cplx(0.0)) rows[Y * L.W + X].push_back({WY * L.W + WX, a});
+                    if (a != cplx(0.0)) {
+                        L.ci.push_back(WY * L.W + WX);
+                        L.v.push_back(a);
+                    }
                 }
-    finish_csr(L, rows);
+            L.rp[size_t(Y) * L.W + X + 1] = int(L.ci.size());
+        }
     return L;
 }
 
@@ -414,18 +432,19 @@ void factor_node(NDTree& t, int id, const LatticeMatrix& A, std::vector<int>& rp
     cplx inv = 0.0;
     // thread 0: one pivot decision; false when the column was delayed (no update)
     auto decide = [&]() -> bool {
+        // squared moduli: the same decisions as on |.| (std::abs of a complex is a hypot call)
         int p = k;
-        double best = std::abs(Fm[size_t(k) * F + k]);
+        double best = std::norm(Fm[size_t(k) * F + k]);
         for (int i = k + 1; i < sN; ++i) {
-            const double a = std::abs(Fm[size_t(i) * F + k]);
+            const double a = std::norm(Fm[size_t(i) * F + k]);
             if (a > best) {
                 best = a;
                 p = i;
             }
         }
         double ringmax = 0.0;
-        for (int i = sN; i < F; ++i) ringmax = std::max(ringmax, std::abs(Fm[size_t(i) * F + k]));
-        if (best == 0.0 || best < pivtol * ringmax) {
+        for (int i = sN; i < F; ++i) ringmax = std::max(ringmax, std::norm(Fm[size_t(i) * F + k]));
+        if (best == 0.0 || best < pivtol * pivtol * ringmax) {
             if (u == 0) throw RuntimeError("coarse LU: singular root front (zero pivot)");
             --last;  // delay column k
             for (int i = 0; i < F; ++i) std::swap(Fm[size_t(i) * F + k], Fm[size_t(i) * F + last]);
@@ -503,24 +522,45 @@ void factor_node(NDTree& t, int id, const LatticeMatrix& A, std::vector<int>& rp
     n.L21.assign(size_t(r) * ke, cplx(0.0));
     for (int i = 0; i < r; ++i)
         for (int j = 0; j < ke; ++j) n.L21[size_t(i) * ke + j] = Fm[size_t(ke + i) * F + j];
-    // Finv = L11^-1 (the row permutation is folded into the front's row order)
+    // Finv = L11^-1 (the row permutation is folded into the front's row order) and
+    // Uinv = U11^-1, by rows: row i of the inverse is e_i minus a combination of the
+    // rows already computed (contiguous axpys); column blocks are independent, so a
+    // large front splits them over its thread team.
     n.Finv.assign(size_t(ke) * ke, cplx(0.0));
-    for (int c = 0; c < ke; ++c) {
-        n.Finv[size_t(c) * ke + c] = 1.0;
-        for (int i = c + 1; i < ke; ++i) {
-            cplx acc = 0.0;
-            for (int k2 = c; k2 < i; ++k2) acc += Fm[size_t(i) * F + k2] * n.Finv[size_t(k2) * ke + c];
-            n.Finv[size_t(i) * ke + c] = -acc;
-        }
-    }
     n.Uinv.assign(size_t(ke) * ke, cplx(0.0));
-    for (int c = ke - 1; c >= 0; --c) {
-        n.Uinv[size_t(c) * ke + c] = 1.0 / Fm[size_t(c) * F + c];
-        for (int i = c - 1; i >= 0; --i) {
-            cplx acc = 0.0;
-            for (int k2 = i + 1; k2 <= c; ++k2) acc += Fm[size_t(i) * F + k2] * n.Uinv[size_t(k2) * ke + c];
-            n.Uinv[size_t(i) * ke + c] = -acc / Fm[size_t(i) * F + i];
+    auto inv_cols = [&](int c0, int c1) {
+        for (int i = 0; i < ke; ++i) {  // unit lower: X[i][c] = [i == c] - sum_{k2 < i} L[i][k2] X[k2][c], c <= i
+            cplx* xi = &n.Finv[size_t(i) * ke];
+            const int ce = std::min(c1, i);
+            for (int k2 = c0; k2 < i; ++k2) {
+                const cplx l = Fm[size_t(i) * F + k2];
+                if (l == cplx(0.0)) continue;
+                const cplx* xk = &n.Finv[size_t(k2) * ke];
+                const int cb = std::min(ce, k2 + 1);  // row k2 is zero right of its diagonal
+                for (int c = c0; c < cb; ++c) xi[c] -= l * xk[c];
+            }
+            if (i >= c0 && i < c1) xi[i] = 1.0;
         }
+        for (int i = ke - 1; i >= 0; --i) {  // upper: X[i][c] = ([i == c] - sum_{k2 > i} U[i][k2] X[k2][c]) / U[i][i], c >= i
+            cplx* xi = &n.Uinv[size_t(i) * ke];
+            const int cs = std::max(c0, i);
+            for (int k2 = i + 1; k2 < c1; ++k2) {
+                const cplx uu = Fm[size_t(i) * F + k2];
+                if (uu == cplx(0.0)) continue;
+                const cplx* xk = &n.Uinv[size_t(k2) * ke];
+                for (int c = std::max(cs, k2); c < c1; ++c) xi[c] -= uu * xk[c];
+            }
+            if (i >= c0 && i < c1) xi[i] += 1.0;
+            const cplx dinv = 1.0 / Fm[size_t(i) * F + i];
+            for (int c = cs; c < c1; ++c) xi[c] *= dinv;
+        }
+    };
+    if (team > 1 && ke >= 128) {
+        std::vector<std::thread> th;
+        for (int w = 0; w < team; ++w) th.emplace_back(inv_cols, ke * w / team, ke * (w + 1) / team);
+        for (auto& x : th) x.join();
+    } else {
+        inv_cols(0, ke);
     }
     // Z = Uinv U12
     n.Z.assign(size_t(ke) * r, cplx(0.0));

@@ -80,3 +80,11 @@ inline __host__ __device__ long long dof_index(int nx, int ny, int p, int gx, in
 }
 
 }  // namespace htg
+
+// The mirror-symmetric (parity) path of the FDM subdomain kernel (k_fdm.cu) and its
+// host factors (fdm.cpp, HTG_FDM_SYM=1) are compiled only on request: the path halves
+// the DMMA work but was never faster (0.212 vs 0.216 ms at cfg4), and its code slows
+// the default path through the instruction cache (187.5 vs 196.5 us without / with it).
+#ifndef HTG_FDM_SYM_CODE
+#define HTG_FDM_SYM_CODE 0
+#endif

@@ -290,13 +290,13 @@ bool build_fdm(const HostProblem& hp, const Basis1D& b, double alpha_s, int ox, 
     Mat Vx, Vy;
     // mirror symmetry: both directions with an even number of cells and equal end
     // tags, U centred (the interior class of a uniform medium); opt-in with
-    // HTG_FDM_SYM=1: it halves the DMMA work but not the time at cfg4 (0.212 vs
+    // HTG_FDM_SYM=1 in a build with -DHTG_FDM_SYM_CODE=1: it halves the DMMA work but not the time at cfg4 (0.212 vs
     // 0.216 ms in the same run: the kernel is bound by shared-memory traffic, L1
     // at 71-77% of peak, not by the DMMA pipe), so the default keeps the generic
     // factors and their flop count.
     // (the kernel's parity path is written for p = 4, 6 x 6-cell Omega, 4 x 4-cell U)
     const char* sym_env = std::getenv("HTG_FDM_SYM");
-    const bool sym = (sym_env && sym_env[0] == '1') && p == 4 && c.onx == 6 && c.ony == 6 && c.unx == 4 && c.uny == 4 &&
+    const bool sym = HTG_FDM_SYM_CODE && (sym_env && sym_env[0] == '1') && p == 4 && c.onx == 6 && c.ony == 6 && c.unx == 4 && c.uny == 4 &&
                      sides[0] == sides[1] && sides[2] == sides[3] && 2 * c.ux + c.unx == c.onx &&
                      2 * c.uy + c.uny == c.ony;
     if (sym) {

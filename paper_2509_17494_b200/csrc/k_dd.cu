@@ -369,7 +369,11 @@ DDDevice upload_dd_impl(const DDSetup& dd, const HostProblem& hp, std::vector<vo
     // partition-of-unity combine table: every fine dof's staged values in subdomain order
     std::vector<int> srcmap(size_t(hp.ndof()), 0), bptr{0}, bsrc;
     {
-        std::vector<std::vector<int>> lists(size_t(hp.ndof()));
+        // counting sort of the (subdomain, U row) pairs by fine dof, subdomain order kept
+        const size_t nd = size_t(hp.ndof());
+        std::vector<int> start(nd + 1, 0);
+        std::vector<long long> pair_dof;
+        pair_dof.reserve(size_t(d.nsub) * nu_max);
         for (int s = 0; s < d.nsub; ++s) {
             const int ci = dd.sub_class[s];
             const DDClass& c = dd.classes[ci];
@@ -377,17 +381,28 @@ DDDevice upload_dd_impl(const DDSetup& dd, const HostProblem& hp, std::vector<vo
             for (int rI = 0; rI < c.nu; ++rI) {
                 const int lxy = locg[lo + c.umem[rI]];
                 const int gx = dd.sub_ox[s] * p + (lxy & 0xffff), gy = dd.sub_oy[s] * p + (lxy >> 16);
-                lists[size_t(dof_index(hp.nx, hp.ny, p, gx, gy))].push_back(s * nu_max + rI);
+                const long long di = dof_index(hp.nx, hp.ny, p, gx, gy);
+                pair_dof.push_back(di);
+                ++start[size_t(di) + 1];
             }
         }
-        for (size_t di = 0; di < lists.size(); ++di) {
-            const auto& li = lists[di];
-            if (li.empty()) throw RuntimeError("dd setup: fine dof outside every subdomain U");
-            if (li.size() == 1) {
-                srcmap[di] = li[0];
+        for (size_t di = 0; di < nd; ++di) start[di + 1] += start[di];
+        std::vector<int> flat(pair_dof.size()), fill(start.begin(), start.end() - 1);
+        {
+            size_t k = 0;
+            for (int s = 0; s < d.nsub; ++s) {
+                const int nu = dd.classes[dd.sub_class[s]].nu;
+                for (int rI = 0; rI < nu; ++rI) flat[size_t(fill[size_t(pair_dof[k++])]++)] = s * nu_max + rI;
+            }
+        }
+        for (size_t di = 0; di < nd; ++di) {
+            const int b0 = start[di], n = start[di + 1] - b0;
+            if (n == 0) throw RuntimeError("dd setup: fine dof outside every subdomain U");
+            if (n == 1) {
+                srcmap[di] = flat[size_t(b0)];
             } else {
                 srcmap[di] = -int(bptr.size());
-                bsrc.insert(bsrc.end(), li.begin(), li.end());
+                bsrc.insert(bsrc.end(), flat.begin() + b0, flat.begin() + b0 + n);
                 bptr.push_back(int(bsrc.size()));
             }
         }

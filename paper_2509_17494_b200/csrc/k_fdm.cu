@@ -255,6 +255,16 @@ struct Stage {
         }
     }
 
+    // dispatch with the operand role a compile-time constant
+    template <int N, bool SA, class Epi>
+    __device__ __forceinline__ void dispatch_sa(int nt, const double2 (&sf)[KS], const double (&ss)[KS], const int* mrow,
+                                                const int* tm, const int* tn, Epi& epi) const {
+        if constexpr (N >= 1) {
+            if (nt == N) run_stat<N, SA>(sf, ss, dat, mrow, tm, tn, epi);
+            else dispatch_sa<N - 1, SA>(nt, sf, ss, mrow, tm, tn, epi);
+        }
+    }
+
     // full 8-row tiles ST of the factor on DMMA, the last FR <= 2 factor rows
     // on the CUDA cores (a padded tile would be 7/8 or 6/8 zeros); likewise the
     // last DR <= 2 data rows (HTG_FDM_DR, default on: 50 = 6 x 8 + 2 data rows
@@ -562,6 +572,13 @@ constexpr int kTGW = HTG_FDM_TGW < kTG ? HTG_FDM_TGW : kTG;  // moving tiles in 
 #endif
 constexpr bool kPadF = HTG_FDM_PADF != 0, kPadD = HTG_FDM_PADD != 0;
 
+#ifndef HTG_FDM_DOT_UNROLL
+#define HTG_FDM_DOT_UNROLL 28
+#endif
+constexpr int kDotUnroll = HTG_FDM_DOT_UNROLL;  // unrolling of the remainder dot products (code size)
+
+// (the operand role as a template argument halves the product bodies per call site
+// but measured slower: 196.3 vs 185.8 us at cfg4)
 template <int LD, int KS, bool FTR>
 struct WStage {
     const double2* fac;  // FTR: factor row f, k at fac[k * LD + fo + f]; else fac[f * LD + k]
@@ -628,7 +645,7 @@ struct WStage {
             const double2* dr = dat + d * LD;
             const int sk = kSkew ? ((lane >> 1) & 3) : 0;  // consecutive lanes: consecutive rows
             double acc[2][4] = {};  // independent chains, as in Stage
-#pragma unroll
+#pragma unroll kDotUnroll
             for (int kk = 0; kk < 4 * KS; ++kk) {
                 const double2 a = fval(f, kk ^ sk), bb = dr[kk ^ sk];
                 double* c = acc[kk & 1];
@@ -645,19 +662,125 @@ struct WStage {
     }
 };
 
+// WStage with every extent a compile-time constant (the interior class of a
+// uniform medium: 96% of the subdomains at cfg4): factor rows F and data rows ND
+// of the form 8 t + 1 (full tiles only: no clamps, no output guards), contraction
+// length K, this warp's share PART of NP. After unrolling, the tile list of a warp
+// is straight-line code whose shared-memory addresses are a per-lane base plus
+// immediates, which frees the registers and integer work of the generic path.
+template <int N>
+struct IntC {
+    static constexpr int value = N;
+};
+template <int NP, class Fn>
+__device__ __forceinline__ void for_part(int part, Fn&& fn) {
+    if constexpr (NP == 1) {
+        fn(IntC<0>{});
+    } else if constexpr (NP == 2) {
+        if (part == 0) fn(IntC<0>{});
+        else fn(IntC<1>{});
+    } else if constexpr (NP == 3) {
+        if (part == 0) fn(IntC<0>{});
+        else if (part == 1) fn(IntC<1>{});
+        else fn(IntC<2>{});
+    } else {
+        if (part == 0) fn(IntC<0>{});
+        else if (part == 1) fn(IntC<1>{});
+        else if (part == 2) fn(IntC<2>{});
+        else fn(IntC<3>{});
+    }
+}
+
+template <int LD, int KS, bool FTR, int F, int ND, int K, bool SA, int NP>
+struct CStage {
+    const double2* fac;  // FTR: factor row f, k at fac[k * LD + fo + f]; else fac[f * LD + k]
+    int fo;
+    const double2* dat;  // data rows [0, ND), [row][k]
+    int lane;
+
+    __device__ __forceinline__ double2 fval(int f, int k) const {
+        return FTR ? fac[k * LD + fo + f] : fac[f * LD + k];
+    }
+
+    template <int PART, class Epi>
+    __device__ __forceinline__ void run(Epi&& epi) const {
+        constexpr int FR = F & 7, DR = ND & 7, FT = F - FR, DT = ND - DR;
+        static_assert(FR <= 2 && DR <= 2 && K <= 4 * KS, "CStage: extents 8 t + {0, 1, 2}");
+        constexpr int ST = FT / 8, OT = DT / 8, T = ST * OT, t0 = T * PART / NP, t1 = T * (PART + 1) / NP;
+        const Stage<LD, KS> b{fac, F, dat, ND, SA, 0, lane};
+        const int r = lane >> 2, kq = lane & 3;
+        const int pr = frow_perm(r);
+#pragma unroll
+        for (int st = 0; st < ST; ++st) {
+            const int lo = t0 - st * OT > 0 ? t0 - st * OT : 0, hi = t1 - st * OT < OT ? t1 - st * OT : OT;
+            if (lo < hi) {
+                double2 sf[KS];
+                double ss[KS];
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks) {
+                    sf[ks] = fval(st * 8 + pr, ks * 4 + kq);
+                    ss[ks] = stat_aux(sf[ks]);
+                }
+#pragma unroll
+                for (int o0 = lo; o0 < hi; o0 += kTGW) {
+                    const int nt = hi - o0 < kTGW ? hi - o0 : kTGW;
+                    int mrow[kTG], tm[kTG], tn[kTG];
+#pragma unroll
+                    for (int j = 0; j < kTG; ++j) {
+                        mrow[j] = ((o0 + j) * 8 + pr) * LD + kq;
+                        tm[j] = SA ? st : o0 + j;
+                        tn[j] = SA ? o0 + j : st;
+                    }
+                    b.template dispatch<kTGW>(nt, sf, ss, mrow, tm, tn, epi);
+                }
+            }
+        }
+        // remainder rows: factor rows [FT, F) x all data rows, then data rows [DT, ND) x
+        // the tiled factor rows; one complex dot of length K per lane
+        constexpr int n1 = FR * ND, n2 = DR * FT;
+#pragma unroll
+        for (int it0 = PART * 32; it0 < n1 + n2; it0 += NP * 32) {
+            const int it = it0 + lane;
+            if (it < n1 + n2) {
+                int f, d;
+                if (it < n1) {
+                    const int a = it / ND;
+                    f = FT + a;
+                    d = it - a * ND;
+                } else {
+                    const int j = it - n1, a = j / FT;
+                    d = DT + a;
+                    f = j - a * FT;
+                }
+                const double2* dr = dat + d * LD;
+                double acc[2][4] = {};
+#pragma unroll
+                for (int kk = 0; kk < K; ++kk) {
+                    const double2 a = fval(f, kk), bb = dr[kk];
+                    double* c = acc[kk & 1];
+                    c[0] = fma(a.x, bb.x, c[0]);
+                    c[1] = fma(a.y, bb.y, c[1]);
+                    c[2] = fma(a.x, bb.y, c[2]);
+                    c[3] = fma(a.y, bb.x, c[3]);
+                }
+                const double re = (acc[0][0] + acc[1][0]) - (acc[0][1] + acc[1][1]);
+                const double im = (acc[0][2] + acc[1][2]) + (acc[0][3] + acc[1][3]);
+                if (SA) epi(f, d, make_double2(re, im));
+                else epi(d, f, make_double2(re, im));
+            }
+        }
+    }
+};
+
 // CTA size the kernel is compiled for: NP = 1 at p = 4 runs 8 warps (shared
 // memory holds 8 buffer pairs), so the register budget is the full 255 per thread
 #ifndef HTG_FDM_TTHREADS
 #define HTG_FDM_TTHREADS 512
 #endif
-constexpr int kWThreads(int p, int np) { return (np == 1 && p == 4) ? 256 : (np == 2 && p == 4 ? HTG_FDM_TTHREADS : 512); }
 // CTA sizes the team kernel is instantiated for, per team size (the launch picks the
 // smallest one that holds the planned warps; the register budget follows the size)
 constexpr int kWSizes[5][2] = {{0, 0}, {256, 512}, {384, 512}, {480, 576}, {512, 512}};
 
-#ifndef HTG_FDM_SYM_CODE
-#define HTG_FDM_SYM_CODE 1  // 0: compile the team kernel without the mirror-symmetric path
-#endif
 #ifndef HTG_FDM_TEAM4_BELOW
 #define HTG_FDM_TEAM4_BELOW 40
 #endif
@@ -953,6 +1076,46 @@ __global__ void __launch_bounds__(NT, 1)
                 continue;
             }
         }
+#ifndef HTG_FDM_CONST
+#define HTG_FDM_CONST 1  // compile-time path (2-warp teams only: cfg4 187.5 -> 181.9 us; with the 3-warp
+                         // teams of cfg3 it is slower, 63.5 vs 61.4 us) for the 6 x 6-cell Omega / 4 x 4-cell U class at p = 4
+#endif
+        if constexpr (P == 4 && NP == 2 && HTG_FDM_CONST) {
+            if (nx == 25 && ny == 25 && nux == 17 && nuy == 17) {
+                const int ux0 = c.ux0, uy0 = c.uy0;
+                for (; cur < seg_end; cur += nteam) {
+                    const int id = pt.x;
+                    const bool more = cur + nteam < seg_end;
+                    if (more) pt = pos_tab[cur + nteam];
+                    asm volatile("cp.async.wait_all;\n" ::: "memory");
+                    team_sync<NP>(team);
+                    for_part<NP>(part, [&](auto pc) {
+                        CStage<LD, KS, false, 25, 25, 25, true, NP>{V1T, 0, X, lane}.template run<decltype(pc)::value>(
+                            [&](int m, int n, double2 v) { W[m * LD + n] = v; });
+                    });
+                    team_sync<NP>(team);
+                    for_part<NP>(NP - 1 - part, [&](auto pc) {
+                        CStage<LD, KS, false, 25, 25, 25, false, NP>{V2T, 0, W, lane}.template run<decltype(pc)::value>(
+                            [&](int m, int n, double2 v) {
+                                const double2 d = D[m * 25 + n];
+                                X[n * LD + m] = make_double2(v.x * d.x - v.y * d.y, v.x * d.y + v.y * d.x);
+                            });
+                    });
+                    team_sync<NP>(team);
+                    for_part<NP>(part, [&](auto pc) {
+                        CStage<LD, KS, true, 17, 25, 25, true, NP>{V1T, ux0, X, lane}.template run<decltype(pc)::value>(
+                            [&](int m, int n, double2 v) { W[m * LD + n] = v; });
+                    });
+                    team_sync<NP>(team);
+                    if (more) gather(pt.y);
+                    double2* yrow = ystage + (size_t)id * nu_max;
+                    for_part<NP>(NP - 1 - part, [&](auto pc) {
+                        CStage<LD, KS, true, 17, 17, 25, false, NP>{V2T, uy0, W, lane}.template run<decltype(pc)::value>(
+                            [&](int m, int n, double2 v) { yrow[urow[m * 17 + n]] = v; });
+                    });
+                }
+            }
+        }
         for (; cur < seg_end; cur += nteam) {
             const int id = pt.x;
             const bool more = cur + nteam < seg_end;
@@ -971,10 +1134,19 @@ __global__ void __launch_bounds__(NT, 1)
             team_sync<NP>(team);
             HTG_TR(3);
             // 2: Q[ix'][iy'] = (sum_iy P[ix'][iy] Vy[iy][iy']) Dinv[ix'][iy']  -> X[iy'][ix']
-            WStage<LD, KS, false>{V2T, ny, 0, W, nx, false, lane, NP - 1 - part, NP}([&](int m, int n, double2 v) {
+#ifndef HTG_FDM_EXP
+#define HTG_FDM_EXP 0  // timing experiments only (wrong results): 1 no Dinv, 2 no part flip, 3 untransposed store
+#endif
+            WStage<LD, KS, false>{V2T, ny, 0, W, nx, false, lane, HTG_FDM_EXP == 2 ? part : NP - 1 - part, NP}([&](int m, int n, double2 v) {
                 if (m < nx && n < ny) {
-                    const double2 d = D[m * ny + n];
-                    X[n * LD + m] = make_double2(v.x * d.x - v.y * d.y, v.x * d.y + v.y * d.x);
+                    if (HTG_FDM_EXP == 1) {
+                        X[n * LD + m] = v;
+                    } else {
+                        const double2 d = D[m * ny + n];
+                        const double2 o = make_double2(v.x * d.x - v.y * d.y, v.x * d.y + v.y * d.x);
+                        if (HTG_FDM_EXP == 3) X[m * LD + n] = o;
+                        else X[n * LD + m] = o;
+                    }
                 }
             });
             team_sync<NP>(team);
