@@ -114,7 +114,7 @@ constexpr bool kF4M = HTG_FDM_4M != 0;
 // as the transposed product with the factor as A (C'[factor][data]); only the
 // epilogue's index interpretation changes
 #ifndef HTG_FDM_SWAPB
-#define HTG_FDM_SWAPB 0
+#define HTG_FDM_SWAPB 1
 #endif
 constexpr bool kSwapB = HTG_FDM_SWAPB != 0;
 // the stationary operand's auxiliary value: Re + Im (3M) or -Im (4M, a sign flip
@@ -561,7 +561,7 @@ int fdm_rows(int fac_elems) {
 // transposed out of Vx^T, Vy^T (their rows are columns there), which leaves
 // shared memory for 8 teams of two 25-row buffers each at p = 4.
 #ifndef HTG_FDM_TGW
-#define HTG_FDM_TGW 3
+#define HTG_FDM_TGW 1  // cfg4 (with HTG_FDM_SWAPB): 1 tile 172.7 us, 2 tiles 176.6, 3 tiles 181.9
 #endif
 constexpr int kTGW = HTG_FDM_TGW < kTG ? HTG_FDM_TGW : kTG;  // moving tiles in flight (team kernel)
 #ifndef HTG_FDM_PADF
@@ -691,6 +691,9 @@ __device__ __forceinline__ void for_part(int part, Fn&& fn) {
     }
 }
 
+#ifndef HTG_FDM_DOTBAL
+#define HTG_FDM_DOTBAL 1
+#endif
 template <int LD, int KS, bool FTR, int F, int ND, int K, bool SA, int NP>
 struct CStage {
     const double2* fac;  // FTR: factor row f, k at fac[k * LD + fo + f]; else fac[f * LD + k]
@@ -737,9 +740,14 @@ struct CStage {
         }
         // remainder rows: factor rows [FT, F) x all data rows, then data rows [DT, ND) x
         // the tiled factor rows; one complex dot of length K per lane
+        // With two warps and an odd tile count (9 = 4 + 5) the warp with fewer tiles takes
+        // every dot product (a pass of 32 dots costs about 0.6 tiles of FP64 pipe time).
         constexpr int n1 = FR * ND, n2 = DR * FT;
+        constexpr bool kUneven = HTG_FDM_DOTBAL && NP == 2 && (T & 1);
+        constexpr bool kLight = (t1 - t0) * 2 < T;
+        constexpr int it_first = kUneven ? (kLight ? 0 : n1 + n2) : PART * 32, it_step = kUneven ? 32 : NP * 32;
 #pragma unroll
-        for (int it0 = PART * 32; it0 < n1 + n2; it0 += NP * 32) {
+        for (int it0 = it_first; it0 < n1 + n2; it0 += it_step) {
             const int it = it0 + lane;
             if (it < n1 + n2) {
                 int f, d;
@@ -892,8 +900,9 @@ __global__ void __launch_bounds__(256) k_fdm_format(const FdmClassDev* __restric
 template <int P, int NP, int NT>
 __global__ void __launch_bounds__(NT, 1)
     k_dd_fdm_w(FineGeom g, const FdmClassDev* __restrict__ classes, const int4* __restrict__ work,
-               const double2* __restrict__ image, const int2* __restrict__ pos_tab, const double2* __restrict__ r,
-               double2* __restrict__ ystage, int nu_max, int rows, int fac_elems) {
+               const __grid_constant__ FdmWorkTab wtab, const double2* __restrict__ image,
+               const int2* __restrict__ pos_tab, const double2* __restrict__ r, double2* __restrict__ ystage, int nu_max,
+               int rows, int fac_elems) {
     constexpr int LD = FdmDims<P>::LD, KS = FdmDims<P>::KS, KP = 4 * KS;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double2* fac = reinterpret_cast<double2*>(smem_raw);
@@ -910,7 +919,8 @@ __global__ void __launch_bounds__(NT, 1)
     double2* V1T = fac;            // [ix'][ix] = Vx[ix][ix'], KP rows (rows >= nx zero)
     double2* V2T = V1T + KP * LD;  // [iy'][iy] = Vy[iy][iy']
     double2* D = V2T + KP * LD;    // Dinv[ix'][iy']
-    const int4 wk = work[blockIdx.x];  // [first, end) of the class-sorted list, class of first
+    // [first, end) of the class-sorted list, class of first (parameter copy unless the table is too long)
+    const int4 wk = work ? work[blockIdx.x] : wtab.w[blockIdx.x];
     int pos = wk.x, ci = wk.z;
     // the class's factor region (formatted once by k_fdm_format) -> shared memory, asynchronously
     auto copy_image = [&](int cls) {
@@ -1207,8 +1217,8 @@ void dd_fdm_launch(const FineGeom& g, const FdmLaunch& L, const double2* r, doub
             HTG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
             attr_w[slot] = true;
         }
-        kern<<<L.nwork, L.nwarps * 32, L.smem, st>>>(g, L.classes, L.work, L.image, L.pos_tab, r, ystage, nu_max,
-                                                     L.rows, L.fac_elems);
+        kern<<<L.nwork, L.nwarps * 32, L.smem, st>>>(g, L.classes, L.nwork <= FdmWorkTab::kMax ? nullptr : L.work, L.tab,
+                                                     L.image, L.pos_tab, r, ystage, nu_max, L.rows, L.fac_elems);
     };
     if (L.nwarps > 0) {
         const bool small = L.nwarps * 32 <= kWSizes[L.team][0];
@@ -1308,6 +1318,7 @@ std::vector<int4> fdm_plan(std::vector<FdmClassDev>& cls, int p, int nsm, FdmLau
             work.push_back(make_int4(a, b, ci, 0));
         }
     }
+    for (size_t i = 0; i < work.size() && i < size_t(FdmWorkTab::kMax); ++i) L.tab.w[i] = work[i];
     return work;
 }
 

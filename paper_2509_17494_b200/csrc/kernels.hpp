@@ -113,6 +113,12 @@ struct FdmClassDev {
     int nsub;
     int first;          // offset of this class in the class-sorted subdomain list
 };
+// the team kernel's work table as a kernel parameter (constant bank: no global round
+// trip in front of the prologue) when it fits
+struct FdmWorkTab {
+    static constexpr int kMax = 152;
+    int4 w[kMax];
+};
 struct FdmLaunch {
     const FdmClassDev* classes;  // device copy of the class table
     const int4* work;            // per CTA: [first, end) of the class-sorted subdomain list
@@ -128,6 +134,7 @@ struct FdmLaunch {
     // the device once (fdm_format), so a CTA's prologue is one coalesced copy
     const double2* image = nullptr;
     const int2* pos_tab = nullptr;
+    FdmWorkTab tab{};            // host copy of the work table (nwork <= FdmWorkTab::kMax)
 };
 // fills L.image / L.pos_tab (L.classes, L.work uploaded; cls = the host copy of the table)
 void fdm_format(const std::vector<FdmClassDev>& cls, int p, FdmLaunch& L, std::vector<void*>& allocs, size_t& bytes,

@@ -16,6 +16,10 @@ full() {  # name regex what [skip]
       -o gpurun_out/prof_$1 -f python tools/run_once.py --what $3 --reps 2 > gpurun_out/ncu_$1.log 2>&1
 }
 full k_dd_fdm_w k_dd_fdm_w sweep
+# the same kernel at cfg3 (80 wavelengths: five 3-warp teams per SM)
+python tools/run_once.py --what sweep --reps 2 --wavelengths 80 > gpurun_out/plain_sweep_cfg3.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_dd_fdm_w -c 1 -o gpurun_out/prof_k_dd_fdm_w_cfg3 -f \
+    python tools/run_once.py --what sweep --reps 2 --wavelengths 80 > gpurun_out/ncu_k_dd_fdm_w_cfg3.log 2>&1
 full k1_cells k1_cells sweep
 full k_dd_combine k_dd_combine sweep
 full k1_restrict k1_cells step 2
