@@ -705,6 +705,46 @@ struct CStage {
         return FTR ? fac[k * LD + fo + f] : fac[f * LD + k];
     }
 
+    // Lean form for the 24-warp CTA (eight 3-warp teams, 80 registers): one tile at a
+    // time, the factor fragment re-read from shared memory at every k step instead of
+    // held in 42 registers across the tiles of a factor tile.
+    template <bool RSV, int PART, class Epi>
+    __device__ __forceinline__ void go(Epi&& epi) const {
+        if constexpr (RSV) run_rs<PART>(epi);
+        else run<PART>(epi);
+    }
+    template <int PART, class Epi>
+    __device__ __forceinline__ void run_rs(Epi&& epi) const {
+        constexpr int FR = F & 7, DR = ND & 7, FT = F - FR, DT = ND - DR;
+        constexpr int ST = FT / 8, OT = DT / 8, T = ST * OT, t0 = T * PART / NP, t1 = T * (PART + 1) / NP;
+        const int r = lane >> 2, kq = lane & 3, pr = frow_perm(r);
+        const double2* sp0 = FTR ? fac + kq * LD + fo + pr : fac + pr * LD + kq;
+        const double2* mp0 = dat + pr * LD + kq;
+        constexpr int SSTEP = FTR ? 4 * LD : 4, STILE = FTR ? 8 : 8 * LD;
+#pragma unroll
+        for (int t = t0; t < t1; ++t) {
+            const int st = t / OT, o = t - st * OT;
+            const double2* sp = sp0 + st * STILE;
+            const double2* mp = mp0 + o * 8 * LD;
+            double a1[2] = {0.0, 0.0}, a2[2] = {0.0, 0.0}, a3[2] = {0.0, 0.0};
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) {
+                const double2 sv = sp[ks * SSTEP], v = mp[ks * 4];
+                dmma(a1[0], a1[1], sv.x, v.x);
+                dmma(a2[0], a2[1], sv.y, v.y);
+                dmma(a3[0], a3[1], sv.x + sv.y, v.x + v.y);
+            }
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int f = st * 8 + pr, d = o * 8 + frow_perm(2 * kq + i);
+                const double2 val = make_double2(a1[i] - a2[i], a3[i] - a1[i] - a2[i]);
+                if (SA) epi(f, d, val);
+                else epi(d, f, val);
+            }
+        }
+        dots<PART, T, t0, t1>(epi);
+    }
+
     template <int PART, class Epi>
     __device__ __forceinline__ void run(Epi&& epi) const {
         constexpr int FR = F & 7, DR = ND & 7, FT = F - FR, DT = ND - DR;
@@ -738,6 +778,12 @@ struct CStage {
                 }
             }
         }
+        dots<PART, T, t0, t1>(epi);
+    }
+
+    template <int PART, int T, int t0, int t1, class Epi>
+    __device__ __forceinline__ void dots(Epi&& epi) const {
+        constexpr int FR = F & 7, DR = ND & 7, FT = F - FR, DT = ND - DR;
         // remainder rows: factor rows [FT, F) x all data rows, then data rows [DT, ND) x
         // the tiled factor rows; one complex dot of length K per lane
         // With two warps and an odd tile count (9 = 4 + 5) the warp with fewer tiles takes
@@ -788,6 +834,7 @@ struct CStage {
 // CTA sizes the team kernel is instantiated for, per team size (the launch picks the
 // smallest one that holds the planned warps; the register budget follows the size)
 constexpr int kWSizes[5][2] = {{0, 0}, {256, 512}, {384, 512}, {480, 576}, {512, 512}};
+constexpr int kWLean = 768;  // eight 3-warp teams, 80 registers (CStage::run_rs)
 
 #ifndef HTG_FDM_TEAM4_BELOW
 #define HTG_FDM_TEAM4_BELOW 40
@@ -1090,7 +1137,8 @@ __global__ void __launch_bounds__(NT, 1)
 #define HTG_FDM_CONST 1  // compile-time path (2-warp teams only: cfg4 187.5 -> 181.9 us; with the 3-warp
                          // teams of cfg3 it is slower, 63.5 vs 61.4 us) for the 6 x 6-cell Omega / 4 x 4-cell U class at p = 4
 #endif
-        if constexpr (P == 4 && NP == 2 && HTG_FDM_CONST) {
+        constexpr bool RS = NT > 576;  // 24 warps: 80 registers per thread
+        if constexpr (P == 4 && (NP == 2 || RS) && HTG_FDM_CONST) {
             if (nx == 25 && ny == 25 && nux == 17 && nuy == 17) {
                 const int ux0 = c.ux0, uy0 = c.uy0;
                 for (; cur < seg_end; cur += nteam) {
@@ -1100,12 +1148,12 @@ __global__ void __launch_bounds__(NT, 1)
                     asm volatile("cp.async.wait_all;\n" ::: "memory");
                     team_sync<NP>(team);
                     for_part<NP>(part, [&](auto pc) {
-                        CStage<LD, KS, false, 25, 25, 25, true, NP>{V1T, 0, X, lane}.template run<decltype(pc)::value>(
+                        CStage<LD, KS, false, 25, 25, 25, true, NP>{V1T, 0, X, lane}.template go<RS, decltype(pc)::value>(
                             [&](int m, int n, double2 v) { W[m * LD + n] = v; });
                     });
                     team_sync<NP>(team);
                     for_part<NP>(NP - 1 - part, [&](auto pc) {
-                        CStage<LD, KS, false, 25, 25, 25, false, NP>{V2T, 0, W, lane}.template run<decltype(pc)::value>(
+                        CStage<LD, KS, false, 25, 25, 25, false, NP>{V2T, 0, W, lane}.template go<RS, decltype(pc)::value>(
                             [&](int m, int n, double2 v) {
                                 const double2 d = D[m * 25 + n];
                                 X[n * LD + m] = make_double2(v.x * d.x - v.y * d.y, v.x * d.y + v.y * d.x);
@@ -1113,14 +1161,14 @@ __global__ void __launch_bounds__(NT, 1)
                     });
                     team_sync<NP>(team);
                     for_part<NP>(part, [&](auto pc) {
-                        CStage<LD, KS, true, 17, 25, 25, true, NP>{V1T, ux0, X, lane}.template run<decltype(pc)::value>(
+                        CStage<LD, KS, true, 17, 25, 25, true, NP>{V1T, ux0, X, lane}.template go<RS, decltype(pc)::value>(
                             [&](int m, int n, double2 v) { W[m * LD + n] = v; });
                     });
                     team_sync<NP>(team);
                     if (more) gather(pt.y);
                     double2* yrow = ystage + (size_t)id * nu_max;
                     for_part<NP>(NP - 1 - part, [&](auto pc) {
-                        CStage<LD, KS, true, 17, 17, 25, false, NP>{V2T, uy0, W, lane}.template run<decltype(pc)::value>(
+                        CStage<LD, KS, true, 17, 17, 25, false, NP>{V2T, uy0, W, lane}.template go<RS, decltype(pc)::value>(
                             [&](int m, int n, double2 v) { yrow[urow[m * 17 + n]] = v; });
                     });
                 }
@@ -1237,7 +1285,8 @@ void dd_fdm_launch(const FineGeom& g, const FdmLaunch& L, const double2* r, doub
                 break;
             case 35:
                 if (small) go_w(k_dd_fdm_w<4, 3, kWSizes[3][0]>, 9);
-                else go_w(k_dd_fdm_w<4, 3, kWSizes[3][1]>, 10);
+                else if (L.nwarps * 32 <= kWSizes[3][1]) go_w(k_dd_fdm_w<4, 3, kWSizes[3][1]>, 10);
+                else go_w(k_dd_fdm_w<4, 3, kWLean>, 11);
                 break;
             case 36: go_w(k_dd_fdm_w<4, 4, 512>, 5); break;
             default: throw InvalidArgument("FDM subdomain kernel: p must be 2 or 4");
@@ -1290,7 +1339,7 @@ std::vector<int4> fdm_plan(std::vector<FdmClassDev>& cls, int p, int nsm, FdmLau
         wfac = (wfac + 7) / 8 * 8;
         const int per_warp = 2 * ext * LD;
         int nt = (kSmemMax / int(sizeof(double2)) - wfac) / per_warp;  // teams (buffer pairs)
-        nt = std::min(nt, (p == 4 ? kWSizes[L.team][1] : (L.team == 3 ? 576 : 512)) / (32 * L.team));
+        nt = std::min(nt, (p == 4 ? (L.team == 3 ? kWLean : kWSizes[L.team][1]) : (L.team == 3 ? 576 : 512)) / (32 * L.team));
         if (L.team != 3 && nt * L.team >= 8) nt = (nt * L.team) / 4 * 4 / L.team;  // whole warps per SM sub-partition
         nt = std::min(nt, (ntk && std::atoi(ntk) >= 1) ? std::atoi(ntk) : nt_default);
         if (nt >= 1) {
