@@ -421,9 +421,9 @@ class NDSolver : public CoarseSolver {
         const auto t0 = std::chrono::steady_clock::now();
         nd_factor(A, t, env_int("HTG_ND_LEAF", 16), pt ? std::atof(pt) : 0.3);
         if (std::getenv("HTG_SETUP_TIMES"))
-            std::fprintf(stderr, "htg setup:   nested-dissection factor %8.3f s (%d fronts, max front %d)\n",
+            std::fprintf(stderr, "htg setup:   nested-dissection factor %8.3f s (%d fronts, %lld sharing factors, max front %d)\n",
                          std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(),
-                         int(t.nodes.size()), t.max_front);
+                         int(t.nodes.size()), t.shared, t.max_front);
         nv_ = t.nv;
         delayed_ = t.delayed;
         const auto t1 = std::chrono::steady_clock::now();
@@ -583,7 +583,7 @@ class NDSolver : public CoarseSolver {
     void upload(NDTree& t, cudaStream_t st) {
         const int nn = int(t.nodes.size());
         std::vector<NodeDev> nd(nn);
-        std::vector<int> idx;
+        std::vector<int> idx, owners;  // owners: nodes holding their own factor blocks
         long long fac_total = 0;
         int front_total = 0, contrib_total = 0, gsrc_total = 0;
         for (int i = 0; i < nn; ++i) {
@@ -591,14 +591,24 @@ class NDSolver : public CoarseSolver {
             NodeDev& d = nd[i];
             d.s = n.ke;
             d.u = n.F - n.ke;
-            d.off_F = fac_total;
-            fac_total += (long long)d.s * d.s;
-            d.off_L = fac_total;
-            fac_total += (long long)d.u * d.s;
-            d.off_U = fac_total;
-            fac_total += (long long)d.s * d.s;
-            d.off_Z = fac_total;
-            fac_total += (long long)d.s * d.u;
+            if (n.rep >= 0) {  // the representative's blocks (an earlier node)
+                const NodeDev& r = nd[size_t(n.rep)];
+                if (n.rep >= i || r.s != d.s || r.u != d.u) throw RuntimeError("coarse solve: bad shared front");
+                d.off_F = r.off_F;
+                d.off_L = r.off_L;
+                d.off_U = r.off_U;
+                d.off_Z = r.off_Z;
+            } else {
+                owners.push_back(i);
+                d.off_F = fac_total;
+                fac_total += (long long)d.s * d.s;
+                d.off_L = fac_total;
+                fac_total += (long long)d.u * d.s;
+                d.off_U = fac_total;
+                fac_total += (long long)d.s * d.s;
+                d.off_Z = fac_total;
+                fac_total += (long long)d.s * d.u;
+            }
             d.off_var = int(idx.size());
             idx.insert(idx.end(), n.cols.begin(), n.cols.begin() + n.ke);
             d.off_ring = int(idx.size());
@@ -655,17 +665,19 @@ class NDSolver : public CoarseSolver {
             auto node_end = [&](int i) { return nd[i].off_Z + (long long)nd[i].s * nd[i].u; };
             const int nthr = std::max(1, int(std::thread::hardware_concurrency()));
             int buf = 0;
-            for (int i0 = 0; i0 < nn;) {
-                const long long base = nd[i0].off_F;
+            const int no = int(owners.size());
+            for (int i0 = 0; i0 < no;) {
+                const long long base = nd[owners[i0]].off_F;
                 int i1 = i0 + 1;
-                while (i1 < nn && size_t(node_end(i1) - base) * sizeof(cplx) <= chunk) ++i1;
-                const size_t bytes = size_t(node_end(i1 - 1) - base) * sizeof(cplx);
+                while (i1 < no && size_t(node_end(owners[i1]) - base) * sizeof(cplx) <= chunk) ++i1;
+                const size_t bytes = size_t(node_end(owners[i1 - 1]) - base) * sizeof(cplx);
                 if (bytes > chunk) throw RuntimeError("coarse solve: a front's factors exceed the staging buffer");
                 HTG_CUDA(cudaEventSynchronize(done[buf]));  // the buffer's previous copy
                 cplx* dst = stage[buf];
                 std::atomic<int> next{i0};
                 auto pack = [&]() {
-                    for (int i; (i = next++) < i1;) {
+                    for (int oi; (oi = next++) < i1;) {
+                        const int i = owners[oi];
                         NDNode& n = t.nodes[i];
                         const NodeDev& d = nd[i];
                         const bool colmajor = d.s + d.u <= warpF;
@@ -744,7 +756,8 @@ class NDSolver : public CoarseSolver {
             const NodeDev& d = nd[i];
             Level& lv = lvs[k];
             const int F = d.s + d.u;
-            read_bytes_ += sizeof(double2) * (size_t(d.s) * (d.s + 1) + 2 * size_t(d.s) * d.u);
+            // bytes one solve has to fetch from HBM: shared blocks once (their owner's)
+            if (t.nodes[i].rep < 0) read_bytes_ += sizeof(double2) * (size_t(d.s) * (d.s + 1) + 2 * size_t(d.s) * d.u);
             if (F <= warpF) {
                 wp[k].push_back(d);
             } else if ((long long)d.s * F <= midData) {

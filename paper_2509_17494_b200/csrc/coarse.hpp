@@ -84,12 +84,24 @@ struct NDNode {
     std::vector<int> rows, cols;
     std::vector<int> rc;  // per front row: coarse vertex whose rhs entry is injected here, or -1
     std::vector<cplx> Finv, L21, Uinv, Z, S;  // factor blocks (host, freed after upload)
+    // Fronts of one depth whose assembled matrices are bit-identical (the boxes of a
+    // uniform medium away from the boundary) are factored once: rep >= 0 names the node
+    // holding the blocks (this node's are empty; its rows / cols / rc are its own, in the
+    // representative's pivot order). perm_r / perm_c: initial position of each final front
+    // row / column (kept by representatives for their sharers).
+    int rep = -1;
+    std::vector<int> perm_r, perm_c;
 };
+// the node holding n's factor blocks
+inline const NDNode& nd_blocks(const std::vector<NDNode>& nodes, const NDNode& n) {
+    return n.rep < 0 ? n : nodes[size_t(n.rep)];
+}
 struct NDTree {
     int W = 0, H = 0, q = 1, nv = 0;
     std::vector<NDNode> nodes;  // postorder: children before parents, root last
     int max_depth = 0;
     long long delayed = 0;  // pivots delayed to an ancestor (summed over nodes)
+    long long shared = 0;   // fronts that share another front's factor blocks
     int max_front = 0;
 };
 // Build and factor the tree. leaf_max: nodes per leaf box; pivtol: the

@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <exception>
 #include <functional>
+#include <map>
 #include <thread>
 
 #include "coarse.hpp"
@@ -366,8 +367,17 @@ void gemm_sub(int m, int n, int k, const cplx* A, const cplx* B, cplx* C, int nt
 // Pivoting restricted to one front cannot otherwise cope with the nearly
 // singular pivot blocks of boxes close to a Dirichlet resonance (Helmholtz),
 // and the growth it lets through costs ~cond * eps in backward error.
+// key of a front for sharing: two independent 64-bit mixes of (F, sN, nown) and the
+// bits of the assembled front matrix
+struct FrontKey {
+    unsigned long long a = 0, b = 0;
+    bool operator<(const FrontKey& o) const { return a != o.a ? a < o.a : b < o.b; }
+};
+
+// key != nullptr: assemble the front and return its key only (no elimination).
+// A sharer (n.rep >= 0) takes the representative's pivot order instead of factoring.
 void factor_node(NDTree& t, int id, const LatticeMatrix& A, std::vector<int>& rpos, std::vector<int>& cpos,
-                 double pivtol, int nthreads) {
+                 double pivtol, int nthreads, FrontKey* key = nullptr) {
     NDNode& n = t.nodes[id];
     std::vector<int> rows = n.vars, cols = n.vars;
     for (int c : n.children) {
@@ -378,10 +388,30 @@ void factor_node(NDTree& t, int id, const LatticeMatrix& A, std::vector<int>& rp
     const int nown = int(n.vars.size()), sN = int(rows.size()), u = int(n.ring.size()), F = sN + u;
     rows.insert(rows.end(), n.ring.begin(), n.ring.end());
     cols.insert(cols.end(), n.ring.begin(), n.ring.end());
+    if (!key && n.rep >= 0) {  // sharer: the representative's pivot order on this node's labels
+        const NDNode& rp = t.nodes[size_t(n.rep)];
+        n.sN = sN;
+        n.F = F;
+        n.ke = rp.ke;
+        n.rows.resize(F);
+        n.cols.resize(F);
+        for (int i = 0; i < F; ++i) {
+            n.rows[i] = rows[size_t(rp.perm_r[i])];
+            n.cols[i] = cols[size_t(rp.perm_c[i])];
+        }
+        n.rc.assign(F, -1);
+        for (int v : n.vars) cpos[v] = 0;
+        for (int i = 0; i < F; ++i)
+            if (cpos[n.rows[i]] == 0) n.rc[i] = n.rows[i];
+        for (int v : n.vars) cpos[v] = -1;
+        return;
+    }
     for (int i = 0; i < F; ++i) {
         rpos[rows[i]] = i;
         cpos[cols[i]] = i;
     }
+    std::vector<int> prow(F), pcol(F);  // initial position of each front row / column
+    for (int i = 0; i < F; ++i) prow[i] = pcol[i] = i;
     std::vector<cplx> Fm(size_t(F) * F, cplx(0.0));
     // original entries not assembled below: own-var rows against own and ring
     // columns, and ring rows against own columns (a delayed variable's
@@ -398,6 +428,7 @@ void factor_node(NDTree& t, int id, const LatticeMatrix& A, std::vector<int>& rp
     }
     for (int c : n.children) {
         NDNode& ch = t.nodes[c];
+        const std::vector<cplx>& chS = nd_blocks(t.nodes, ch).S;
         const int uc = ch.F - ch.ke;
         std::vector<int> rm(uc), cm(uc);
         for (int a = 0; a < uc; ++a) {
@@ -405,16 +436,40 @@ void factor_node(NDTree& t, int id, const LatticeMatrix& A, std::vector<int>& rp
             cm[a] = cpos[ch.cols[ch.ke + a]];
         }
         for (int a = 0; a < uc; ++a)
-            for (int b = 0; b < uc; ++b) Fm[size_t(rm[a]) * F + cm[b]] += ch.S[size_t(a) * uc + b];
+            for (int b = 0; b < uc; ++b) Fm[size_t(rm[a]) * F + cm[b]] += chS[size_t(a) * uc + b];
     }
     for (int i = 0; i < F; ++i) {
         rpos[rows[i]] = -1;
         cpos[cols[i]] = -1;
     }
+    if (key) {
+        unsigned long long h1 = 0x9E3779B97F4A7C15ull ^ (unsigned long long)F, h2 = 0xC2B2AE3D27D4EB4Full + (unsigned long long)sN;
+        auto mix = [&](unsigned long long x) {
+            h1 = (h1 ^ x) * 0x9E3779B97F4A7C15ull;
+            h1 ^= h1 >> 29;
+            h2 = (h2 + x) * 0xC2B2AE3D27D4EB4Full;
+            h2 ^= h2 >> 31;
+        };
+        mix((unsigned long long)nown);
+        const unsigned long long* w = reinterpret_cast<const unsigned long long*>(Fm.data());
+        for (size_t i = 0; i < Fm.size() * 2; ++i) mix(w[i]);
+        key->a = h1;
+        key->b = h2;
+        return;
+    }
 
-    // Elimination. Large fronts use a team of threads that lives for the whole
-    // front: thread 0 makes the pivot decision (search, delay, swap), then every
-    // thread updates its share of the rows below; two spin barriers per pivot.
+    // Elimination, right-looking by panels of kPanel pivot columns. Inside a panel
+    // a pivot's rank-1 update is applied at once to the panel's columns only (all
+    // rows below, so the next column's pivot test sees up-to-date entries); the
+    // columns right of the panel get the whole panel's update in one pass per row
+    // (the row segment stays in L1 over the panel's pivots; with one pivot at a
+    // time the trailing matrix of a 1200-row front streamed through memory once
+    // per pivot). A column that fails the pivot test ends its panel early: after
+    // the trailing update every column right of it is current, and it is swapped
+    // with the last candidate column. Large fronts use a team of threads that
+    // lives for the whole front: thread 0 factors the panel, every thread updates
+    // its share of the trailing rows; two spin barriers per panel.
+    constexpr int kPanel = 32;
     int k = 0, last = sN;  // columns [k, last) are still candidates
     const int team = (nthreads > 1 && F >= 192) ? nthreads : 1;
     std::atomic<int> bar_count{0}, bar_gen{0};
@@ -427,11 +482,9 @@ void factor_node(NDTree& t, int id, const LatticeMatrix& A, std::vector<int>& rp
             while (bar_gen.load(std::memory_order_acquire) == g) std::this_thread::yield();
         }
     };
-    bool done = false;
-    std::exception_ptr err;
-    cplx inv = 0.0;
-    // thread 0: one pivot decision; false when the column was delayed (no update)
-    auto decide = [&]() -> bool {
+    // pivot test of column k (current for all rows >= k): the row of the largest
+    // candidate, or -1 when the column has to be delayed
+    auto find_pivot = [&]() -> int {
         // squared moduli: the same decisions as on |.| (std::abs of a complex is a hypot call)
         int p = k;
         double best = std::norm(Fm[size_t(k) * F + k]);
@@ -444,46 +497,85 @@ void factor_node(NDTree& t, int id, const LatticeMatrix& A, std::vector<int>& rp
         }
         double ringmax = 0.0;
         for (int i = sN; i < F; ++i) ringmax = std::max(ringmax, std::norm(Fm[size_t(i) * F + k]));
-        if (best == 0.0 || best < pivtol * pivtol * ringmax) {
-            if (u == 0) throw RuntimeError("coarse LU: singular root front (zero pivot)");
-            --last;  // delay column k
-            for (int i = 0; i < F; ++i) std::swap(Fm[size_t(i) * F + k], Fm[size_t(i) * F + last]);
-            std::swap(cols[k], cols[last]);
-            return false;
-        }
-        if (p != k) {
-            std::swap_ranges(Fm.begin() + size_t(k) * F, Fm.begin() + size_t(k) * F + F, Fm.begin() + size_t(p) * F);
-            std::swap(rows[k], rows[p]);
-        }
-        inv = 1.0 / Fm[size_t(k) * F + k];
-        return true;
+        if (best == 0.0 || best < pivtol * pivtol * ringmax) return -1;
+        return p;
     };
-    auto elim = [&](int i0, int i1) {  // rows k + 1 + [i0, i1)
-        const cplx* rk = &Fm[size_t(k) * F];
-        for (int i = k + 1 + i0; i < k + 1 + i1; ++i) {
+    auto delay_column = [&]() {
+        if (u == 0) throw RuntimeError("coarse LU: singular root front (zero pivot)");
+        --last;  // delay column k
+        if (last != k)
+            for (int i = 0; i < F; ++i) std::swap(Fm[size_t(i) * F + k], Fm[size_t(i) * F + last]);
+        std::swap(cols[k], cols[last]);
+        std::swap(pcol[k], pcol[last]);
+    };
+    int k0 = 0, kend = 0;  // the open panel: pivots [k0, k), columns [k0, kend)
+    // thread 0: pivots of one panel; returns true when a column failed its test
+    auto panel = [&]() -> bool {
+        k0 = k;
+        kend = std::min(k0 + kPanel, last);
+        while (k < kend) {
+            const int p = find_pivot();
+            if (p < 0) return true;
+            if (p != k) {
+                std::swap_ranges(Fm.begin() + size_t(k) * F, Fm.begin() + size_t(k) * F + F, Fm.begin() + size_t(p) * F);
+                std::swap(rows[k], rows[p]);
+                std::swap(prow[k], prow[p]);
+            }
+            const cplx inv = 1.0 / Fm[size_t(k) * F + k];
+            const cplx* rk = &Fm[size_t(k) * F];
+            for (int i = k + 1; i < F; ++i) {
+                cplx* ri = &Fm[size_t(i) * F];
+                if (ri[k] == cplx(0.0)) continue;
+                const cplx l = ri[k] * inv;
+                ri[k] = l;
+                for (int j = k + 1; j < kend; ++j) ri[j] -= l * rk[j];
+            }
+            ++k;
+        }
+        return false;
+    };
+    // thread 0: the panel's own rows right of the panel (U12 of the panel), in pivot order
+    auto panel_rows = [&]() {
+        for (int q = k0 + 1; q < k; ++q) {
+            cplx* rq = &Fm[size_t(q) * F];
+            for (int q2 = k0; q2 < q; ++q2) {
+                const cplx l = rq[q2];
+                if (l == cplx(0.0)) continue;
+                const cplx* r2 = &Fm[size_t(q2) * F];
+                for (int j = kend; j < F; ++j) rq[j] -= l * r2[j];
+            }
+        }
+    };
+    // rows k + [i0, i1): minus the panel's multipliers times the panel's rows, columns [kend, F)
+    auto trailing = [&](int i0, int i1) {
+        for (int i = k + i0; i < k + i1; ++i) {
             cplx* ri = &Fm[size_t(i) * F];
-            if (ri[k] == cplx(0.0)) continue;
-            const cplx l = ri[k] * inv;
-            ri[k] = l;
-            for (int j = k + 1; j < F; ++j) ri[j] -= l * rk[j];
+            for (int q = k0; q < k; ++q) {
+                const cplx l = ri[q];
+                if (l == cplx(0.0)) continue;
+                const cplx* rq = &Fm[size_t(q) * F];
+                for (int j = kend; j < F; ++j) ri[j] -= l * rq[j];
+            }
         }
     };
     if (team == 1) {
         while (k < last) {
-            if (!decide()) continue;
-            elim(0, F - k - 1);
-            ++k;
+            const bool failed = panel();
+            if (k > k0 && kend < F) {
+                panel_rows();
+                trailing(0, F - k);
+            }
+            if (failed) delay_column();
         }
     } else {
-        bool piv = false;
+        bool done = false, failed = false;
+        std::exception_ptr err;
         auto worker = [&](int w) {
             for (;;) {
                 if (w == 0) {
                     try {
-                        piv = false;
-                        while (k < last && !(piv = decide())) {
-                        }
-                        done = k >= last;
+                        failed = panel();
+                        if (k > k0 && kend < F) panel_rows();
                     } catch (...) {
                         err = std::current_exception();
                         done = true;
@@ -491,16 +583,31 @@ void factor_node(NDTree& t, int id, const LatticeMatrix& A, std::vector<int>& rp
                 }
                 barrier();
                 if (done) return;
-                const int nrows = F - k - 1;
-                elim(nrows * w / team, nrows * (w + 1) / team);
+                if (k > k0 && kend < F) {
+                    const int nrows = F - k;
+                    trailing(nrows * w / team, nrows * (w + 1) / team);
+                }
                 barrier();
-                if (w == 0) ++k;
+                if (w == 0) {
+                    try {
+                        if (failed) delay_column();
+                    } catch (...) {
+                        err = std::current_exception();
+                        done = true;
+                    }
+                    if (k >= last) done = true;
+                }
+                barrier();
+                if (done) return;
             }
         };
-        std::vector<std::thread> th;
-        for (int w = 1; w < team; ++w) th.emplace_back(worker, w);
-        worker(0);
-        for (auto& x : th) x.join();
+        if (k >= last) done = true;
+        if (!done) {
+            std::vector<std::thread> th;
+            for (int w = 1; w < team; ++w) th.emplace_back(worker, w);
+            worker(0);
+            for (auto& x : th) x.join();
+        }
         if (err) std::rethrow_exception(err);
     }
     const int ke = k, r = F - ke;  // eliminated here / handed to the parent
@@ -574,6 +681,8 @@ void factor_node(NDTree& t, int id, const LatticeMatrix& A, std::vector<int>& rp
     }
     n.rows.swap(rows);
     n.cols.swap(cols);
+    n.perm_r.swap(prow);
+    n.perm_c.swap(pcol);
 }
 
 }  // namespace
@@ -590,26 +699,61 @@ void nd_factor(const LatticeMatrix& A, NDTree& t, int leaf_max, double pivtol) {
     std::vector<std::vector<int>> bydepth(t.max_depth + 1);
     for (int i = 0; i < int(t.nodes.size()); ++i) bydepth[t.nodes[i].depth].push_back(i);
     const bool times = std::getenv("HTG_ND_TIMES") != nullptr;
+    const char* share_env = std::getenv("HTG_ND_SHARE");
+    const bool share = !(share_env && share_env[0] == '0');
     for (int d = t.max_depth; d >= 0; --d) {
         const auto& ids = bydepth[d];
         const auto td0 = std::chrono::steady_clock::now();
         if (int(ids.size()) >= nthr) {
-            std::vector<std::thread> th;
-            std::vector<std::exception_ptr> errs(nthr);
-            std::atomic<int> next{0};
-            for (int w = 0; w < nthr; ++w)
-                th.emplace_back([&, w] {
-                    try {
-                        std::vector<int> rpos(nv, -1), cpos(nv, -1);
-                        for (int i; (i = next++) < int(ids.size());)
-                            factor_node(t, ids[i], A, rpos, cpos, pivtol, 1);
-                    } catch (...) {
-                        errs[w] = std::current_exception();
-                    }
+            // every thread takes fronts off a shared counter; fn(front index in list, scratch maps)
+            auto for_fronts = [&](const std::vector<int>& list, auto&& fn) {
+                std::vector<std::thread> th;
+                std::vector<std::exception_ptr> errs(nthr);
+                std::atomic<int> next{0};
+                for (int w = 0; w < nthr; ++w)
+                    th.emplace_back([&, w] {
+                        try {
+                            std::vector<int> rpos(nv, -1), cpos(nv, -1);
+                            for (int i; (i = next++) < int(list.size());) fn(i, rpos, cpos);
+                        } catch (...) {
+                            errs[w] = std::current_exception();
+                        }
+                    });
+                for (auto& x : th) x.join();
+                for (auto& e : errs)
+                    if (e) std::rethrow_exception(e);
+            };
+            // Fronts with bit-identical assembled matrices (same size, same pivot block)
+            // have identical factors: key every front, factor the first of each key,
+            // give the others its pivot order (HTG_ND_SHARE=0: factor every front).
+            std::vector<int> reps, sharers;
+            if (share) {
+                std::vector<FrontKey> keys(ids.size());
+                for_fronts(ids, [&](int i, std::vector<int>& rpos, std::vector<int>& cpos) {
+                    factor_node(t, ids[i], A, rpos, cpos, pivtol, 1, &keys[i]);
                 });
-            for (auto& x : th) x.join();
-            for (auto& e : errs)
-                if (e) std::rethrow_exception(e);
+                std::map<FrontKey, int> first;
+                for (size_t i = 0; i < ids.size(); ++i) {
+                    auto it = first.find(keys[i]);
+                    if (it == first.end()) {
+                        first.emplace(keys[i], ids[i]);
+                        reps.push_back(ids[i]);
+                    } else {
+                        t.nodes[size_t(ids[i])].rep = it->second;
+                        sharers.push_back(ids[i]);
+                    }
+                }
+                t.shared += (long long)sharers.size();
+            } else {
+                reps = ids;
+            }
+            for_fronts(reps, [&](int i, std::vector<int>& rpos, std::vector<int>& cpos) {
+                factor_node(t, reps[i], A, rpos, cpos, pivtol, 1);
+            });
+            if (!sharers.empty())
+                for_fronts(sharers, [&](int i, std::vector<int>& rpos, std::vector<int>& cpos) {
+                    factor_node(t, sharers[i], A, rpos, cpos, pivtol, 1);
+                });
         } else {  // fewer fronts than threads: all fronts at once, a thread team each
             const int per = std::max(1, nthr / std::max(1, int(ids.size())));
             std::vector<std::thread> th;
@@ -630,7 +774,9 @@ void nd_factor(const LatticeMatrix& A, NDTree& t, int leaf_max, double pivtol) {
         if (times) {
             int fmax = 0;
             for (int id : ids) fmax = std::max(fmax, t.nodes[id].F);
-            std::fprintf(stderr, "htg nd: depth %2d fronts %6d max F %5d  %.3f s\n", d, int(ids.size()), fmax,
+            int nshare = 0;
+            for (int id : ids) nshare += t.nodes[id].rep >= 0;
+            std::fprintf(stderr, "htg nd: depth %2d fronts %6d (%6d shared) max F %5d  %.3f s\n", d, int(ids.size()), nshare, fmax,
                          std::chrono::duration<double>(std::chrono::steady_clock::now() - td0).count());
         }
         for (int id : ids) {

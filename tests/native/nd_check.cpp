@@ -57,7 +57,7 @@ int nd_stencil(const htg_problem* prob, double* a9, long long cap) {
 
 // Factor and solve A_c x = rc for nrhs right-hand sides (interleaved complex),
 // applying the explicit blocks exactly as the GPU level kernels do.
-// stats: [delayed pivots, max front, live nodes, 0]
+// stats: [delayed pivots, max front, live nodes, fronts sharing another front's factors]
 static int nd_run(const htg::LatticeMatrix& A, int leaf, double pivtol, const double* rc, double* x, int nrhs,
                   double* stats) {
     try {
@@ -67,7 +67,7 @@ static int nd_run(const htg::LatticeMatrix& A, int leaf, double pivtol, const do
         stats[0] = double(t.delayed);
         stats[1] = t.max_front;
         stats[2] = double(t.nodes.size());
-        stats[3] = 0;
+        stats[3] = double(t.shared);
         const cplx* R = reinterpret_cast<const cplx*>(rc);
         cplx* X = reinterpret_cast<cplx*>(x);
         const int nn = int(t.nodes.size());
@@ -91,11 +91,11 @@ static int nd_run(const htg::LatticeMatrix& A, int leaf, double pivtol, const do
                 }
                 for (int k = 0; k < n.F; ++k) rpos[n.rows[k]] = -1;
                 std::vector<cplx> y(s);
-                matvec_sub(n.Finv, s, s, v.data(), y.data(), false);
+                matvec_sub(htg::nd_blocks(t.nodes, n).Finv, s, s, v.data(), y.data(), false);
                 for (int k = 0; k < s; ++k) Y[n.cols[k]] = y[k];
                 contrib[i].assign(v.begin() + s, v.end());
                 std::vector<cplx> ly(u);
-                matvec_sub(n.L21, u, s, y.data(), ly.data(), false);
+                matvec_sub(htg::nd_blocks(t.nodes, n).L21, u, s, y.data(), ly.data(), false);
                 for (int k = 0; k < u; ++k) contrib[i][k] -= ly[k];
             }
             for (int i = nn - 1; i >= 0; --i) {
@@ -104,8 +104,8 @@ static int nd_run(const htg::LatticeMatrix& A, int leaf, double pivtol, const do
                 std::vector<cplx> y1(s), x2(u), x1(s), z(s);
                 for (int k = 0; k < s; ++k) y1[k] = Y[n.cols[k]];
                 for (int k = 0; k < u; ++k) x2[k] = xo[n.cols[s + k]];
-                matvec_sub(n.Uinv, s, s, y1.data(), x1.data(), false);
-                if (u) matvec_sub(n.Z, s, u, x2.data(), z.data(), false);
+                matvec_sub(htg::nd_blocks(t.nodes, n).Uinv, s, s, y1.data(), x1.data(), false);
+                if (u) matvec_sub(htg::nd_blocks(t.nodes, n).Z, s, u, x2.data(), z.data(), false);
                 for (int k = 0; k < s; ++k) xo[n.cols[k]] = x1[k] - (u ? z[k] : cplx(0.0));
             }
         }
