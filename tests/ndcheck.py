@@ -51,7 +51,7 @@ def coarse_check(problem, rc, leaf=16, pivtol=0.1):
             for dx in (-1, 0, 1):
                 y += A[:, :, dy + 1, dx + 1] * X[1 + dy:CX + 2 + dy, 1 + dx:CX + 2 + dx]
         be.append(np.linalg.norm(y.ravel() - rc[r]) / np.linalg.norm(rc[r]))
-    stats = dict(delayed=int(st[0]), max_front=int(st[1]), nodes=int(st[2]))
+    stats = dict(delayed=int(st[0]), max_front=int(st[1]), nodes=int(st[2]), shared=int(st[3]))
     return x, max(be), stats
 
 

@@ -87,3 +87,30 @@ def test_fe_nd_solve(kw):
         for r in range(2):
             res = fe_apply(prob, q, alpha, x[r]) - b[r]
             assert np.linalg.norm(res) / np.linalg.norm(b[r]) < 1e-12, (q, st)
+
+
+def test_nd_shared_fronts_equal_unshared(monkeypatch):
+    """Fronts with bit-identical assembled matrices share one set of factor blocks
+    (uniform medium: most of the tree). The shared factorization must give the same
+    solution, bit for bit, as factoring every front (HTG_ND_SHARE=0), and still match the
+    oracle's coarse solve; a medium with a different k in every cell finds nothing to share
+    beyond chance and stays correct."""
+    kw = dict(order=4, wavelengths=16, ppw=10)  # 40 x 40 cells: 81 x 81 coarse vertices
+    prob = hb.build_problem(hb.ProblemSpec(**kw))
+    ses = po.Session(po.ProblemSpec(**kw), po.SolverConfig())
+    rc = _rhs(ses.coarse_ndof, 3, 1)
+    x1, be1, st1 = coarse_check(prob, rc)
+    monkeypatch.setenv("HTG_ND_SHARE", "0")
+    x0, be0, st0 = coarse_check(prob, rc)
+    monkeypatch.delenv("HTG_ND_SHARE")
+    assert st0["shared"] == 0 and st1["shared"] > st1["nodes"] // 2
+    assert np.array_equal(x0, x1)
+    assert be1 < 1e-13
+    ref = ses.coarse_solve(rc[0])
+    assert np.linalg.norm(x1[0] - ref) / np.linalg.norm(ref) < 1e-12
+    # heterogeneous medium
+    g = np.random.default_rng(11)
+    prob_h = hb.build_problem(hb.ProblemSpec(**kw))
+    prob_h.k_cells = prob_h.k_cells * g.uniform(0.9, 1.1, size=prob_h.k_cells.shape)
+    xh, beh, sth = coarse_check(prob_h, rc)
+    assert beh < 1e-12 and sth["shared"] < sth["nodes"] // 10
