@@ -691,6 +691,10 @@ __device__ __forceinline__ void for_part(int part, Fn&& fn) {
     }
 }
 
+#ifndef HTG_FDM_MERGE
+#define HTG_FDM_MERGE 1
+#endif
+constexpr bool kFdmMerge = HTG_FDM_MERGE != 0;
 #ifndef HTG_FDM_DOTBAL
 #define HTG_FDM_DOTBAL 1
 #endif
@@ -992,8 +996,16 @@ __global__ void __launch_bounds__(NT, 1)
         // bfn[r]: natural rows of reordered row r; ubn[n]: reordered rows of natural row n
         int* bfn = gpos + nx * ny;
         int* ubn = bfn + 32;
+        // Last round of the CTA's last segment with R < nteam subdomains left: the teams
+        // merge, g = nteam / R of them per subdomain (cfg3: 17 subdomains per SM are two
+        // rounds of eight 2-warp teams and one subdomain solved by all 16 warps instead of
+        // a third round run by one team), HTG_FDM_MERGE
+        const int nseg = seg_end - pos, full = nseg / nteam * nteam, Rl = nseg - full;
+        const int mg = (kFdmMerge && NP >= 2 && nteam <= 8 && !sym && Rl > 0 && seg_end == wk.y) ? nteam / Rl : 1;
+        const bool merge = mg >= 2;
+        const int main_end = merge ? pos + full : seg_end;  // subdomains of the team-per-subdomain rounds
         int cur = pos + team;
-        int2 pt = cur < seg_end ? pos_tab[cur] : make_int2(0, 0);  // (subdomain id, Omega origin)
+        int2 pt = cur < main_end ? pos_tab[cur] : make_int2(0, 0);  // (subdomain id, Omega origin)
         asm volatile("cp.async.wait_all;\n" ::: "memory");
         __syncthreads();
         const int nxy = nx * ny;
@@ -1012,13 +1024,13 @@ __global__ void __launch_bounds__(NT, 1)
             asm volatile("cp.async.commit_group;\n" ::: "memory");
         };
         HTG_TR(0);  // segment setup (factor image)
-        if (cur < seg_end) gather(pt.y);
+        if (cur < main_end) gather(pt.y);
         if constexpr (P == 4) {
             if (sym) {
                 constexpr double r2 = 0.70710678118654752440;
-                for (; cur < seg_end; cur += nteam) {
+                for (; cur < main_end; cur += nteam) {
                     const int id = pt.x;
-                    const bool more = cur + nteam < seg_end;
+                    const bool more = cur + nteam < main_end;
                     if (more) pt = pos_tab[cur + nteam];
                     asm volatile("cp.async.wait_all;\n" ::: "memory");
                     team_sync<NP>(team);
@@ -1141,9 +1153,9 @@ __global__ void __launch_bounds__(NT, 1)
         if constexpr (P == 4 && (NP == 2 || RS) && HTG_FDM_CONST) {
             if (nx == 25 && ny == 25 && nux == 17 && nuy == 17) {
                 const int ux0 = c.ux0, uy0 = c.uy0;
-                for (; cur < seg_end; cur += nteam) {
+                for (; cur < main_end; cur += nteam) {
                     const int id = pt.x;
-                    const bool more = cur + nteam < seg_end;
+                    const bool more = cur + nteam < main_end;
                     if (more) pt = pos_tab[cur + nteam];
                     asm volatile("cp.async.wait_all;\n" ::: "memory");
                     team_sync<NP>(team);
@@ -1174,9 +1186,9 @@ __global__ void __launch_bounds__(NT, 1)
                 }
             }
         }
-        for (; cur < seg_end; cur += nteam) {
+        for (; cur < main_end; cur += nteam) {
             const int id = pt.x;
-            const bool more = cur + nteam < seg_end;
+            const bool more = cur + nteam < main_end;
             if (more) pt = pos_tab[cur + nteam];  // next subdomain of the team, used at stage 4
             HTG_TR(1);
             asm volatile("cp.async.wait_all;\n" ::: "memory");
@@ -1224,6 +1236,52 @@ __global__ void __launch_bounds__(NT, 1)
                     if (m < nux && n < nuy) yrow[urow[m * nuy + n]] = v;
                 });
             HTG_TR(6);
+        }
+        if (merge) {
+            const int st = team / mg;  // merged team; works in the buffers of its first team
+            if (st < Rl) {
+                const int prt = (team - st * mg) * NP + part, npp = mg * NP;
+                double2* Xs = fac + fac_elems + size_t(st * mg) * 2 * rows * LD;
+                double2* Ws = Xs + rows * LD;
+                auto sbar = [&]() { asm volatile("bar.sync %0, %1;\n" ::"r"(9 + st), "r"(npp * 32) : "memory"); };
+                const int2 p2 = pos_tab[pos + full + st];
+                sbar();  // every member team is through its own rounds: the buffers are free
+                {
+                    const int ox = (p2.y & 0xffff) * P, oy = (p2.y >> 16) * P;
+                    if (c.goff) {
+                        const double2* rb = r + dof_index(g.nx, g.ny, P, ox, oy);
+                        for (int l = prt * 32 + lane; l < nxy; l += npp * 32) cp_async16(&Xs[gpos[l]], rb + gofs[l]);
+                    } else {
+                        for (int l = prt * 32 + lane; l < nxy; l += npp * 32) {
+                            const int iy = fdiv(l, inv_nx), ix = l - iy * nx;
+                            cp_async16(&Xs[iy * LD + ix], r + dof_index(g.nx, g.ny, P, ox + ix, oy + iy));
+                        }
+                    }
+                    asm volatile("cp.async.commit_group;\n" ::: "memory");
+                }
+                asm volatile("cp.async.wait_all;\n" ::: "memory");
+                sbar();
+                WStage<LD, KS, false>{V1T, nx, 0, Xs, ny, true, lane, prt, npp}([&](int m, int n, double2 v) {
+                    if (m < nx && n < ny) Ws[m * LD + n] = v;
+                });
+                sbar();
+                WStage<LD, KS, false>{V2T, ny, 0, Ws, nx, false, lane, npp - 1 - prt, npp}([&](int m, int n, double2 v) {
+                    if (m < nx && n < ny) {
+                        const double2 d = D[m * ny + n];
+                        Xs[n * LD + m] = make_double2(v.x * d.x - v.y * d.y, v.x * d.y + v.y * d.x);
+                    }
+                });
+                sbar();
+                WStage<LD, KS, true>{V1T, nux, c.ux0, Xs, ny, true, lane, prt, npp}([&](int m, int n, double2 v) {
+                    if (m < nux && n < ny) Ws[m * LD + n] = v;
+                });
+                sbar();
+                double2* yrow = ystage + (size_t)p2.x * nu_max;
+                WStage<LD, KS, true>{V2T, nuy, c.uy0, Ws, nux, false, lane, npp - 1 - prt, npp}(
+                    [&](int m, int n, double2 v) {
+                        if (m < nux && n < nuy) yrow[urow[m * nuy + n]] = v;
+                    });
+            }
         }
         asm volatile("cp.async.wait_all;\n" ::: "memory");
         pos = seg_end;
