@@ -691,8 +691,12 @@ __device__ __forceinline__ void for_part(int part, Fn&& fn) {
     }
 }
 
+// Merged last round (teams join on the R < nteam subdomains left): measured without
+// gain (cfg3 59.5 vs 59.0 us, cfg4 175.6 vs 172.6): a team's subdomain takes ~19,000
+// cycles alone and ~44,000 beside seven others, the merged round ~10,000 plus an
+// unprefetched gather, and the extra code slows the main rounds.
 #ifndef HTG_FDM_MERGE
-#define HTG_FDM_MERGE 1
+#define HTG_FDM_MERGE 0
 #endif
 constexpr bool kFdmMerge = HTG_FDM_MERGE != 0;
 #ifndef HTG_FDM_DOTBAL
