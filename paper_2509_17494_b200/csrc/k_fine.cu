@@ -1038,7 +1038,13 @@ __global__ void __launch_bounds__(KCCfg<P>::NT * kKCStreams, kKCCtasPerSM)
         else k1c_body<P, MODE, 2, DIR>(a, &tmu, &tmf, sm, ct, str);
     } else {
         const int ct = (w >> 1) * 32 + (threadIdx.x & 31);
-        if ((w & 1) == 0) k1c_body<P, MODE, 0, DIR>(a, &tmu, &tmf, sm, ct, str);
+        // HTG_KC_MIXGRP: the second pipeline swaps its groups' warps, so every scheduler
+        // hosts one warp of each group (group 1 carries 3 node rows, group 0 two)
+#ifndef HTG_KC_MIXGRP
+#define HTG_KC_MIXGRP 0
+#endif
+        const int gsel = (w & 1) ^ (HTG_KC_MIXGRP ? (str & 1) : 0);
+        if (gsel == 0) k1c_body<P, MODE, 0, DIR>(a, &tmu, &tmf, sm, ct, str);
         else k1c_body<P, MODE, 1, DIR>(a, &tmu, &tmf, sm, ct, str);
     }
 }
