@@ -653,7 +653,15 @@ class NDSolver : public CoarseSolver {
         // for cols_dot) and copied asynchronously, so packing overlaps the transfer
         // (one cudaMemcpy per block took seconds at cfg4: 4 blocks x 68k fronts; one
         // thread packing through one buffer 0.5 s).
-        {
+        // (on its own thread and stream: the solve plan below is built meanwhile)
+        std::exception_ptr pack_err;
+        int pack_dev = 0;
+        HTG_CUDA(cudaGetDevice(&pack_dev));
+        auto pack_all = [&]() {
+          try {
+            HTG_CUDA(cudaSetDevice(pack_dev));
+            cudaStream_t st = nullptr;  // shadows the caller's stream inside this thread
+            HTG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
             const auto tp0 = std::chrono::steady_clock::now();
             const size_t chunk = size_t(64) << 20;  // bytes
             cplx* stage[2] = {nullptr, nullptr};
@@ -713,10 +721,22 @@ class NDSolver : public CoarseSolver {
                 HTG_CUDA(cudaEventDestroy(done[b]));
                 HTG_CUDA(cudaFreeHost(stage[b]));
             }
+            HTG_CUDA(cudaStreamSynchronize(st));
+            cudaStreamDestroy(st);
             if (std::getenv("HTG_SETUP_TIMES"))
                 std::fprintf(stderr, "htg setup:     factor pack + copy       %8.3f s\n",
                              std::chrono::duration<double>(std::chrono::steady_clock::now() - tp0).count());
-        }
+          } catch (...) {
+            pack_err = std::current_exception();
+          }
+        };
+        std::thread pack_thread(pack_all);
+        struct PackJoin {  // joined on every path out of upload()
+            std::thread& t;
+            ~PackJoin() {
+                if (t.joinable()) t.join();
+            }
+        } pack_join{pack_thread};
         args_.fac = static_cast<const double2*>(facp);
         args_.idx = up(idx, st);
         args_.gsrc = up(gsrc, st);
@@ -846,6 +866,8 @@ class NDSolver : public CoarseSolver {
             ev_join_.push_back(e);
         }
         HTG_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+        pack_thread.join();
+        if (pack_err) std::rethrow_exception(pack_err);
         if (max_smem > 227 * 1024) throw InvalidArgument("coarse front too large for shared memory");
         // The attribute is process-global: always grant the opt-in maximum (it is a
         // permission, not a reservation), so handles of different sizes never lower
