@@ -13,6 +13,15 @@
 
 #include "coarse.hpp"
 
+// host AVX2 + FMA kernel of the trailing update (the product build passes
+// -march=x86-64-v3; HTG_ND_NOAVX keeps the scalar form; never in device code)
+#if defined(__AVX2__) && defined(__FMA__) && !defined(__CUDA_ARCH__) && !defined(HTG_ND_NOAVX)
+#include <immintrin.h>
+#define HTG_ND_AVX2 1
+#else
+#define HTG_ND_AVX2 0
+#endif
+
 namespace htg {
 
 // ------------------------------------------------------------------ QSFEM
@@ -548,7 +557,63 @@ void factor_node(NDTree& t, int id, const LatticeMatrix& A, std::vector<int>& rp
     };
     // rows k + [i0, i1): minus the panel's multipliers times the panel's rows, columns [kend, F)
     auto trailing = [&](int i0, int i1) {
-        for (int i = k + i0; i < k + i1; ++i) {
+        int i = k + i0;
+        const int iend = k + i1;
+#if HTG_ND_AVX2
+        // register-blocked form for wide updates: 2 rows x 8 columns of complex
+        // accumulators held over the panel's pivots (the row segments are loaded and
+        // stored once per panel instead of once per pivot, every panel row segment once
+        // per row pair), fused multiply-adds
+        if (F - kend >= 64) {
+            const double* base = reinterpret_cast<const double*>(Fm.data());
+            for (; i + 2 <= iend; i += 2) {
+                double* ra = reinterpret_cast<double*>(&Fm[size_t(i) * F]);
+                double* rb = reinterpret_cast<double*>(&Fm[size_t(i + 1) * F]);
+                int j = kend;
+                for (; j + 8 <= F; j += 8) {
+                    __m256d a0 = _mm256_loadu_pd(ra + 2 * j), a1 = _mm256_loadu_pd(ra + 2 * j + 4),
+                            a2 = _mm256_loadu_pd(ra + 2 * j + 8), a3 = _mm256_loadu_pd(ra + 2 * j + 12);
+                    __m256d b0 = _mm256_loadu_pd(rb + 2 * j), b1 = _mm256_loadu_pd(rb + 2 * j + 4),
+                            b2 = _mm256_loadu_pd(rb + 2 * j + 8), b3 = _mm256_loadu_pd(rb + 2 * j + 12);
+                    for (int q = k0; q < k; ++q) {
+                        const double* rq = base + 2 * (size_t(q) * F + j);
+                        const __m256d lar = _mm256_set1_pd(ra[2 * q]), lbr = _mm256_set1_pd(rb[2 * q]);
+                        const double ai = ra[2 * q + 1], bi = rb[2 * q + 1];
+                        const __m256d lai = _mm256_set_pd(-ai, ai, -ai, ai), lbi = _mm256_set_pd(-bi, bi, -bi, bi);
+                        __m256d v = _mm256_loadu_pd(rq), w = _mm256_permute_pd(v, 5);
+                        a0 = _mm256_fmadd_pd(lai, w, _mm256_fnmadd_pd(lar, v, a0));
+                        b0 = _mm256_fmadd_pd(lbi, w, _mm256_fnmadd_pd(lbr, v, b0));
+                        v = _mm256_loadu_pd(rq + 4), w = _mm256_permute_pd(v, 5);
+                        a1 = _mm256_fmadd_pd(lai, w, _mm256_fnmadd_pd(lar, v, a1));
+                        b1 = _mm256_fmadd_pd(lbi, w, _mm256_fnmadd_pd(lbr, v, b1));
+                        v = _mm256_loadu_pd(rq + 8), w = _mm256_permute_pd(v, 5);
+                        a2 = _mm256_fmadd_pd(lai, w, _mm256_fnmadd_pd(lar, v, a2));
+                        b2 = _mm256_fmadd_pd(lbi, w, _mm256_fnmadd_pd(lbr, v, b2));
+                        v = _mm256_loadu_pd(rq + 12), w = _mm256_permute_pd(v, 5);
+                        a3 = _mm256_fmadd_pd(lai, w, _mm256_fnmadd_pd(lar, v, a3));
+                        b3 = _mm256_fmadd_pd(lbi, w, _mm256_fnmadd_pd(lbr, v, b3));
+                    }
+                    _mm256_storeu_pd(ra + 2 * j, a0);
+                    _mm256_storeu_pd(ra + 2 * j + 4, a1);
+                    _mm256_storeu_pd(ra + 2 * j + 8, a2);
+                    _mm256_storeu_pd(ra + 2 * j + 12, a3);
+                    _mm256_storeu_pd(rb + 2 * j, b0);
+                    _mm256_storeu_pd(rb + 2 * j + 4, b1);
+                    _mm256_storeu_pd(rb + 2 * j + 8, b2);
+                    _mm256_storeu_pd(rb + 2 * j + 12, b3);
+                }
+                for (int r2 = 0; r2 < 2; ++r2) {  // columns left over
+                    cplx* ri = &Fm[size_t(i + r2) * F];
+                    for (int q = k0; q < k; ++q) {
+                        const cplx l = ri[q];
+                        const cplx* rq = &Fm[size_t(q) * F];
+                        for (int jj = j; jj < F; ++jj) ri[jj] -= l * rq[jj];
+                    }
+                }
+            }
+        }
+#endif
+        for (; i < iend; ++i) {
             cplx* ri = &Fm[size_t(i) * F];
             for (int q = k0; q < k; ++q) {
                 const cplx l = ri[q];
