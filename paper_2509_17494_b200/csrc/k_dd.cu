@@ -254,12 +254,13 @@ DDDevice upload_dd_impl(const DDSetup& dd, const HostProblem& hp, std::vector<vo
         in[6] = int(locg.size());
         in[7] = int(subs[ci].size());
         const size_t b0 = Bm.size();
-        if (!c.band) Bm.resize(b0 + size_t(rpad) * kpad, make_double2(0.0, 0.0));
+        const bool fdm_cls = c.fdm && fdm_supported(p, c.fdm_nx, c.fdm_ny);  // no dense B (setup.cpp)
+        if (!c.band && !fdm_cls) Bm.resize(b0 + size_t(rpad) * kpad, make_double2(0.0, 0.0));
         if (c.devB && !subs[ci].empty()) {  // B_c filled on the device (k_band.cu) from a band factor
             const int s0 = subs[ci][0];
             jobs.push_back({s0, dd.sub_ox[s0], dd.sub_oy[s0], c.onx, c.ony, &c.umem, ci, (long long)b0, kpad});
         }
-        for (int rI = 0; rI < (c.band || c.devB ? 0 : c.nu); ++rI)
+        for (int rI = 0; rI < (c.band || c.devB || fdm_cls ? 0 : c.nu); ++rI)
             for (int l = 0; l < c.nloc; ++l) {
                 const cplx v = c.B[size_t(rI) * c.nloc + l];
                 Bm[b0 + size_t(rI) * kpad + l] = make_double2(v.real(), v.imag());

@@ -526,6 +526,13 @@ DDSetup build_dd(const HostProblem& hp, const Basis1D& b, double alpha_s, int l_
                 if (isU[l]) c.umem.push_back(l);
             c.nu = int(c.umem.size());
             if (c.band || c.devB) return;  // factored on the device
+            // fast diagonalisation where the FDM kernel takes the class: its factors are
+            // checked against A by probing, and no dense inverse is formed
+            const char* fdm_env = std::getenv("HTG_FDM");
+            if (!(fdm_env && fdm_env[0] == '0') && fdm_supported(p, c.onx * p + 1, c.ony * p + 1)) {
+                c.fdm = build_fdm(hp, b, alpha_s, first[ci].ox, first[ci].oy, c, A);
+                if (c.fdm) return;
+            }
             // B = A^-1 [U, :] = (A^-T [:, U])^T: solve A^T X = E_U
             std::vector<cplx> At(size_t(n) * n);
             for (int i = 0; i < n; ++i)
@@ -536,11 +543,6 @@ DDSetup build_dd(const HostProblem& hp, const Basis1D& b, double alpha_s, int l_
             c.B.resize(size_t(c.nu) * n);
             for (int r = 0; r < c.nu; ++r)
                 for (int l = 0; l < n; ++l) c.B[size_t(r) * n + l] = X[size_t(l) * c.nu + r];
-            // fast diagonalisation only where the FDM kernel takes the class (its
-            // validation against B is O(|U| |Omega|^2), seconds for large Omega)
-            const char* fdm_env = std::getenv("HTG_FDM");
-            if (!(fdm_env && fdm_env[0] == '0') && fdm_supported(p, c.onx * p + 1, c.ony * p + 1))
-                c.fdm = build_fdm(hp, b, alpha_s, first[ci].ox, first[ci].oy, c);
         } catch (...) {
             errs[ci] = std::current_exception();
         }

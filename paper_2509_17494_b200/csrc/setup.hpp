@@ -88,7 +88,7 @@ struct DDClass {
     int fdm_nux = 0, fdm_nuy = 0;  // 1-D extent of U
     std::vector<cplx> Vx, Vy;      // (nx x nx), (ny x ny) row-major, columns are eigenvectors
     std::vector<cplx> Dinv;        // nx x ny
-    double fdm_err = 0.0;          // max |B_fdm - B| / max |B| over the class
+    double fdm_err = 0.0;          // forward-error estimate of the FDM solve on probe vectors (fdm.cpp)
     // mirror-symmetric classes (an even number of Omega cells per direction, equal
     // ends, U centred): the 1-D operators commute with the reflection R (a signed
     // permutation of the hierarchical dofs), so each direction splits into an even
@@ -112,7 +112,9 @@ struct DDClass {
 bool fdm_candidate(const HostProblem& hp, int ox, int oy, const DDClass& c);
 // Build the FDM factors of a class whose first subdomain's Omega starts at
 // cell (ox, oy); false if the class is not separable or fails validation.
-bool build_fdm(const HostProblem& hp, const Basis1D& b, double alpha_s, int ox, int oy, DDClass& c);
+// A: the assembled Omega operator (dense n x n, local dof order) the factors are checked against
+bool build_fdm(const HostProblem& hp, const Basis1D& b, double alpha_s, int ox, int oy, DDClass& c,
+               const std::vector<cplx>& A);
 struct DDSetup {
     int l_dd = 4;
     int nbx = 0, nby = 0;  // blocks per direction
