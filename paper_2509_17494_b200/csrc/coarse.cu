@@ -342,6 +342,44 @@ __global__ void __launch_bounds__(kCT) k_nd_bwd_warp(const NodeDev* __restrict__
     dev_bwd_warp(list, n, a, blockIdx.x, ws);
 }
 
+// The warp-tier bottom of a subtree branch in one launch per direction: a CTA owns the
+// sub-subtree below one front of the first all-warp-tier level and walks its levels
+// itself (deepest first going forward, root first going backward), a block barrier
+// between levels: the contributions / solution entries a level reads were written by
+// this CTA's previous level. Replaces one launch per level (HTG_ND_SUBTREE).
+constexpr int kSubLevels = 8;
+struct WarpSub {
+    int off[kSubLevels];  // per level below the root (0 = root level): first front of this CTA's list
+    int cnt[kSubLevels];
+    int nlev;
+};
+__global__ void __launch_bounds__(kCT) k_nd_fwd_sub(const NodeDev* __restrict__ list, const WarpSub* __restrict__ subs,
+                                                   NDArgs a) {
+    __shared__ double2 ws[(kCT / 32) * 2 * kWarpFMax];
+    const WarpSub s = subs[blockIdx.x];
+    for (int L = s.nlev - 1; L >= 0; --L) {
+        for (int it = 0; it * (kCT / 32) < s.cnt[L]; ++it) {
+            dev_fwd_warp(list + s.off[L], s.cnt[L], a, it, ws);
+            __syncwarp();
+        }
+        __threadfence_block();
+        __syncthreads();
+    }
+}
+__global__ void __launch_bounds__(kCT) k_nd_bwd_sub(const NodeDev* __restrict__ list, const WarpSub* __restrict__ subs,
+                                                   NDArgs a) {
+    __shared__ double2 ws[(kCT / 32) * 2 * kWarpFMax];
+    const WarpSub s = subs[blockIdx.x];
+    for (int L = 0; L < s.nlev; ++L) {
+        for (int it = 0; it * (kCT / 32) < s.cnt[L]; ++it) {
+            dev_bwd_warp(list + s.off[L], s.cnt[L], a, it, ws);
+            __syncwarp();
+        }
+        __threadfence_block();
+        __syncthreads();
+    }
+}
+
 // backward, CTA tasks (whole front for the CTA tier, row blocks for the large tier)
 __device__ __forceinline__ void dev_bwd(const Task& tk, const NDArgs& a, double2* smem) {
     const NodeDev& nd = tk.nd;
@@ -474,8 +512,15 @@ class NDSolver : public CoarseSolver {
         HTG_CUDA(cudaEventRecord(ev_fork_, st));
         for (int b = 1; b <= nb; ++b) {
             HTG_CUDA(cudaStreamWaitEvent(bst_[b - 1], ev_fork_, 0));
-            if (skip != 1)
-                for (int L = int(br_[b].size()) - 1; L >= 0; --L) fwd_level(br_[b][L], a, bst_[b - 1]);
+            if (skip != 1) {
+                const SubFused& sf = sub_[b];
+                int Ltop = int(br_[b].size());
+                if (sf.nroots > 0) {
+                    launch(k_nd_fwd_sub, sf.nroots, 0, bst_[b - 1], sf.list, sf.subs, a);
+                    Ltop = sf.Lw;
+                }
+                for (int L = Ltop - 1; L >= 0; --L) fwd_level(br_[b][L], a, bst_[b - 1]);
+            }
             HTG_CUDA(cudaEventRecord(ev_join_[b - 1], bst_[b - 1]));
         }
         for (int b = 1; b <= nb; ++b) HTG_CUDA(cudaStreamWaitEvent(st, ev_join_[b - 1], 0));
@@ -486,8 +531,12 @@ class NDSolver : public CoarseSolver {
         HTG_CUDA(cudaEventRecord(ev_fork_, st));
         for (int b = 1; b <= nb; ++b) {
             HTG_CUDA(cudaStreamWaitEvent(bst_[b - 1], ev_fork_, 0));
-            if (skip != 1)
-                for (int L = 0; L < int(br_[b].size()); ++L) bwd_level(br_[b][L], a, bst_[b - 1]);
+            if (skip != 1) {
+                const SubFused& sf = sub_[b];
+                const int Ltop = sf.nroots > 0 ? sf.Lw : int(br_[b].size());
+                for (int L = 0; L < Ltop; ++L) bwd_level(br_[b][L], a, bst_[b - 1]);
+                if (sf.nroots > 0) launch(k_nd_bwd_sub, sf.nroots, 0, bst_[b - 1], sf.list, sf.subs, a);
+            }
             HTG_CUDA(cudaEventRecord(ev_join_[b - 1], bst_[b - 1]));
         }
         for (int b = 1; b <= nb; ++b) HTG_CUDA(cudaStreamWaitEvent(st, ev_join_[b - 1], 0));
@@ -553,6 +602,13 @@ class NDSolver : public CoarseSolver {
     }
     // br_[0]: levels 0 .. split-1 (the top); br_[b]: the subtree of the b-th node at
     // the split depth, indexed by depth - split
+    // per branch: the fused warp-tier bottom (levels >= Lw of the branch), or nroots == 0
+    struct SubFused {
+        const NodeDev* list = nullptr;
+        const WarpSub* subs = nullptr;
+        int nroots = 0, Lw = 0;
+    };
+    std::vector<SubFused> sub_;
     std::vector<std::vector<Level>> br_;
     std::vector<cudaStream_t> bst_;
     std::vector<cudaEvent_t> ev_join_;
@@ -819,6 +875,48 @@ class NDSolver : public CoarseSolver {
                 max_smem = std::max({max_smem, lv.smem_mid, lv.smem_big, lv.smem_b});
                 br_[b][L] = lv;
             }
+        // fused warp-tier bottoms: per branch the first level from which every deeper level
+        // holds warp-tier fronts only; one CTA per front of that level
+        sub_.assign(size_t(nbranch) + 1, SubFused{});
+        if (env_int("HTG_ND_SUBTREE", 0) && split > 0) {
+            for (int b = 1; b <= nbranch; ++b) {
+                const int NLb = int(br_[b].size());
+                int Lw = NLb;
+                while (Lw > 0 && br_[b][Lw - 1].nmid == 0 && br_[b][Lw - 1].nf1 == 0 && br_[b][Lw - 1].nb == 0 &&
+                       br_[b][Lw - 1].nwarp > 0)
+                    --Lw;
+                Lw = std::max(Lw, NLb - std::min(kSubLevels, env_int("HTG_ND_SUBLEVELS", kSubLevels)));
+                if (NLb - Lw < 2) continue;
+                const int dep0 = split + Lw;
+                std::vector<NodeDev> list;
+                std::vector<WarpSub> subs;
+                for (int i = 0; i < nn; ++i) {
+                    if (branch[i] != b || t.nodes[i].depth != dep0) continue;
+                    WarpSub ws{};
+                    std::vector<int> cur{i};
+                    int L = 0;
+                    while (!cur.empty() && L < kSubLevels) {
+                        ws.off[L] = int(list.size());
+                        ws.cnt[L] = int(cur.size());
+                        std::vector<int> next;
+                        for (int id : cur) {
+                            list.push_back(nd[id]);
+                            next.insert(next.end(), t.nodes[id].children.begin(), t.nodes[id].children.end());
+                        }
+                        cur.swap(next);
+                        ++L;
+                    }
+                    if (!cur.empty()) throw RuntimeError("coarse solve: fused subtree deeper than expected");
+                    ws.nlev = L;
+                    subs.push_back(ws);
+                }
+                if (subs.empty()) continue;
+                sub_[b].list = up(list, st);
+                sub_[b].subs = up(subs, st);
+                sub_[b].nroots = int(subs.size());
+                sub_[b].Lw = Lw;
+            }
+        }
         // persistent solve: the same work lists merged over the branches, per depth
         if (env_int("HTG_ND_PERSIST", 0)) {
             std::vector<NDPhase> ph;
