@@ -1154,7 +1154,10 @@ __global__ void __launch_bounds__(NT, 1)
                          // teams of cfg3 it is slower, 63.5 vs 61.4 us) for the 6 x 6-cell Omega / 4 x 4-cell U class at p = 4
 #endif
         constexpr bool RS = NT > 576;  // 24 warps: 80 registers per thread
-        if constexpr (P == 4 && (NP == 2 || RS) && HTG_FDM_CONST) {
+#ifndef HTG_FDM_CONST3
+#define HTG_FDM_CONST3 0  // compile-time path also for 3-warp teams
+#endif
+        if constexpr (P == 4 && (NP == 2 || RS || (NP == 3 && HTG_FDM_CONST3)) && HTG_FDM_CONST) {
             if (nx == 25 && ny == 25 && nux == 17 && nuy == 17) {
                 const int ux0 = c.ux0, uy0 = c.uy0;
                 for (; cur < main_end; cur += nteam) {
