@@ -457,7 +457,7 @@ class NDSolver : public CoarseSolver {
         NDTree t;
         const char* pt = std::getenv("HTG_ND_PIVTOL");
         const auto t0 = std::chrono::steady_clock::now();
-        nd_factor(A, t, env_int("HTG_ND_LEAF", 16), pt ? std::atof(pt) : 0.3);
+        nd_factor(A, t, env_int("HTG_ND_LEAF", 36), pt ? std::atof(pt) : 0.3);
         if (std::getenv("HTG_SETUP_TIMES"))
             std::fprintf(stderr, "htg setup:   nested-dissection factor %8.3f s (%d fronts, %lld sharing factors, max front %d)\n",
                          std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(),
